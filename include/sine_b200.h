@@ -1,0 +1,138 @@
+/*
+ * sine_b200.h -- C ABI of the B200-native Sine stage-1 index and LCFU
+ * eviction engine (libsine_b200.so).
+ *
+ * Plain pointers and sizes only; no torch / CUDA types in the signatures
+ * (a stream is passed as `void*` = cudaStream_t).  Every call returns an
+ * int status; on failure `sine_last_error()` (thread-local) describes it.
+ *
+ * Reference interfaces each entry point replaces (semcache = the reference
+ * package at /root/reference/pkg/src/semcache):
+ *
+ *   sine_create / sine_destroy   ExactCosineIndex.__init__   index.py:54-62
+ *   sine_insert[_device]         ExactCosineIndex.insert     index.py:71-78
+ *                                (+ the SemanticElement columns LCFU reads,
+ *                                 model.py:85-110, engine.py:330-334)
+ *   sine_remove                  ExactCosineIndex.remove     index.py:80-92
+ *   sine_size / sine_ids         __len__ / ids()             index.py:64-69
+ *   sine_get_rows                snapshot_lines() rows       index.py:104-107
+ *   sine_query[_device]          ExactCosineIndex.query      index.py:94-102
+ *                                + _rank                     index.py:42-46
+ *                                (batched: B independent queries)
+ *   sine_update_meta             hit bookkeeping             engine.py:209-217
+ *   sine_expired                 _purge_expired_locked       engine.py:362-367
+ *   sine_select_victims          _victim_order_locked +      engine.py:369-383
+ *                                the pop-until-fits loops    engine.py:321-327,
+ *                                                            engine.py:353-359
+ */
+#ifndef SINE_B200_H
+#define SINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SINE_OK          0
+#define SINE_EINVAL      1  /* bad argument -> semcache ValidationError      */
+#define SINE_ECUDA       2  /* CUDA runtime / kernel failure                 */
+#define SINE_ENCCL       3  /* reserved (collectives live in the host layer) */
+#define SINE_ENOMEM      4  /* device or pinned-host allocation failed       */
+#define SINE_ENOTFOUND   5  /* unknown id       -> ValidationError           */
+#define SINE_EDUP        6  /* duplicate id     -> ValidationError           */
+#define SINE_ENORM       7  /* not L2-normalised / wrong dimension           */
+
+/* ---- sine_create flags --------------------------------------------------- */
+#define SINE_STORE_F32   0x1u  /* keep fp32 scan rows  (exact mode)          */
+#define SINE_STORE_BF16  0x2u  /* keep bf16 scan rows  (fast mode)           */
+#define SINE_STORE_META  0x4u  /* keep LCFU metadata columns (engine mode)   */
+
+/* ---- sine_query modes ------------------------------------------------------ */
+#define SINE_SCAN_F32      0x0u  /* fp32 rows, fp32 accumulation             */
+#define SINE_SCAN_BF16     0x1u  /* bf16 rows, fp32 accumulation             */
+#define SINE_RERANK_F64    0x10u /* re-score final candidates in fp64        */
+#define SINE_NO_NORM_CHECK 0x100u/* caller already validated (|norm-1|<=1e-6)*/
+#define SINE_SCAN_CUDA_CORE 0x200u /* force the CUDA-core streaming scan      */
+
+/* ---- eviction policies (CacheConfig.eviction_policy, model.py:15) -------- */
+#define SINE_POLICY_LCFU 0
+#define SINE_POLICY_LRU  1
+#define SINE_POLICY_LFU  2
+
+/* Per-element LCFU columns, structure-of-arrays, one entry per inserted id.
+ * log_* are the natural logs the reference multiplies (engine.py:43-46),
+ * evaluated on the HOST with libm so the device product is bit-exact:
+ *   log_freq = log(frequency + 1)          log_cost = log(cost*1000.0 + 1)
+ *   log_lat  = log(latency_ms + 1)         log_stat = log(staticity + 1)   */
+typedef struct sine_meta_cols {
+    const double  *log_freq, *log_cost, *log_lat, *log_stat;
+    const int64_t *frequency, *size_tokens;
+    const double  *created_at, *expiration_time, *last_access;
+} sine_meta_cols_t;
+
+typedef struct sine_index sine_index_t;
+
+const char *sine_last_error(void);
+int sine_version(void);
+int sine_device_count(int *n);
+
+int sine_create(int device, int64_t dim, uint32_t flags, int64_t reserve_rows,
+                sine_index_t **out);
+int sine_destroy(sine_index_t *h);
+int sine_reserve(sine_index_t *h, int64_t rows);
+
+/* rows: host float64 [n, dim] row-major.  meta may be NULL unless the
+ * index was created with SINE_STORE_META. */
+int sine_insert(sine_index_t *h, int64_t n, const int64_t *ids, const double *rows,
+                const sine_meta_cols_t *meta, uint32_t flags);
+/* Same, rows already in device memory (bulk load). */
+int sine_insert_device(sine_index_t *h, int64_t n, const int64_t *ids,
+                       const double *rows_dev, const sine_meta_cols_t *meta,
+                       uint32_t flags);
+int sine_remove(sine_index_t *h, int64_t n, const int64_t *ids);
+
+int sine_size(sine_index_t *h, int64_t *live, int64_t *slots);
+int sine_ids(sine_index_t *h, int64_t *out, int64_t cap, int64_t *n);
+int sine_get_rows(sine_index_t *h, int64_t n, const int64_t *ids, double *out);
+
+/* B queries, host float64 [B, dim].  Outputs (host): ids [B, k] (-1 padded),
+ * sims [B, k], counts [B].  Each query's result equals
+ * ExactCosineIndex.query(q, k, min_similarity) on the same snapshot. */
+int sine_query(sine_index_t *h, int64_t B, const double *q, int k, double min_sim,
+               uint32_t mode, int64_t *out_ids, double *out_sims, int32_t *out_counts);
+/* Same, all buffers in device memory, enqueued on `stream` (NULL = the
+ * handle's own stream).  Does not synchronise. */
+int sine_query_device(sine_index_t *h, int64_t B, const double *q_dev, int k,
+                      double min_sim, uint32_t mode, int64_t *ids_dev,
+                      double *sims_dev, int32_t *counts_dev, void *stream);
+
+int sine_update_meta(sine_index_t *h, int64_t n, const int64_t *ids,
+                     const double *log_freq, const int64_t *frequency,
+                     const double *last_access);
+/* Ids with expiration_time - now <= 0, ascending.  remove != 0 also
+ * tombstones them. */
+int sine_expired(sine_index_t *h, double now, int remove, int64_t *out,
+                 int64_t cap, int64_t *n);
+/* The shortest prefix of the (key, created_at, id)-ascending order whose
+ * size_tokens sum reaches `excess`, in order.  Not removed. */
+int sine_select_victims(sine_index_t *h, int policy, double now, int64_t excess,
+                        int64_t *out, int64_t cap, int64_t *n);
+
+/* Introspection for benchmarks: the handle's stream, and the device time
+ * (CUDA events on that stream) of the last query's scan and merge kernels
+ * and the last victim selection. */
+int sine_stream(sine_index_t *h, void **stream);
+int sine_set_timing(sine_index_t *h, int on);
+int sine_last_timing(sine_index_t *h, float *scan_ms, float *merge_ms, float *evict_ms);
+int sine_kernel_launches(sine_index_t *h, int64_t *n);
+
+int sine_host_alloc(size_t bytes, void **p);
+int sine_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINE_B200_H */

@@ -1,0 +1,1036 @@
+// libsine_b200 -- C ABI over the device SE store, the stage-1 kernels and the
+// eviction kernels.  See include/sine_b200.h for the contract and the
+// reference interfaces each entry point replaces.
+//
+// Device store (one per handle / GPU), structure-of-arrays in HBM:
+//   rows32 [cap][stride32] fp32     scan rows, exact mode   (128-B padded)
+//   rows16 [cap][stride16] bf16     scan rows, fast mode    (128-B padded)
+//   rows64 [cap][dim]      fp64     master copy: fp64 re-rank + snapshots
+//   ids    [cap] int64,  valid bitmap [cap/32] uint32
+//   LCFU columns (engine mode): log_freq/log_cost/log_lat/log_stat,
+//     created_at, expiration_time, last_access (fp64), frequency,
+//     size_tokens (int64)
+// Slots are append-only; removal clears the validity bit (tombstone) and
+// the store is compacted (order preserving) once tombstones exceed a
+// quarter of the live rows, mirroring the reference graph index's rebuild
+// rule (index.py:271).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/sine_b200.h"
+#include "common.cuh"
+#include "evict.cuh"
+#include "merge.cuh"
+#include "scan.cuh"
+
+using namespace sine;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+    g_err = msg;
+    throw Fail{code};
+}
+
+#define CK(x)                                                                                     \
+    do {                                                                                          \
+        cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess)                                                                    \
+            fail(e_ == cudaErrorMemoryAllocation ? SINE_ENOMEM : SINE_ECUDA,                       \
+                 std::string(#x) + ": " + cudaGetErrorString(e_));                                \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SINE_OK;
+    } catch (const Fail& e) {
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SINE_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SINE_ECUDA;
+    }
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t want) {
+        if (want <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, want * sizeof(T)));
+        n = want;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+template <typename T>
+struct HostBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t want) {
+        if (want <= n) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        CK(cudaMallocHost(&p, want * sizeof(T)));
+        n = want;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct sine_index {
+    int device = 0;
+    int num_sms = 148;
+    int64_t dim = 0;
+    uint32_t flags = 0;
+    int64_t stride32 = 0, stride16 = 0;  // elements per row
+    int64_t cap = 0, nslots = 0, nlive = 0;
+    bool ids_ascending = true;
+    int64_t max_id = INT64_MIN;
+
+    float* rows32 = nullptr;
+    __nv_bfloat16* rows16 = nullptr;
+    double* rows64 = nullptr;
+    int64_t* ids = nullptr;
+    uint32_t* valid = nullptr;
+    double *lf = nullptr, *lc = nullptr, *ll = nullptr, *ls = nullptr;
+    double *created = nullptr, *expiration = nullptr, *last_access = nullptr;
+    int64_t *freq = nullptr, *size = nullptr;
+
+    std::vector<int64_t> ids_h;   // by slot
+    std::vector<uint8_t> live_h;  // by slot
+    std::unordered_map<int64_t, int64_t> pos;
+
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    bool timing = false;
+    float t_scan = 0.f, t_merge = 0.f, t_evict = 0.f;
+    int64_t launches = 0;
+    std::mutex mu;
+
+    // workspaces
+    DevBuf<double> q64;
+    DevBuf<uint32_t> lkey;
+    DevBuf<int32_t> lslot, ln;
+    DevBuf<int64_t> o_ids;
+    DevBuf<double> o_sims;
+    DevBuf<int32_t> o_cnt;
+    DevBuf<uint64_t> k1;
+    DevBuf<uint64_t> vkeys;
+    DevBuf<int32_t> vslots, cand, scratch_i32;
+    DevBuf<int64_t> vids;
+    DevBuf<uint8_t> cub_tmp;
+    DevBuf<unsigned long long> hist;  // hw[256] hc[256] hand[3] hor[3] + counter
+    DevBuf<SelectState> st;
+    DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
+    HostBuf<SelectState> st_h;
+    HostBuf<unsigned long long> n_h;
+    HostBuf<int32_t> cnt_h;
+};
+
+namespace {
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+__global__ void convert_rows_kernel(const double* __restrict__ src, int64_t n, int64_t dim, float* rows32,
+                                    int64_t stride32, __nv_bfloat16* rows16, int64_t stride16) {
+    const int64_t width = max(stride32, stride16);
+    const int64_t total = n * width;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = t / width, c = t - r * width;
+        const double v = c < dim ? src[r * dim + c] : 0.0;
+        if (rows32 && c < stride32) rows32[r * stride32 + c] = static_cast<float>(v);
+        if (rows16 && c < stride16) rows16[r * stride16 + c] = __float2bfloat16_rn(static_cast<float>(v));
+    }
+}
+
+__global__ void set_bits_kernel(uint32_t* valid, const int64_t* slots, int64_t n, int set) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = slots[i];
+        const uint32_t bit = 1u << (s & 31);
+        if (set)
+            atomicOr(valid + (s >> 5), bit);
+        else
+            atomicAnd(valid + (s >> 5), ~bit);
+    }
+}
+
+__global__ void set_range_kernel(uint32_t* valid, int64_t s0, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = s0 + i;
+        atomicOr(valid + (s >> 5), 1u << (s & 31));
+    }
+}
+
+template <typename T>
+__global__ void gather_rows_kernel(const T* __restrict__ src, T* __restrict__ dst, const int64_t* from,
+                                   int64_t n, int64_t width) {
+    const int64_t total = n * width;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = t / width, c = t - r * width;
+        dst[r * width + c] = src[from[r] * width + c];
+    }
+}
+
+__global__ void scatter_meta_kernel(const int64_t* slots, int64_t n, const double* lfv, const int64_t* fv,
+                                    const double* lav, double* lf, int64_t* freq, double* la) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = slots[i];
+        lf[s] = lfv[i];
+        freq[s] = fv[i];
+        la[s] = lav[i];
+    }
+}
+
+int grid_for(int64_t work, int threads, int num_sms) {
+    const int64_t g = (work + threads - 1) / threads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 8ll * num_sms)));
+}
+
+template <typename T>
+void alloc_col(T*& p, int64_t n) {
+    CK(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(T)));
+}
+
+void grow(sine_index* h, int64_t want) {
+    if (want <= h->cap) return;
+    int64_t nc = std::max<int64_t>(want, std::max<int64_t>(1024, h->cap * 2));
+    nc = round_up(nc, 32);
+    auto move = [&](auto*& col, int64_t width) {
+        using T = std::remove_reference_t<decltype(*col)>;
+        if (!col && width >= 0) return;
+        T* nw = nullptr;
+        CK(cudaMalloc(&nw, nc * width * sizeof(T)));
+        if (h->nslots)
+            CK(cudaMemcpyAsync(nw, col, h->nslots * width * sizeof(T), cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaFree(col));
+        col = nw;
+    };
+    if (h->cap == 0) {
+        if (h->flags & SINE_STORE_F32) alloc_col(h->rows32, nc * h->stride32);
+        if (h->flags & SINE_STORE_BF16) alloc_col(h->rows16, nc * h->stride16);
+        alloc_col(h->rows64, nc * h->dim);
+        alloc_col(h->ids, nc);
+        alloc_col(h->valid, nc / 32);
+        CK(cudaMemsetAsync(h->valid, 0, nc / 32 * sizeof(uint32_t), h->stream));
+        if (h->flags & SINE_STORE_META) {
+            alloc_col(h->lf, nc), alloc_col(h->lc, nc), alloc_col(h->ll, nc), alloc_col(h->ls, nc);
+            alloc_col(h->created, nc), alloc_col(h->expiration, nc), alloc_col(h->last_access, nc);
+            alloc_col(h->freq, nc), alloc_col(h->size, nc);
+        }
+    } else {
+        move(h->rows32, h->stride32);
+        move(h->rows16, h->stride16);
+        move(h->rows64, h->dim);
+        move(h->ids, 1);
+        {
+            uint32_t* nv = nullptr;
+            CK(cudaMalloc(&nv, nc / 32 * sizeof(uint32_t)));
+            CK(cudaMemsetAsync(nv, 0, nc / 32 * sizeof(uint32_t), h->stream));
+            CK(cudaMemcpyAsync(nv, h->valid, h->cap / 32 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            CK(cudaFree(h->valid));
+            h->valid = nv;
+        }
+        if (h->flags & SINE_STORE_META) {
+            move(h->lf, 1), move(h->lc, 1), move(h->ll, 1), move(h->ls, 1);
+            move(h->created, 1), move(h->expiration, 1), move(h->last_access, 1);
+            move(h->freq, 1), move(h->size, 1);
+        }
+    }
+    h->cap = nc;
+    h->ids_h.reserve(nc);
+    h->live_h.reserve(nc);
+}
+
+void check_rows_host(const sine_index* h, int64_t n, const double* rows) {
+    for (int64_t i = 0; i < n; ++i) {
+        const double* r = rows + i * h->dim;
+        double ss = 0.0;
+        for (int64_t j = 0; j < h->dim; ++j) ss += r[j] * r[j];
+        const double nrm = std::sqrt(ss);
+        if (std::fabs(nrm - 1.0) > 1e-6) {
+            char b[128];
+            snprintf(b, sizeof b, "vector is not L2-normalized (norm=%.8f)", nrm);
+            fail(SINE_ENORM, b);
+        }
+    }
+}
+
+void check_new_ids(const sine_index* h, int64_t n, const int64_t* ids) {
+    std::unordered_set<int64_t> seen;
+    seen.reserve(n * 2);
+    for (int64_t i = 0; i < n; ++i) {
+        if (h->pos.count(ids[i]) || !seen.insert(ids[i]).second)
+            fail(SINE_EDUP, "duplicate id " + std::to_string(ids[i]));
+    }
+}
+
+void copy_meta(sine_index* h, int64_t s0, int64_t n, const sine_meta_cols_t* m) {
+    if (!(h->flags & SINE_STORE_META)) return;
+    if (!m) fail(SINE_EINVAL, "metadata columns required (index created with SINE_STORE_META)");
+    auto cp = [&](auto* dst, const auto* src) {
+        if (!src) fail(SINE_EINVAL, "null metadata column");
+        CK(cudaMemcpyAsync(dst + s0, src, n * sizeof(*src), cudaMemcpyHostToDevice, h->stream));
+    };
+    cp(h->lf, m->log_freq), cp(h->lc, m->log_cost), cp(h->ll, m->log_lat), cp(h->ls, m->log_stat);
+    cp(h->freq, m->frequency), cp(h->size, m->size_tokens), cp(h->created, m->created_at);
+    cp(h->expiration, m->expiration_time), cp(h->last_access, m->last_access);
+}
+
+void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bool rows_on_device,
+            const sine_meta_cols_t* meta) {
+    grow(h, h->nslots + n);
+    const int64_t s0 = h->nslots;
+    const cudaMemcpyKind kind = rows_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(h->rows64 + s0 * h->dim, rows, n * h->dim * sizeof(double), kind, h->stream));
+    const int64_t width = std::max(h->rows32 ? h->stride32 : 0, h->rows16 ? h->stride16 : 0);
+    if (width) {
+        convert_rows_kernel<<<grid_for(n * width, 256, h->num_sms), 256, 0, h->stream>>>(
+            h->rows64 + s0 * h->dim, n, h->dim, h->rows32 ? h->rows32 + s0 * h->stride32 : nullptr,
+            h->stride32, h->rows16 ? h->rows16 + s0 * h->stride16 : nullptr, h->stride16);
+        ++h->launches;
+    }
+    CK(cudaMemcpyAsync(h->ids + s0, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    copy_meta(h, s0, n, meta);
+    set_range_kernel<<<grid_for(n, 256, h->num_sms), 256, 0, h->stream>>>(h->valid, s0, n);
+    ++h->launches;
+    CK(cudaGetLastError());
+    for (int64_t i = 0; i < n; ++i) {
+        h->pos[ids[i]] = s0 + i;
+        h->ids_h.push_back(ids[i]);
+        h->live_h.push_back(1);
+        if (ids[i] <= h->max_id) h->ids_ascending = false;
+        h->max_id = std::max(h->max_id, ids[i]);
+    }
+    h->nslots += n;
+    h->nlive += n;
+    CK(cudaStreamSynchronize(h->stream));  // caller buffers may be released
+}
+
+void compact(sine_index* h) {
+    std::vector<int64_t> from;
+    from.reserve(h->nlive);
+    for (int64_t s = 0; s < h->nslots; ++s)
+        if (h->live_h[s]) from.push_back(s);
+    const int64_t n = static_cast<int64_t>(from.size());
+    DevBuf<int64_t> dfrom;
+    dfrom.ensure(std::max<int64_t>(n, 1));
+    CK(cudaMemcpyAsync(dfrom.p, from.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    auto redo = [&](auto*& col, int64_t width) {
+        using T = std::remove_reference_t<decltype(*col)>;
+        if (!col) return;
+        T* nw = nullptr;
+        CK(cudaMalloc(&nw, h->cap * width * sizeof(T)));
+        if (n)
+            gather_rows_kernel<T><<<grid_for(n * width, 256, h->num_sms), 256, 0, h->stream>>>(col, nw, dfrom.p, n,
+                                                                                               width);
+        ++h->launches;
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaFree(col));
+        col = nw;
+    };
+    redo(h->rows32, h->stride32);
+    redo(h->rows16, h->stride16);
+    redo(h->rows64, h->dim);
+    redo(h->ids, 1);
+    redo(h->lf, 1), redo(h->lc, 1), redo(h->ll, 1), redo(h->ls, 1);
+    redo(h->created, 1), redo(h->expiration, 1), redo(h->last_access, 1);
+    redo(h->freq, 1), redo(h->size, 1);
+    CK(cudaMemsetAsync(h->valid, 0, h->cap / 32 * sizeof(uint32_t), h->stream));
+    if (n) set_range_kernel<<<grid_for(n, 256, h->num_sms), 256, 0, h->stream>>>(h->valid, 0, n);
+    ++h->launches;
+    CK(cudaStreamSynchronize(h->stream));
+    std::vector<int64_t> nid(n);
+    for (int64_t i = 0; i < n; ++i) {
+        nid[i] = h->ids_h[from[i]];
+        h->pos[nid[i]] = i;
+    }
+    h->ids_h.swap(nid);
+    h->live_h.assign(n, 1);
+    h->nslots = n;
+    dfrom.release();
+}
+
+// ------------------------------------------------------------ query pipeline
+
+struct ScanCfg {
+    int C, CPW, CW, G, R, S, NQmax;
+    int64_t row_bytes;
+};
+
+ScanCfg scan_cfg(const sine_index* h, bool bf16) {
+    ScanCfg c{};
+    c.row_bytes = bf16 ? h->stride16 * 2 : h->stride32 * 4;
+    c.C = static_cast<int>((c.row_bytes + 511) / 512);
+    c.CPW = c.C <= 8 ? 1 : 2;
+    if (c.C > 16) fail(SINE_EINVAL, "dimension too large for the streaming scan (max 2048 fp32 / 4096 bf16)");
+    c.CW = (c.C + c.CPW - 1) / c.CPW;
+    c.G = std::max(1, 8 / c.CW);
+    c.R = 32;
+    while (c.R > 1 && c.R * c.row_bytes > 24576) c.R /= 2;
+    c.R = std::max(c.R, c.G);
+    const int epl = bf16 ? 8 : 4;
+    c.NQmax = std::min(16, 64 / (epl * c.CPW));
+    return c;
+}
+
+template <typename RowT, int NQ, int CPW>
+void launch_scan_t(const ScanParams& p, int grid, int threads, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(scan_kernel<RowT, NQ, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    scan_kernel<RowT, NQ, CPW><<<grid, threads, smem, st>>>(p);
+}
+
+template <typename RowT, int CPW>
+void launch_scan_nq(int NQ, const ScanParams& p, int grid, int threads, size_t smem, cudaStream_t st) {
+    switch (NQ) {
+        case 1: return launch_scan_t<RowT, 1, CPW>(p, grid, threads, smem, st);
+        case 2: return launch_scan_t<RowT, 2, CPW>(p, grid, threads, smem, st);
+        case 4: return launch_scan_t<RowT, 4, CPW>(p, grid, threads, smem, st);
+        case 8: return launch_scan_t<RowT, 8, CPW>(p, grid, threads, smem, st);
+        default:
+            if constexpr (sizeof(RowT) == 4 && CPW == 1) return launch_scan_t<RowT, 16, CPW>(p, grid, threads, smem, st);
+            fail(SINE_EINVAL, "unsupported query group");
+    }
+}
+
+void record(sine_index* h, int i, cudaStream_t st) {
+    if (h->timing) CK(cudaEventRecord(h->ev[i], st));
+}
+
+// tcgen05 path (large batches) -- not yet enabled
+bool umma_eligible(const sine_index*, int64_t, bool, uint32_t) { return false; }
+void umma_query(sine_index*, int64_t, const double*, int, int, float, double, bool, int64_t*, double*, int32_t*,
+                cudaStream_t) {
+    fail(SINE_EINVAL, "tensor-core path unavailable");
+}
+
+// Runs the full stage-1 pipeline for B device-resident queries.
+void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, double min_sim, uint32_t mode,
+                       int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+    if (k < 1) fail(SINE_EINVAL, "k must be >= 1");
+    if (B <= 0) return;
+    const bool bf16 = (mode & 0xF) == SINE_SCAN_BF16;
+    const bool rerank = (mode & SINE_RERANK_F64) != 0;
+    if (bf16 && !h->rows16) fail(SINE_EINVAL, "index has no bf16 rows (create with SINE_STORE_BF16)");
+    if (!bf16 && !h->rows32) fail(SINE_EINVAL, "index has no fp32 rows (create with SINE_STORE_F32)");
+    int kp = rerank ? k + kSlack : k;
+    if (kp > kMaxKp) {
+        if (k > kMaxKp) fail(SINE_EINVAL, "k > 128 is not supported by the device top-k");
+        kp = kMaxKp;
+    }
+    if (h->nlive == 0) {
+        CK(cudaMemsetAsync(counts_dev, 0, B * sizeof(int32_t), st));
+        CK(cudaMemsetAsync(ids_dev, 0xff, B * k * sizeof(int64_t), st));
+        CK(cudaMemsetAsync(sims_dev, 0, B * k * sizeof(double), st));
+        return;
+    }
+    // admission floor: exact threshold, or widened by the scan precision so
+    // the fp64 re-rank sees every row whose exact similarity passes
+    float thr0;
+    if (rerank) {
+        const double margin = bf16 ? 8e-3 : 1e-5;
+        thr0 = std::nextafter(static_cast<float>(min_sim - margin), -INFINITY);
+    } else {
+        thr0 = static_cast<float>(min_sim);
+        if (static_cast<double>(thr0) > min_sim) thr0 = std::nextafter(thr0, -INFINITY);
+    }
+
+    const bool use_umma = umma_eligible(h, B, bf16, mode);
+    if (use_umma) {
+        umma_query(h, B, q_dev, k, kp, thr0, min_sim, rerank, ids_dev, sims_dev, counts_dev, st);
+        return;
+    }
+
+    const ScanCfg c = scan_cfg(h, bf16);
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(h->num_sms, (h->nslots + c.R - 1) / c.R)));
+    const int64_t rows_per_cta = round_up((h->nslots + grid - 1) / grid, c.R);
+    h->lkey.ensure(static_cast<size_t>(grid) * c.NQmax * kp);
+    h->lslot.ensure(static_cast<size_t>(grid) * c.NQmax * kp);
+    h->ln.ensure(static_cast<size_t>(grid) * c.NQmax);
+
+    for (int64_t q0 = 0; q0 < B; q0 += c.NQmax) {
+        const int nq = static_cast<int>(std::min<int64_t>(c.NQmax, B - q0));
+        int NQ = 1;
+        while (NQ < nq) NQ <<= 1;
+        ScanParams p{};
+        p.rows = bf16 ? reinterpret_cast<const uint8_t*>(h->rows16) : reinterpret_cast<const uint8_t*>(h->rows32);
+        p.row_bytes = c.row_bytes;
+        p.nslots = h->nslots;
+        p.valid = h->valid;
+        p.ids = h->ids;
+        p.q64 = q_dev + q0 * h->dim;
+        p.dim = h->dim;
+        p.nq = nq;
+        p.kp = kp;
+        p.thr0 = thr0;
+        p.rows_per_stage = c.R;
+        p.rows_per_cta = rows_per_cta;
+        p.chunks = c.C;
+        p.chunk_warps = c.CW;
+        p.row_groups = c.G;
+        p.out_key = h->lkey.p;
+        p.out_slot = h->lslot.p;
+        p.out_n = h->ln.p;
+        // stages: fill ~200 KB of shared memory
+        const ScanSmemLayout L0 = scan_smem_layout(0, c.R, c.row_bytes, NQ, c.C, kp);
+        const size_t stage_bytes = static_cast<size_t>(c.R) * c.row_bytes;
+        int S = static_cast<int>(std::min<size_t>(8, (200 * 1024 - L0.total) / stage_bytes));
+        S = std::max(S, 2);
+        p.stages = S;
+        const ScanSmemLayout L = scan_smem_layout(S, c.R, c.row_bytes, NQ, c.C, kp);
+        if (L.total > 227 * 1024) fail(SINE_EINVAL, "scan shared-memory plan exceeds 227 KB");
+        const int threads = (c.CW * c.G + 1) * 32;
+        record(h, 0, st);
+        if (bf16) {
+            if (c.CPW == 1)
+                launch_scan_nq<__nv_bfloat16, 1>(NQ, p, grid, threads, L.total, st);
+            else
+                launch_scan_nq<__nv_bfloat16, 2>(NQ, p, grid, threads, L.total, st);
+        } else {
+            if (c.CPW == 1)
+                launch_scan_nq<float, 1>(NQ, p, grid, threads, L.total, st);
+            else
+                launch_scan_nq<float, 2>(NQ, p, grid, threads, L.total, st);
+        }
+        ++h->launches;
+        CK(cudaGetLastError());
+        record(h, 1, st);
+        MergeParams m{};
+        m.in_key = h->lkey.p;
+        m.in_slot = h->lslot.p;
+        m.in_n = h->ln.p;
+        m.ncta = grid;
+        m.nq = nq;
+        m.kp = kp;
+        m.ids = h->ids;
+        m.rows64 = h->rows64;
+        m.q64 = q_dev + q0 * h->dim;
+        m.dim = h->dim;
+        m.k = k;
+        m.min_sim = min_sim;
+        m.rerank = rerank ? 1 : 0;
+        m.out_ids = ids_dev + q0 * k;
+        m.out_sims = sims_dev + q0 * k;
+        m.out_counts = counts_dev + q0;
+        merge_kernel<<<nq, kMergeThreads, 0, st>>>(m);
+        ++h->launches;
+        CK(cudaGetLastError());
+        record(h, 2, st);
+    }
+}
+
+void check_queries_host(const sine_index* h, int64_t B, const double* q) {
+    for (int64_t b = 0; b < B; ++b) {
+        const double* r = q + b * h->dim;
+        double ss = 0.0;
+        for (int64_t j = 0; j < h->dim; ++j) ss += r[j] * r[j];
+        const double nrm = std::sqrt(ss);
+        if (std::fabs(nrm - 1.0) > 1e-6) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "vector is not L2-normalized (norm=%.8f)", nrm);
+            fail(SINE_ENORM, buf);
+        }
+    }
+}
+
+// ------------------------------------------------------------ eviction driver
+
+EvictCols evict_cols(const sine_index* h) {
+    EvictCols c{};
+    c.lf = h->lf, c.lc = h->lc, c.ll = h->ll, c.ls = h->ls;
+    c.created = h->created, c.expiration = h->expiration, c.last_access = h->last_access;
+    c.freq = h->freq, c.size = h->size, c.ids = h->ids, c.valid = h->valid;
+    c.nslots = h->nslots;
+    return c;
+}
+
+struct KeyDecomposer {
+    __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&, uint64_t&> operator()(Key3& k) const {
+        return {k.a, k.b, k.c};
+    }
+};
+
+void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, std::vector<int64_t>& out) {
+    out.clear();
+    if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata (SINE_STORE_META)");
+    if (excess <= 0 || h->nlive == 0) return;
+    cudaStream_t st = h->stream;
+    record(h, 3, st);
+    h->k1.ensure(std::max<int64_t>(h->cap, 1));
+    h->hist.ensure(256 * 2 + 6 + 2);
+    h->st.ensure(1);
+    h->st_h.ensure(1);
+    h->n_h.ensure(1);
+    unsigned long long* hw = h->hist.p;
+    unsigned long long* hc = hw + 256;
+    unsigned long long* hand = hc + 256;
+    unsigned long long* hor = hand + 3;
+    unsigned long long* counter = hor + 3;
+    CK(cudaMemsetAsync(hw, 0, 512 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(hand, 0xff, 3 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(hor, 0, 3 * sizeof(unsigned long long), st));
+    SelectState s0{};
+    s0.rem = excess;
+    s0.count = h->nlive;
+    *h->st_h.p = s0;
+    CK(cudaMemcpyAsync(h->st.p, h->st_h.p, sizeof(SelectState), cudaMemcpyHostToDevice, st));
+
+    const EvictCols cols = evict_cols(h);
+    const int64_t cand_max = std::max<int64_t>(1 << 20, h->nlive / 8);
+    const int32_t* cand = nullptr;
+    int64_t ncand = 0;
+    bool first = true;
+    const int grid_all = grid_for(h->nslots, 256, h->num_sms);
+    for (int pass = 0; pass < 25; ++pass) {
+        HistArgs a{};
+        a.c = cols;
+        a.policy = policy;
+        a.now = now;
+        a.cand = cand;
+        a.ncand = ncand;
+        a.k1 = h->k1.p;
+        a.first = first ? 1 : 0;
+        a.st = h->st.p;
+        a.hw = hw, a.hc = hc, a.hand = hand, a.hor = hor;
+        const int g = cand ? grid_for(ncand, 256, h->num_sms) : grid_all;
+        evict_hist_kernel<<<g, 256, 0, st>>>(a);
+        evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, first ? 1 : 0);
+        h->launches += 2;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->st_h.p, h->st.p, sizeof(SelectState), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        first = false;
+        const SelectState s = *h->st_h.p;
+        if (s.done) break;
+        if (!cand && s.count <= cand_max) {
+            // shrink the working set to the slots that match the prefix
+            h->cand.ensure(s.count);
+            CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+            CollectArgs ca{};
+            ca.c = cols;
+            ca.k1 = h->k1.p;
+            ca.st = h->st.p;
+            ca.mode = 1;
+            ca.out_slot = h->cand.p;
+            ca.out_n = counter;
+            ca.cap = s.count;
+            evict_collect_kernel<<<grid_all, 256, 0, st>>>(ca);
+            ++h->launches;
+            CK(cudaGetLastError());
+            cand = h->cand.p;
+            ncand = s.count;
+        }
+    }
+    // collect victims (key prefix <= T) and order them
+    const SelectState s = *h->st_h.p;
+    const int64_t vmax = s.done == 2 ? h->nlive : h->nlive;  // upper bound
+    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+    h->vkeys.ensure(3 * std::max<int64_t>(vmax, 1));
+    h->vslots.ensure(std::max<int64_t>(vmax, 1));
+    CollectArgs ca{};
+    ca.c = cols;
+    ca.k1 = h->k1.p;
+    ca.st = h->st.p;
+    ca.mode = 0;
+    ca.out_k = h->vkeys.p;
+    ca.out_slot = h->vslots.p;
+    ca.out_n = counter;
+    ca.cap = vmax;
+    evict_collect_kernel<<<grid_all, 256, 0, st>>>(ca);
+    ++h->launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->n_h.p, counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t V = static_cast<int64_t>(*h->n_h.p);
+    h->vids.ensure(std::max<int64_t>(V, 1));
+    if (V <= 2048) {
+        evict_small_sort_kernel<<<1, 1024, 3 * V * sizeof(uint64_t), st>>>(h->vkeys.p, h->vslots.p, h->ids,
+                                                                          static_cast<int>(V), h->vids.p);
+        ++h->launches;
+        CK(cudaGetLastError());
+    } else {
+        Key3* keys_in = reinterpret_cast<Key3*>(h->vkeys.p);
+        DevBuf<Key3> keys_out;
+        DevBuf<int32_t> slots_out;
+        keys_out.ensure(V);
+        slots_out.ensure(V);
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, keys_out.p, h->vslots.p, slots_out.p, V,
+                                           KeyDecomposer{}, st));
+        h->cub_tmp.ensure(tmp);
+        CK(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, keys_in, keys_out.p, h->vslots.p, slots_out.p, V,
+                                           KeyDecomposer{}, st));
+        gather_ids_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(slots_out.p, h->ids, V, h->vids.p);
+        h->launches += 2;
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        keys_out.release();
+        slots_out.release();
+    }
+    out.resize(V);
+    CK(cudaMemcpyAsync(out.data(), h->vids.p, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    record(h, 4, st);
+    CK(cudaStreamSynchronize(st));
+    if (h->timing) CK(cudaEventElapsedTime(&h->t_evict, h->ev[3], h->ev[4]));
+}
+
+void remove_slots(sine_index* h, const std::vector<int64_t>& slots) {
+    if (slots.empty()) return;
+    DevBuf<int64_t> d;
+    d.ensure(slots.size());
+    CK(cudaMemcpyAsync(d.p, slots.data(), slots.size() * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    set_bits_kernel<<<grid_for(slots.size(), 256, h->num_sms), 256, 0, h->stream>>>(h->valid, d.p, slots.size(), 0);
+    ++h->launches;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    d.release();
+    for (int64_t s : slots) {
+        h->pos.erase(h->ids_h[s]);
+        h->live_h[s] = 0;
+    }
+    h->nlive -= static_cast<int64_t>(slots.size());
+    const int64_t dead = h->nslots - h->nlive;
+    if (dead > std::max<int64_t>(64, h->nlive / 4)) compact(h);
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* sine_last_error(void) { return g_err.c_str(); }
+int sine_version(void) { return 1; }
+
+int sine_device_count(int* n) {
+    return guarded([&] { CK(cudaGetDeviceCount(n)); });
+}
+
+int sine_create(int device, int64_t dim, uint32_t flags, int64_t reserve_rows, sine_index_t** out) {
+    return guarded([&] {
+        if (!out) fail(SINE_EINVAL, "null output handle");
+        if (dim < 1) fail(SINE_EINVAL, "dimension must be >= 1");
+        if (!(flags & (SINE_STORE_F32 | SINE_STORE_BF16))) flags |= SINE_STORE_F32;
+        CK(cudaSetDevice(device));
+        auto* h = new sine_index();
+        h->device = device;
+        h->dim = dim;
+        h->flags = flags;
+        h->stride32 = round_up(dim, 32);
+        h->stride16 = round_up(dim, 64);
+        CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        for (auto& e : h->ev) CK(cudaEventCreate(&e));
+        if (reserve_rows > 0) grow(h, reserve_rows);
+        *out = h;
+    });
+}
+
+int sine_destroy(sine_index_t* h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaSetDevice(h->device);
+        cudaStreamSynchronize(h->stream);
+        for (void* p : {(void*)h->rows32, (void*)h->rows16, (void*)h->rows64, (void*)h->ids, (void*)h->valid,
+                        (void*)h->lf, (void*)h->lc, (void*)h->ll, (void*)h->ls, (void*)h->created,
+                        (void*)h->expiration, (void*)h->last_access, (void*)h->freq, (void*)h->size})
+            if (p) cudaFree(p);
+        h->q64.release(), h->lkey.release(), h->lslot.release(), h->ln.release();
+        h->o_ids.release(), h->o_sims.release(), h->o_cnt.release(), h->k1.release();
+        h->vkeys.release(), h->vslots.release(), h->cand.release(), h->scratch_i32.release();
+        h->vids.release(), h->cub_tmp.release(), h->hist.release(), h->st.release(), h->qbf.release();
+        h->st_h.release(), h->n_h.release(), h->cnt_h.release();
+        for (auto& e : h->ev) cudaEventDestroy(e);
+        cudaStreamDestroy(h->stream);
+        delete h;
+    });
+}
+
+int sine_reserve(sine_index_t* h, int64_t rows) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        grow(h, rows);
+    });
+}
+
+int sine_insert(sine_index_t* h, int64_t n, const int64_t* ids, const double* rows, const sine_meta_cols_t* meta,
+                uint32_t flags) {
+    return guarded([&] {
+        if (n <= 0) return;
+        if (!ids || !rows) fail(SINE_EINVAL, "null ids/rows");
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        if (!(flags & SINE_NO_NORM_CHECK)) check_rows_host(h, n, rows);
+        check_new_ids(h, n, ids);
+        append(h, n, ids, rows, false, meta);
+    });
+}
+
+int sine_insert_device(sine_index_t* h, int64_t n, const int64_t* ids, const double* rows_dev,
+                       const sine_meta_cols_t* meta, uint32_t flags) {
+    (void)flags;
+    return guarded([&] {
+        if (n <= 0) return;
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        check_new_ids(h, n, ids);
+        append(h, n, ids, rows_dev, true, meta);
+    });
+}
+
+int sine_remove(sine_index_t* h, int64_t n, const int64_t* ids) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        std::vector<int64_t> slots;
+        slots.reserve(n);
+        std::unordered_set<int64_t> seen;
+        for (int64_t i = 0; i < n; ++i) {
+            auto it = h->pos.find(ids[i]);
+            if (it == h->pos.end() || !seen.insert(ids[i]).second)
+                fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
+            slots.push_back(it->second);
+        }
+        remove_slots(h, slots);
+    });
+}
+
+int sine_size(sine_index_t* h, int64_t* live, int64_t* slots) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        if (live) *live = h->nlive;
+        if (slots) *slots = h->nslots;
+    });
+}
+
+int sine_ids(sine_index_t* h, int64_t* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        int64_t j = 0;
+        for (int64_t s = 0; s < h->nslots; ++s) {
+            if (!h->live_h[s]) continue;
+            if (j < cap) out[j] = h->ids_h[s];
+            ++j;
+        }
+        *n = j;
+    });
+}
+
+int sine_get_rows(sine_index_t* h, int64_t n, const int64_t* ids, double* out) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        for (int64_t i = 0; i < n; ++i) {
+            auto it = h->pos.find(ids[i]);
+            if (it == h->pos.end()) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
+            CK(cudaMemcpyAsync(out + i * h->dim, h->rows64 + it->second * h->dim, h->dim * sizeof(double),
+                               cudaMemcpyDeviceToHost, h->stream));
+        }
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_sim, uint32_t mode, int64_t* out_ids,
+               double* out_sims, int32_t* out_counts) {
+    return guarded([&] {
+        if (B <= 0) return;
+        if (k < 1) fail(SINE_EINVAL, "k must be >= 1");
+        if (!(mode & SINE_NO_NORM_CHECK)) check_queries_host(h, B, q);
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        h->q64.ensure(B * h->dim);
+        h->o_ids.ensure(B * k);
+        h->o_sims.ensure(B * k);
+        h->o_cnt.ensure(B);
+        CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
+        CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->timing) {
+            CK(cudaEventElapsedTime(&h->t_scan, h->ev[0], h->ev[1]));
+            CK(cudaEventElapsedTime(&h->t_merge, h->ev[1], h->ev[2]));
+        }
+    });
+}
+
+int sine_query_device(sine_index_t* h, int64_t B, const double* q_dev, int k, double min_sim, uint32_t mode,
+                      int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, void* stream) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        query_device_impl(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
+    });
+}
+
+int sine_update_meta(sine_index_t* h, int64_t n, const int64_t* ids, const double* log_freq,
+                     const int64_t* frequency, const double* last_access) {
+    return guarded([&] {
+        if (n <= 0) return;
+        std::lock_guard<std::mutex> g(h->mu);
+        if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata");
+        CK(cudaSetDevice(h->device));
+        std::vector<int64_t> slots(n);
+        for (int64_t i = 0; i < n; ++i) {
+            auto it = h->pos.find(ids[i]);
+            if (it == h->pos.end()) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
+            slots[i] = it->second;
+        }
+        if (n == 1) {
+            const int64_t s = slots[0];
+            CK(cudaMemcpyAsync(h->lf + s, log_freq, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(h->freq + s, frequency, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(h->last_access + s, last_access, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        } else {
+            DevBuf<int64_t> ds, dfq;
+            DevBuf<double> dlf, dla;
+            ds.ensure(n), dfq.ensure(n), dlf.ensure(n), dla.ensure(n);
+            CK(cudaMemcpyAsync(ds.p, slots.data(), n * 8, cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(dlf.p, log_freq, n * 8, cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(dfq.p, frequency, n * 8, cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(dla.p, last_access, n * 8, cudaMemcpyHostToDevice, h->stream));
+            scatter_meta_kernel<<<grid_for(n, 256, h->num_sms), 256, 0, h->stream>>>(ds.p, n, dlf.p, dfq.p, dla.p,
+                                                                                      h->lf, h->freq, h->last_access);
+            ++h->launches;
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata");
+        CK(cudaSetDevice(h->device));
+        *n = 0;
+        if (h->nlive == 0) return;
+        const int64_t chunk = 1 << 16;
+        const int nb = static_cast<int>((h->nslots + chunk - 1) / chunk);
+        h->scratch_i32.ensure(nb);
+        h->cnt_h.ensure(nb);
+        expire_count_kernel<<<nb, 256, 0, h->stream>>>(h->expiration, h->valid, h->nslots, now, chunk,
+                                                       h->scratch_i32.p);
+        ++h->launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->cnt_h.p, h->scratch_i32.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        int64_t total = 0;
+        for (int b = 0; b < nb; ++b) total += h->cnt_h.p[b];
+        *n = total;
+        if (total == 0) return;
+        h->vids.ensure(total);
+        h->vslots.ensure(total);
+        expire_write_kernel<<<nb, 256, 0, h->stream>>>(h->expiration, h->valid, h->ids, h->nslots, now, chunk,
+                                                       h->scratch_i32.p, h->vids.p, h->vslots.p);
+        ++h->launches;
+        CK(cudaGetLastError());
+        std::vector<int64_t> ids(total);
+        std::vector<int32_t> slots(total);
+        CK(cudaMemcpyAsync(ids.data(), h->vids.p, total * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(slots.data(), h->vslots.p, total * 4, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (!h->ids_ascending) std::sort(ids.begin(), ids.end());
+        if (total > cap) fail(SINE_EINVAL, "output buffer too small for expired ids");
+        std::copy(ids.begin(), ids.end(), out);
+        if (remove) {
+            std::vector<int64_t> s64(slots.begin(), slots.end());
+            remove_slots(h, s64);
+        }
+    });
+}
+
+int sine_select_victims(sine_index_t* h, int policy, double now, int64_t excess, int64_t* out, int64_t cap,
+                        int64_t* n) {
+    return guarded([&] {
+        if (policy < 0 || policy > 2) fail(SINE_EINVAL, "unknown eviction policy");
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        std::vector<int64_t> v;
+        select_victims_impl(h, policy, now, excess, v);
+        *n = static_cast<int64_t>(v.size());
+        if (*n > cap) fail(SINE_EINVAL, "output buffer too small for the victim list");
+        std::copy(v.begin(), v.end(), out);
+    });
+}
+
+int sine_stream(sine_index_t* h, void** stream) {
+    return guarded([&] { *stream = h->stream; });
+}
+
+int sine_set_timing(sine_index_t* h, int on) {
+    return guarded([&] { h->timing = on != 0; });
+}
+
+int sine_last_timing(sine_index_t* h, float* scan_ms, float* merge_ms, float* evict_ms) {
+    return guarded([&] {
+        if (scan_ms) *scan_ms = h->t_scan;
+        if (merge_ms) *merge_ms = h->t_merge;
+        if (evict_ms) *evict_ms = h->t_evict;
+    });
+}
+
+int sine_kernel_launches(sine_index_t* h, int64_t* n) {
+    return guarded([&] { *n = h->launches; });
+}
+
+int sine_host_alloc(size_t bytes, void** p) {
+    return guarded([&] { CK(cudaMallocHost(p, bytes)); });
+}
+
+int sine_host_free(void* p) {
+    return guarded([&] { CK(cudaFreeHost(p)); });
+}
+
+}  // extern "C"

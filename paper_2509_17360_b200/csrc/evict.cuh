@@ -1,0 +1,328 @@
+// LCFU / LRU / LFU victim selection and TTL expiry on the device SE store.
+//
+// Reference semantics (pkg/src/semcache/engine.py):
+//   cal_score            :33-48   0 if size==0 or expiration-now<=0, else
+//                                 log(f+1)*log(c*1000+1)*log(l+1)*log(s+1)/size
+//   _victim_order_locked :369-383 ascending (key, created_at, id)
+//   admit / evict loops  :321-327, :353-359 pop until the freed size reaches
+//                                 the excess -> a size-weighted prefix
+//   _purge_expired_locked:362-367 expired ids, ascending
+//
+// The logs are evaluated on the host with libm (bit-identical to the
+// reference's math.log) and stored per element; the device evaluates the
+// product with explicit round-to-nearest intrinsics (no FMA contraction)
+// in the reference's left-to-right order, so scores are bit-exact.
+//
+// Victim selection never sorts all N elements: a weighted MSB-first radix
+// select over the 192-bit composite key (primary, created_at, id) finds the
+// last victim T (8-bit digits; digits that are constant over the surviving
+// candidates are skipped using AND/OR reductions), then only the victims
+// (keys <= T) are collected and sorted.
+#pragma once
+
+#include "common.cuh"
+
+namespace sine {
+
+struct EvictCols {
+    const double *lf, *lc, *ll, *ls, *created, *expiration, *last_access;
+    const int64_t *freq, *size, *ids;
+    const uint32_t* valid;
+    int64_t nslots;
+};
+
+struct SelectState {
+    uint64_t prefix[3];
+    int32_t ndigits;  // digits of the composite key fixed so far (0..24)
+    int32_t done;     // 1: prefix identifies the last victim; 2: everything is a victim
+    int64_t rem;      // weight still needed inside the prefix bucket
+    int64_t count;    // candidates matching the prefix
+    int64_t total_w;  // first pass: live weight
+};
+
+__device__ __forceinline__ double lcfu_score(const EvictCols& c, int64_t s, double now) {
+    const int64_t size = c.size[s];
+    if (size == 0 || __dsub_rn(c.expiration[s], now) <= 0.0) return 0.0;
+    double v = __dmul_rn(c.lf[s], c.lc[s]);
+    v = __dmul_rn(v, c.ll[s]);
+    v = __dmul_rn(v, c.ls[s]);
+    return __ddiv_rn(v, static_cast<double>(size));
+}
+
+__device__ __forceinline__ uint64_t primary_key(const EvictCols& c, int64_t s, int policy, double now) {
+    if (policy == 0) return f64_key(lcfu_score(c, s, now));
+    if (policy == 1) return f64_key(c.last_access[s]);
+    return i64_key(c.freq[s]);
+}
+
+__device__ __forceinline__ uint32_t key_digit(const uint64_t k[3], int d) {
+    return static_cast<uint32_t>((k[d >> 3] >> (8 * (7 - (d & 7)))) & 0xff);
+}
+
+// compare the first nd digits of k against prefix: -1 / 0 / +1
+__device__ __forceinline__ int prefix_cmp(const uint64_t k[3], const uint64_t pre[3], int nd) {
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+        const int dw = nd - 8 * w;  // digits of this word that count
+        if (dw <= 0) return 0;
+        const uint64_t mask = dw >= 8 ? ~0ull : ~((1ull << (8 * (8 - dw))) - 1);
+        const uint64_t a = k[w] & mask, b = pre[w] & mask;
+        if (a != b) return a < b ? -1 : 1;
+    }
+    return 0;
+}
+
+struct HistArgs {
+    EvictCols c;
+    int policy;
+    double now;
+    const int32_t* cand;   // nullptr: all slots
+    int64_t ncand;
+    uint64_t* k1;          // cached primary keys [nslots]
+    int first;             // compute (and cache) primary keys
+    const SelectState* st;
+    unsigned long long* hw;   // [256] weights
+    unsigned long long* hc;   // [256] counts
+    unsigned long long* hand; // [3]
+    unsigned long long* hor;  // [3]
+};
+
+__global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
+    __shared__ unsigned long long sw[256], sc[256];
+    sw[threadIdx.x] = 0;
+    sc[threadIdx.x] = 0;
+    __syncthreads();
+    const int nd = a.st->ndigits;
+    uint64_t pre[3] = {a.st->prefix[0], a.st->prefix[1], a.st->prefix[2]};
+    uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
+    const int64_t n = a.cand ? a.ncand : a.c.nslots;
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
+        const int64_t s = a.cand ? a.cand[i] : i;
+        if (!a.cand && !valid_bit(a.c.valid, s)) continue;
+        uint64_t k[3];
+        if (a.first) {
+            k[0] = primary_key(a.c, s, a.policy, a.now);
+            a.k1[s] = k[0];
+        } else {
+            k[0] = a.k1[s];
+        }
+        k[1] = f64_key(a.c.created[s]);
+        k[2] = i64_key(a.c.ids[s]);
+        if (prefix_cmp(k, pre, nd) != 0) continue;
+        const uint32_t dg = key_digit(k, nd);
+        atomicAdd(&sw[dg], static_cast<unsigned long long>(a.c.size[s]));
+        atomicAdd(&sc[dg], 1ull);
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+            vand[w] &= k[w];
+            vor[w] |= k[w];
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vand[w] &= __shfl_xor_sync(0xffffffffu, vand[w], o);
+            vor[w] |= __shfl_xor_sync(0xffffffffu, vor[w], o);
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+            atomicAnd(a.hand + w, static_cast<unsigned long long>(vand[w]));
+            atomicOr(a.hor + w, static_cast<unsigned long long>(vor[w]));
+        }
+    }
+    __syncthreads();
+    if (sc[threadIdx.x]) {
+        atomicAdd(a.hw + threadIdx.x, sw[threadIdx.x]);
+        atomicAdd(a.hc + threadIdx.x, sc[threadIdx.x]);
+    }
+}
+
+// One CTA: choose the digit bucket where the cumulative weight reaches rem,
+// then skip the following digits that are constant over that bucket.
+__global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsigned long long* hw,
+                                                         unsigned long long* hc, unsigned long long* hand,
+                                                         unsigned long long* hor, int first) {
+    __shared__ unsigned long long cw[256];
+    __shared__ int chosen;
+    __shared__ unsigned long long before_w;
+    const int t = threadIdx.x;
+    cw[t] = hw[t];
+    if (t == 0) chosen = -1;
+    __syncthreads();
+    // inclusive scan (Hillis-Steele, 256 entries)
+    for (int o = 1; o < 256; o <<= 1) {
+        const unsigned long long v = t >= o ? cw[t - o] : 0ull;
+        __syncthreads();
+        cw[t] += v;
+        __syncthreads();
+    }
+    const long long rem = st->rem;
+    const unsigned long long ex = t ? cw[t - 1] : 0ull;
+    if (static_cast<long long>(ex) < rem && rem <= static_cast<long long>(cw[t])) {
+        chosen = t;
+        before_w = ex;
+    }
+    __syncthreads();
+    if (t == 0) {
+        if (first) st->total_w = static_cast<int64_t>(cw[255]);
+        if (chosen < 0) {
+            // the excess is at least the whole candidate weight: all are victims
+            st->done = 2;
+        } else {
+            const int nd = st->ndigits;
+            st->prefix[nd >> 3] |= static_cast<uint64_t>(chosen) << (8 * (7 - (nd & 7)));
+            st->rem = rem - static_cast<long long>(before_w);
+            const unsigned long long cnt = hc[chosen];
+            int ndn = nd + 1;
+            // total candidates that matched this pass
+            unsigned long long tot = 0;
+            for (int b = 0; b < 256; ++b) tot += hc[b];
+            if (cnt == tot) {
+                // every candidate was in one bucket: AND/OR describe the bucket
+                // exactly, so digits equal in AND and OR are constant -- skip them
+                while (ndn < 24) {
+                    const int w = ndn >> 3, sh = 8 * (7 - (ndn & 7));
+                    const uint64_t da = (hand[w] >> sh) & 0xff, dor = (hor[w] >> sh) & 0xff;
+                    if (da != dor) break;
+                    st->prefix[w] |= da << sh;
+                    ++ndn;
+                }
+            }
+            st->ndigits = ndn;
+            st->count = static_cast<int64_t>(cnt);
+            if (cnt <= 1 || ndn >= 24) st->done = 1;
+        }
+    }
+    __syncthreads();
+    hw[t] = 0;
+    hc[t] = 0;
+    if (t < 3) {
+        hand[t] = ~0ull;
+        hor[t] = 0ull;
+    }
+}
+
+struct CollectArgs {
+    EvictCols c;
+    const uint64_t* k1;
+    const SelectState* st;
+    const int32_t* cand;  // nullptr: all slots
+    int64_t ncand;
+    int mode;             // 0: victims (prefix <=), 1: candidates (prefix ==)
+    uint64_t* out_k;      // [cap][3] (victims) or unused
+    int32_t* out_slot;    // [cap]
+    unsigned long long* out_n;
+    int64_t cap;
+};
+
+__global__ void __launch_bounds__(256) evict_collect_kernel(const CollectArgs a) {
+    const int nd = a.st->ndigits;
+    const bool all = a.st->done == 2;
+    const uint64_t pre[3] = {a.st->prefix[0], a.st->prefix[1], a.st->prefix[2]};
+    const int64_t n = a.cand ? a.ncand : a.c.nslots;
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
+        const int64_t s = a.cand ? a.cand[i] : i;
+        if (!a.cand && !valid_bit(a.c.valid, s)) continue;
+        uint64_t k[3] = {a.k1[s], f64_key(a.c.created[s]), i64_key(a.c.ids[s])};
+        const int cmp = all ? -1 : prefix_cmp(k, pre, nd);
+        const bool take = a.mode == 0 ? cmp <= 0 : cmp == 0;
+        if (!take) continue;
+        const unsigned long long at = atomicAdd(a.out_n, 1ull);
+        if (static_cast<int64_t>(at) < a.cap) {
+            a.out_slot[at] = static_cast<int32_t>(s);
+            if (a.mode == 0) {
+                a.out_k[3 * at] = k[0];
+                a.out_k[3 * at + 1] = k[1];
+                a.out_k[3 * at + 2] = k[2];
+            }
+        }
+    }
+}
+
+struct Key3 {
+    uint64_t a, b, c;  // (primary, created_at, id) order-preserving keys
+};
+
+__global__ void gather_ids_kernel(const int32_t* slots, const int64_t* ids, int64_t n, int64_t* out) {
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) out[i] = ids[slots[i]];
+}
+
+// Small victim sets: one CTA sorts by the 192-bit key (rank sort in smem).
+__device__ __forceinline__ bool key3_less(const uint64_t* a, const uint64_t* b) {
+    if (a[0] != b[0]) return a[0] < b[0];
+    if (a[1] != b[1]) return a[1] < b[1];
+    return a[2] < b[2];
+}
+
+__global__ void __launch_bounds__(1024) evict_small_sort_kernel(const uint64_t* keys, const int32_t* slots,
+                                                                const int64_t* ids, int n, int64_t* out_ids) {
+    extern __shared__ uint64_t sk[];  // [n][3]
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) sk[i] = keys[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int r = 0;
+        for (int j = 0; j < n; ++j) r += key3_less(sk + 3 * j, sk + 3 * i) ? 1 : 0;
+        out_ids[r] = ids[slots[i]];
+    }
+}
+
+// ------------------------------------------------------------------ expiry
+
+__global__ void __launch_bounds__(256) expire_count_kernel(const double* expiration, const uint32_t* valid,
+                                                           int64_t nslots, double now, int64_t chunk,
+                                                           int32_t* counts) {
+    __shared__ int32_t s;
+    if (threadIdx.x == 0) s = 0;
+    __syncthreads();
+    const int64_t b = blockIdx.x * chunk, e = min(b + chunk, nslots);
+    int32_t c = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += 256)
+        c += (valid_bit(valid, i) && __dsub_rn(expiration[i], now) <= 0.0) ? 1 : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s, c);
+    __syncthreads();
+    if (threadIdx.x == 0) counts[blockIdx.x] = s;
+}
+
+// Ordered write: block b writes its expired slots (ascending) at offsets[b].
+__global__ void __launch_bounds__(256) expire_write_kernel(const double* expiration, const uint32_t* valid,
+                                                           const int64_t* ids, int64_t nslots, double now,
+                                                           int64_t chunk, const int32_t* counts,
+                                                           int64_t* out_ids, int32_t* out_slots) {
+    __shared__ int32_t warp_tot[8];
+    __shared__ int32_t base;
+    if (threadIdx.x == 0) {
+        int32_t o = 0;
+        for (int j = 0; j < static_cast<int>(blockIdx.x); ++j) o += counts[j];
+        base = o;
+    }
+    __syncthreads();
+    const int64_t b = blockIdx.x * chunk, e = min(b + chunk, nslots);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t i0 = b; i0 < e; i0 += 256) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool f = i < e && valid_bit(valid, i) && __dsub_rn(expiration[i], now) <= 0.0;
+        const uint32_t m = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) warp_tot[warp] = __popc(m);
+        __syncthreads();
+        int32_t off = base;
+        for (int w = 0; w < warp; ++w) off += warp_tot[w];
+        off += __popc(m & ((1u << lane) - 1));
+        if (f) {
+            out_ids[off] = ids[i];
+            out_slots[off] = static_cast<int32_t>(i);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int32_t t = 0;
+            for (int w = 0; w < 8; ++w) t += warp_tot[w];
+            base += t;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace sine

@@ -1,0 +1,222 @@
+// Merge of per-CTA candidate lists + optional fp64 re-rank + final order.
+//
+// One CTA per query.  The pooled per-CTA lists (score keys) go through a
+// block radix select (8-bit digits, MSB first) that finds the exact k'-th
+// best key; entries above it are kept, entries equal to it are resolved by
+// ascending id (a second radix select on ids when the tie straddles the
+// cut).  The surviving k' candidates are optionally re-scored in fp64
+// against the fp64 master rows (fixed lane order, so identical rows give
+// identical similarities), ordered by (similarity desc, id asc), filtered by
+// the inclusive threshold and cut to k -- the rest of `_rank`
+// (reference pkg/src/semcache/index.py:42-46).
+#pragma once
+
+#include "common.cuh"
+
+namespace sine {
+
+struct MergeParams {
+    const uint32_t* in_key;  // [ncta][nq][kp]
+    const int32_t* in_slot;
+    const int32_t* in_n;     // [ncta][nq]
+    int ncta, nq, kp;
+    const int64_t* ids;
+    const double* rows64;    // [nslots][dim]
+    const double* q64;       // [nq][dim]
+    int64_t dim;
+    int k;
+    double min_sim;
+    int rerank;
+    int64_t* out_ids;        // [nq][k]
+    double* out_sims;
+    int32_t* out_counts;     // [nq]
+};
+
+constexpr int kMergeThreads = 256;
+
+// Block-wide exclusive scan of one value per thread (256 threads).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += warp_tot[w];
+    __syncthreads();
+    return off + inc - v;
+}
+
+// Select, among the entries accepted by `get` (returns false to skip), the
+// `kth` (1-based) key in descending (desc=true) or ascending order.  Keys
+// are `nbits` wide (multiple of 8).  Returns the key; *before = number of
+// entries strictly before it in that order; *equal = entries equal to it.
+template <typename KeyT, typename Get>
+__device__ KeyT block_select(Get get, int nflat, uint32_t kth, bool desc, int nbits, uint32_t* hist,
+                             uint32_t* scratch, uint32_t* before, uint32_t* equal) {
+    KeyT prefix = 0, pmask = 0;
+    uint32_t need = kth, found_bin = 0;
+    for (int shift = nbits - 8; shift >= 0; shift -= 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
+            KeyT key;
+            if (get(f, key) && (key & pmask) == prefix)
+                atomicAdd(hist + static_cast<uint32_t>((key >> shift) & 0xff), 1u);
+        }
+        __syncthreads();
+        const int bin = desc ? 255 - static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x);
+        const uint32_t c = hist[bin];
+        const uint32_t ex = block_excl_scan(c, scratch);
+        if (ex < need && need <= ex + c) {
+            scratch[8] = bin;
+            scratch[9] = ex;
+            scratch[10] = c;
+        }
+        __syncthreads();
+        found_bin = scratch[8];
+        need -= scratch[9];
+        *equal = scratch[10];
+        prefix |= static_cast<KeyT>(found_bin) << shift;
+        pmask |= static_cast<KeyT>(0xff) << shift;
+        __syncthreads();
+    }
+    *before = kth - need;
+    return prefix;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams p) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t scratch[16];
+    __shared__ int32_t ns[1024];
+    __shared__ int32_t sel_slot[kMaxKp];
+    __shared__ uint32_t sel_key[kMaxKp];
+    __shared__ int64_t sel_id[kMaxKp];
+    __shared__ double sel_sim[kMaxKp];
+    __shared__ uint32_t nsel;
+
+    const int qi = blockIdx.x;
+    const int kp = p.kp, nq = p.nq;
+    const int nflat = p.ncta * kp;
+    for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) ns[c] = p.in_n[c * nq + qi];
+    if (threadIdx.x == 0) nsel = 0;
+    __syncthreads();
+
+    auto flat_ok = [&](int f, int& c, int& e) {
+        c = f / kp;
+        e = f - c * kp;
+        return e < ns[c];
+    };
+    auto key_at = [&](int c, int e) { return p.in_key[(static_cast<size_t>(c) * nq + qi) * kp + e]; };
+    auto slot_at = [&](int c, int e) { return p.in_slot[(static_cast<size_t>(c) * nq + qi) * kp + e]; };
+
+    // total candidates
+    uint32_t local = 0;
+    for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) local += ns[c];
+    const uint32_t before_me = block_excl_scan(local, scratch);
+    if (threadIdx.x == kMergeThreads - 1) scratch[12] = before_me + local;
+    __syncthreads();
+    const uint32_t total = scratch[12];
+    __syncthreads();
+
+    if (total <= static_cast<uint32_t>(kp)) {
+        for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
+            int c, e;
+            if (!flat_ok(f, c, e)) continue;
+            const uint32_t at = atomicAdd(&nsel, 1u);
+            sel_key[at] = key_at(c, e);
+            sel_slot[at] = slot_at(c, e);
+        }
+    } else {
+        uint32_t nbefore, nequal;
+        const uint32_t kstar = block_select<uint32_t>(
+            [&](int f, uint32_t& key) {
+                int c, e;
+                if (!flat_ok(f, c, e)) return false;
+                key = key_at(c, e);
+                return true;
+            },
+            nflat, static_cast<uint32_t>(kp), true, 32, hist, scratch, &nbefore, &nequal);
+        const uint32_t need_eq = kp - nbefore;
+        // ties at the cut: keep the need_eq smallest ids
+        uint64_t idcut = ~0ull;
+        if (nequal > need_eq) {
+            uint32_t b2, e2;
+            idcut = block_select<uint64_t>(
+                [&](int f, uint64_t& key) {
+                    int c, e;
+                    if (!flat_ok(f, c, e) || key_at(c, e) != kstar) return false;
+                    key = i64_key(__ldg(p.ids + slot_at(c, e)));
+                    return true;
+                },
+                nflat, need_eq, false, 64, hist, scratch, &b2, &e2);
+        }
+        for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
+            int c, e;
+            if (!flat_ok(f, c, e)) continue;
+            const uint32_t key = key_at(c, e);
+            bool take = key > kstar;
+            if (key == kstar) take = (idcut == ~0ull) || i64_key(__ldg(p.ids + slot_at(c, e))) <= idcut;
+            if (take) {
+                const uint32_t at = atomicAdd(&nsel, 1u);
+                sel_key[at] = key;
+                sel_slot[at] = slot_at(c, e);
+            }
+        }
+    }
+    __syncthreads();
+    const int m = static_cast<int>(nsel);
+
+    for (int i = threadIdx.x; i < m; i += kMergeThreads) {
+        sel_id[i] = __ldg(p.ids + sel_slot[i]);
+        sel_sim[i] = static_cast<double>(key_f32(sel_key[i]));
+    }
+    __syncthreads();
+
+    if (p.rerank) {
+        // fp64 re-score: one warp per candidate, lane-strided fma chain then
+        // a fixed butterfly -> identical rows give identical similarities.
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const double* q = p.q64 + static_cast<size_t>(qi) * p.dim;
+        for (int i = warp; i < m; i += kMergeThreads / 32) {
+            const double* x = p.rows64 + static_cast<size_t>(sel_slot[i]) * p.dim;
+            double a = 0.0;
+            for (int64_t t = lane; t < p.dim; t += 32) a = fma(__ldg(x + t), __ldg(q + t), a);
+            a = warp_sum64(a);
+            if (lane == 0) sel_sim[i] = a + 0.0;
+        }
+        __syncthreads();
+    }
+
+    // rank sort by (sim desc, id asc) -- keys are unique (ids unique)
+    __shared__ int32_t order[kMaxKp];
+    for (int i = threadIdx.x; i < m; i += kMergeThreads) {
+        int r = 0;
+        const double si = sel_sim[i];
+        const int64_t ii = sel_id[i];
+        for (int j = 0; j < m; ++j) r += cand_before64(sel_sim[j], sel_id[j], si, ii) ? 1 : 0;
+        order[r] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int outn = 0;
+        for (int r = 0; r < m && outn < p.k; ++r) {
+            const int i = order[r];
+            if (!(sel_sim[i] >= p.min_sim)) break;  // sorted desc: the rest fail too
+            p.out_ids[static_cast<size_t>(qi) * p.k + outn] = sel_id[i];
+            p.out_sims[static_cast<size_t>(qi) * p.k + outn] = sel_sim[i];
+            ++outn;
+        }
+        for (int r = outn; r < p.k; ++r) {
+            p.out_ids[static_cast<size_t>(qi) * p.k + r] = -1;
+            p.out_sims[static_cast<size_t>(qi) * p.k + r] = 0.0;
+        }
+        p.out_counts[qi] = outn;
+    }
+}
+
+}  // namespace sine

@@ -1,0 +1,307 @@
+"""GpuCosineIndex -- the device-resident Sine stage-1 index.
+
+Drop-in for the reference `ExactCosineIndex` (pkg/src/semcache/index.py:49-120):
+same constructor arguments, `insert` / `remove` / `query` / `__len__` /
+`ids` / `snapshot_lines` / `save` / `load`, attributes `dimension`, `seed`
+and `SNAPSHOT_MAGIC`, the same `ValidationError`s, and results ordered by
+(similarity desc, id asc) with an inclusive `min_similarity` threshold.
+
+Pass it to `semcache.engine.CacheEngine(config, embedder, judge, index=...)`
+(engine.py:103-109) or use `paper_2509_17360_b200.engine.CacheEngine`,
+which also moves the LCFU eviction pass onto the device.
+
+Modes: `scan="fp32"` (exact mode: fp32 rows, then an fp64 re-rank of the
+final candidates -- similarities agree with the reference's float64 to
+~1e-16) or `scan="bf16"` (fast mode: half the HBM bytes; with `rerank=True`
+the candidates are still re-scored in fp64, with `rerank=False` the
+similarities are the bf16/fp32-accumulated scores, within 2e-2).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ValidationError
+
+_NORM_TOL = 1e-6
+
+
+@dataclass(frozen=True)
+class Candidate:
+    """(id, similarity) -- mirrors reference index.py:26-29."""
+    id: int
+    similarity: float
+
+
+def check_vector(vec, dimension: int) -> np.ndarray:
+    """Same validation as the reference `_check_vector` (index.py:32-39)."""
+    arr = np.asarray(vec.components if hasattr(vec, "components") else vec, dtype=np.float64)
+    if arr.ndim != 1 or arr.shape[0] != dimension:
+        raise ValidationError(f"expected dimension {dimension}, got shape {arr.shape}")
+    n = float(np.linalg.norm(arr))
+    if abs(n - 1.0) > _NORM_TOL:
+        raise ValidationError(f"vector is not L2-normalized (norm={n:.8f})")
+    return arr
+
+
+def check_matrix(rows, dimension: int) -> np.ndarray:
+    """Row-wise `_check_vector` for a batch (identical per-row arithmetic)."""
+    arr = np.ascontiguousarray(rows, dtype=np.float64)
+    if arr.ndim != 2 or arr.shape[1] != dimension:
+        raise ValidationError(f"expected rows of dimension {dimension}, got shape {arr.shape}")
+    for i in range(arr.shape[0]):
+        n = float(np.linalg.norm(arr[i]))
+        if abs(n - 1.0) > _NORM_TOL:
+            raise ValidationError(f"vector is not L2-normalized (norm={n:.8f})")
+    return arr
+
+
+class GpuCosineIndex:
+    """Exact cosine index on one B200: rows stream from HBM through the
+    sm_100a stage-1 kernels; the reference's result contract is preserved."""
+
+    SNAPSHOT_MAGIC = "exact-cosine-index"
+
+    def __init__(self, dimension: int, seed: int = 1, *, device: int = 0, scan: str = "fp32",
+                 rerank: bool = True, store_bf16: bool | None = None, store_f32: bool | None = None,
+                 metadata: bool = False, capacity: int = 0):
+        if dimension < 1:
+            raise ValidationError("dimension must be >= 1")
+        if scan not in ("fp32", "bf16"):
+            raise ValidationError(f"scan must be 'fp32' or 'bf16', got {scan!r}")
+        self.dimension = dimension
+        self.seed = seed
+        self.device = device
+        self.scan = scan
+        self.rerank = rerank
+        if store_f32 is None:
+            store_f32 = scan == "fp32"
+        if store_bf16 is None:
+            store_bf16 = scan == "bf16"
+        flags = (N.STORE_F32 if store_f32 else 0) | (N.STORE_BF16 if store_bf16 else 0) | \
+            (N.STORE_META if metadata else 0)
+        self._lib = N.load_library()
+        h = ctypes.c_void_p()
+        N.check(self._lib.sine_create(device, dimension, flags, int(capacity), ctypes.byref(h)))
+        self._h = h
+        self.metadata = metadata
+        self._wlock = threading.Lock()  # single writer (engine.py:95-101 discipline)
+
+    # ---------------------------------------------------------- lifecycle
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.sine_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def _mode(self, scan: str | None = None, rerank: bool | None = None) -> int:
+        scan = scan or self.scan
+        rerank = self.rerank if rerank is None else rerank
+        m = N.SCAN_BF16 if scan == "bf16" else N.SCAN_F32
+        if rerank:
+            m |= N.RERANK_F64
+        return m | N.NO_NORM_CHECK
+
+    # ------------------------------------------------------------ queries
+    def __len__(self) -> int:
+        live = ctypes.c_int64()
+        N.check(self._lib.sine_size(self._h, ctypes.byref(live), None))
+        return live.value
+
+    def ids(self) -> list[int]:
+        n = len(self)
+        out = np.empty(max(n, 1), dtype=np.int64)
+        got = ctypes.c_int64()
+        N.check(self._lib.sine_ids(self._h, N.ptr(out, ctypes.c_int64), n, ctypes.byref(got)))
+        return out[:got.value].tolist()
+
+    def insert(self, id: int, vector, meta=None) -> None:
+        arr = check_vector(vector, self.dimension)
+        self.insert_batch(np.array([id], dtype=np.int64), arr[None, :], meta=meta, _checked=True)
+
+    def insert_batch(self, ids, rows, meta=None, _checked: bool = False) -> None:
+        """Append many rows at once (host float64 [n, dimension])."""
+        ids = N.i64(ids)
+        rows = N.f64(rows) if _checked else check_matrix(rows, self.dimension)
+        if rows.shape[0] != ids.shape[0]:
+            raise ValidationError("ids and rows differ in length")
+        cols, keep = _meta_struct(meta, ids.shape[0]) if meta is not None else (None, None)
+        with self._wlock:
+            N.check(self._lib.sine_insert(self._h, ids.shape[0], N.ptr(ids, ctypes.c_int64),
+                                          N.ptr(rows, ctypes.c_double),
+                                          ctypes.byref(cols) if cols is not None else None,
+                                          N.NO_NORM_CHECK))
+        del keep
+
+    def insert_device(self, ids, rows_dev_ptr: int, meta=None) -> None:
+        """Bulk append from device memory (float64 [n, dimension], already
+        unit-norm -- e.g. a torch CUDA tensor's data_ptr())."""
+        ids = N.i64(ids)
+        cols, keep = _meta_struct(meta, ids.shape[0]) if meta is not None else (None, None)
+        with self._wlock:
+            N.check(self._lib.sine_insert_device(self._h, ids.shape[0], N.ptr(ids, ctypes.c_int64),
+                                                 ctypes.c_void_p(rows_dev_ptr),
+                                                 ctypes.byref(cols) if cols is not None else None, 0))
+        del keep
+
+    def remove(self, id: int) -> None:
+        self.remove_batch([id])
+
+    def remove_batch(self, ids) -> None:
+        ids = N.i64(ids)
+        if ids.size == 0:
+            return
+        with self._wlock:
+            N.check(self._lib.sine_remove(self._h, ids.shape[0], N.ptr(ids, ctypes.c_int64)))
+
+    def query(self, vector, k: int, min_similarity: float = -1.0) -> list[Candidate]:
+        """Reference `ExactCosineIndex.query` (index.py:94-102) on the GPU."""
+        arr = check_vector(vector, self.dimension)
+        if k < 1:
+            raise ValidationError("k must be >= 1")
+        ids, sims, counts = self._query(arr[None, :], k, min_similarity, self._mode())
+        n = int(counts[0])
+        return [Candidate(int(ids[0, j]), float(sims[0, j])) for j in range(n)]
+
+    def query_batch(self, queries, k: int, min_similarity: float = -1.0, *, scan: str | None = None,
+                    rerank: bool | None = None, check: bool = True):
+        """B independent queries in one pass over the index.
+
+        Returns (ids int64[B, k] padded with -1, sims float64[B, k],
+        counts int32[B]); row b equals query(queries[b], k, min_similarity)."""
+        q = check_matrix(queries, self.dimension) if check else N.f64(queries)
+        if k < 1:
+            raise ValidationError("k must be >= 1")
+        return self._query(q, k, min_similarity, self._mode(scan, rerank))
+
+    def _query(self, q: np.ndarray, k: int, min_similarity: float, mode: int):
+        B = q.shape[0]
+        ids = np.empty((B, k), dtype=np.int64)
+        sims = np.empty((B, k), dtype=np.float64)
+        counts = np.empty(B, dtype=np.int32)
+        N.check(self._lib.sine_query(self._h, B, N.ptr(q, ctypes.c_double), int(k), float(min_similarity),
+                                     mode, N.ptr(ids, ctypes.c_int64), N.ptr(sims, ctypes.c_double),
+                                     N.ptr(counts, ctypes.c_int32)))
+        return ids, sims, counts
+
+    def query_into(self, q: np.ndarray, k: int, min_similarity: float, ids: np.ndarray, sims: np.ndarray,
+                   counts: np.ndarray, *, scan: str | None = None, rerank: bool | None = None) -> None:
+        """query_batch writing into caller buffers (e.g. pinned host memory)."""
+        N.check(self._lib.sine_query(self._h, q.shape[0], N.ptr(q, ctypes.c_double), int(k),
+                                     float(min_similarity), self._mode(scan, rerank),
+                                     N.ptr(ids, ctypes.c_int64), N.ptr(sims, ctypes.c_double),
+                                     N.ptr(counts, ctypes.c_int32)))
+
+    def query_device(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
+                     counts_ptr: int, stream: int | None = None, *, scan: str | None = None,
+                     rerank: bool | None = None) -> None:
+        """Device-pointer variant (torch tensors); enqueued on `stream`."""
+        N.check(self._lib.sine_query_device(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
+                                            float(min_similarity), self._mode(scan, rerank),
+                                            ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
+                                            ctypes.c_void_p(counts_ptr),
+                                            ctypes.c_void_p(stream) if stream else None))
+
+    # --------------------------------------------------------- timing hooks
+    def set_timing(self, on: bool = True) -> None:
+        N.check(self._lib.sine_set_timing(self._h, 1 if on else 0))
+
+    def last_timing(self):
+        a, b, c = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+        N.check(self._lib.sine_last_timing(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def kernel_launches(self) -> int:
+        n = ctypes.c_int64()
+        N.check(self._lib.sine_kernel_launches(self._h, ctypes.byref(n)))
+        return n.value
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        N.check(self._lib.sine_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    # ----------------------------------------------------------- snapshots
+    def rows(self, ids) -> np.ndarray:
+        ids = N.i64(ids)
+        out = np.empty((ids.shape[0], self.dimension), dtype=np.float64)
+        if ids.size:
+            N.check(self._lib.sine_get_rows(self._h, ids.shape[0], N.ptr(ids, ctypes.c_int64),
+                                            N.ptr(out, ctypes.c_double)))
+        return out
+
+    def snapshot_lines(self) -> list[str]:
+        """Reference snapshot format (index.py:340-354): header + one line of
+        float-hex components per id, in slot order."""
+        ids = self.ids()
+        rows = self.rows(ids)
+        lines = [self.SNAPSHOT_MAGIC, f"dimension: {self.dimension}", f"seed: {self.seed}",
+                 f"count: {len(ids)}"]
+        for i, r in zip(ids, rows):
+            lines.append(f"{i} " + " ".join(float(c).hex() for c in r))
+        return lines
+
+    def save(self, path: str) -> None:
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write("\n".join(self.snapshot_lines()) + "\n")
+
+    @classmethod
+    def load(cls, path: str, **kwargs) -> "GpuCosineIndex":
+        with open(path, "r", encoding="utf-8") as fh:
+            lines = fh.read().splitlines()
+        dimension, seed, entries = parse_snapshot_lines(lines, cls.SNAPSHOT_MAGIC)
+        idx = cls(dimension, seed=seed, **kwargs)
+        if entries:
+            idx.insert_batch([e[0] for e in entries], np.stack([e[1] for e in entries]))
+        return idx
+
+
+def parse_snapshot_lines(lines: list[str], magic: str):
+    """Reader for the reference snapshot format (index.py:357-373)."""
+    if not lines or lines[0] != magic:
+        raise ValidationError(f"snapshot is not a {magic} file")
+    try:
+        dimension = int(lines[1].split(":", 1)[1])
+        seed = int(lines[2].split(":", 1)[1])
+        count = int(lines[3].split(":", 1)[1])
+    except (IndexError, ValueError) as exc:
+        raise ValidationError(f"malformed snapshot header: {exc}") from exc
+    body = lines[4:4 + count]
+    if len(body) != count:
+        raise ValidationError(f"snapshot count {count} does not match {len(body)} entries")
+    entries = []
+    for line in body:
+        head, _, rest = line.partition(" ")
+        vec = np.array([float.fromhex(p) for p in rest.split(" ")]) if rest else np.zeros(0)
+        entries.append((int(head), vec))
+    return dimension, seed, entries
+
+
+def _meta_struct(meta: dict, n: int):
+    """Pack LCFU metadata columns (dict of arrays, length n) for the C ABI."""
+    keep = {}
+    cols = N.MetaCols()
+    for name, kind in (("log_freq", "f"), ("log_cost", "f"), ("log_lat", "f"), ("log_stat", "f"),
+                       ("frequency", "i"), ("size_tokens", "i"), ("created_at", "f"),
+                       ("expiration_time", "f"), ("last_access", "f")):
+        a = N.f64(meta[name]) if kind == "f" else N.i64(meta[name])
+        if a.shape[0] != n:
+            raise ValidationError(f"metadata column {name} has {a.shape[0]} entries, expected {n}")
+        keep[name] = a
+        setattr(cols, name, N.ptr(a, ctypes.c_double if kind == "f" else ctypes.c_int64))
+    return cols, keep

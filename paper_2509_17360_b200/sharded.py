@@ -1,0 +1,127 @@
+"""Row-sharded Sine stage-1 across the GPUs of one box (config C).
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Every
+rank owns a contiguous-by-arrival share of the SE rows in its own
+`GpuCosineIndex`; a batch of B queries is scanned by every rank against its
+shard, each rank produces its exact local top-k (fp64 re-ranked), and one
+all-gather of the B x k (similarity, id) candidates per rank is merged on
+every rank with the reference comparator (similarity desc, id asc,
+index.py:45).  Because each local list is the exact top-k of its shard,
+the merged list equals the single-index result.
+
+Bookkeeping (id -> owner rank, rows per rank) is replicated: all ranks see
+the same insert/remove sequence (SPMD), and a new row goes to the
+least-full rank (lowest rank on ties).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import ValidationError
+
+
+def merge_topk(sims: torch.Tensor, ids: torch.Tensor, k: int):
+    """Merge per-rank candidate lists.
+
+    sims/ids: [P, B, k] (ids == -1 marks padding).  Returns (ids [B, k]
+    -1 padded, sims [B, k], counts [B]) ordered by (sim desc, id asc)."""
+    P, B, kk = sims.shape
+    s = sims.permute(1, 0, 2).reshape(B, P * kk).clone()
+    i = ids.permute(1, 0, 2).reshape(B, P * kk).clone()
+    pad = i < 0
+    s[pad] = -float("inf")
+    i_key = torch.where(pad, torch.full_like(i, torch.iinfo(torch.int64).max), i)
+    # stable two-key sort: id ascending, then similarity descending
+    o1 = torch.argsort(i_key, dim=1, stable=True)
+    s1, i1 = torch.gather(s, 1, o1), torch.gather(i_key, 1, o1)
+    o2 = torch.argsort(-s1, dim=1, stable=True)
+    s2, i2 = torch.gather(s1, 1, o2)[:, :k], torch.gather(i1, 1, o2)[:, :k]
+    valid = torch.isfinite(s2)
+    counts = valid.sum(dim=1).to(torch.int32)
+    i2 = torch.where(valid, i2, torch.full_like(i2, -1))
+    s2 = torch.where(valid, s2, torch.zeros_like(s2))
+    return i2, s2, counts
+
+
+class ShardedCosineIndex:
+    """SPMD wrapper: call every method on every rank with the same args."""
+
+    def __init__(self, local_index, group=None):
+        if not dist.is_initialized():
+            raise ValidationError("ShardedCosineIndex needs an initialised torch.distributed group")
+        self.local = local_index
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.dimension = local_index.dimension
+        self._owner: dict[int, int] = {}
+        self._rows = [0] * self.world
+
+    def __len__(self) -> int:
+        return len(self._owner)
+
+    def _place(self, n: int) -> np.ndarray:
+        owners = np.empty(n, dtype=np.int64)
+        for j in range(n):
+            r = int(np.argmin(self._rows))
+            owners[j] = r
+            self._rows[r] += 1
+        return owners
+
+    def insert_batch(self, ids, rows) -> None:
+        ids = np.asarray(ids, dtype=np.int64)
+        for i in ids.tolist():
+            if i in self._owner:
+                raise ValidationError(f"duplicate id {i}")
+        owners = self._place(ids.shape[0])
+        for i, r in zip(ids.tolist(), owners.tolist()):
+            self._owner[i] = r
+        mine = owners == self.rank
+        if mine.any():
+            self.local.insert_batch(ids[mine], np.asarray(rows)[mine])
+
+    def remove_batch(self, ids) -> None:
+        ids = [int(i) for i in ids]
+        for i in ids:
+            if i not in self._owner:
+                raise ValidationError(f"unknown id {i}")
+        mine = [i for i in ids if self._owner[i] == self.rank]
+        for i in ids:
+            self._rows[self._owner.pop(i)] -= 1
+        if mine:
+            self.local.remove_batch(mine)
+
+    def query_batch(self, queries, k: int, min_similarity: float = -1.0):
+        """Exact top-k over all shards; returns numpy (ids, sims, counts)."""
+        ids, sims, _ = self.local.query_batch(queries, k, min_similarity)
+        dev = torch.device("cuda", torch.cuda.current_device()) \
+            if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        t_ids = torch.as_tensor(ids, device=dev)
+        t_sims = torch.as_tensor(sims, device=dev)
+        B = t_ids.shape[0]
+        g_ids = torch.empty((self.world * B, k), dtype=t_ids.dtype, device=dev)
+        g_sims = torch.empty((self.world * B, k), dtype=t_sims.dtype, device=dev)
+        dist.all_gather_into_tensor(g_ids, t_ids, group=self.group)
+        dist.all_gather_into_tensor(g_sims, t_sims, group=self.group)
+        mi, ms, mc = merge_topk(g_sims.view(self.world, B, k), g_ids.view(self.world, B, k), k)
+        return mi.cpu().numpy(), ms.cpu().numpy(), mc.cpu().numpy()
+
+    def query_device(self, q: torch.Tensor, k: int, min_similarity: float = -1.0):
+        """Device-resident variant (NCCL): q is a CUDA float64 [B, d] tensor;
+        the local scan is enqueued on torch's current stream, so the
+        all-gather and the merge follow it without a host round trip."""
+        B = q.shape[0]
+        stream = torch.cuda.current_stream().cuda_stream
+        ids = torch.empty((B, k), dtype=torch.int64, device=q.device)
+        sims = torch.empty((B, k), dtype=torch.float64, device=q.device)
+        counts = torch.empty((B,), dtype=torch.int32, device=q.device)
+        self.local.query_device(B, q.data_ptr(), k, min_similarity, ids.data_ptr(), sims.data_ptr(),
+                                counts.data_ptr(), stream)
+        g_ids = torch.empty((self.world * B, k), dtype=torch.int64, device=q.device)
+        g_sims = torch.empty((self.world * B, k), dtype=torch.float64, device=q.device)
+        dist.all_gather_into_tensor(g_ids, ids, group=self.group)
+        dist.all_gather_into_tensor(g_sims, sims, group=self.group)
+        return merge_topk(g_sims.view(self.world, B, k), g_ids.view(self.world, B, k), k)

@@ -1,0 +1,280 @@
+"""Stage-1 parity on the B200: GpuCosineIndex vs the reference's own golden
+outputs (tests/golden/index_golden.json, produced by the reference) and vs
+the CPU oracle on seeded inputs.  Mirrors pkg/tests/test_index.py."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import gen_inputs as G
+from oracle import sine_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2509_17360_b200 as P
+    from paper_2509_17360_b200 import _native as N
+    if N.device_count() < 1:
+        pytest.skip("no CUDA device")
+    return P
+
+
+def _same(got, want, tol=1e-12):
+    assert [c.id for c in got] == [w[0] for w in want]
+    for c, w in zip(got, want):
+        assert c.similarity == pytest.approx(float.fromhex(w[1]), abs=tol)
+
+
+def test_validation_mirrors_reference(pkg):
+    # pkg/tests/test_index.py:36-49
+    idx = pkg.GpuCosineIndex(4)
+    idx.insert(1, G.normalize([1, 2, 3, 4]))
+    with pytest.raises(pkg.ValidationError):
+        idx.insert(1, G.normalize([1, 0, 0, 0]))
+    with pytest.raises(pkg.ValidationError):
+        idx.insert(2, [1.0, 2.0, 3.0, 4.0])
+    with pytest.raises(pkg.ValidationError):
+        idx.insert(3, G.normalize([1, 2, 3]))
+    with pytest.raises(pkg.ValidationError):
+        idx.remove(42)
+    with pytest.raises(pkg.ValidationError):
+        idx.query(G.normalize([1, 0, 0, 0]), k=0)
+    assert idx.query(G.normalize([1, 0, 0, 0]), k=3)[0].id == 1
+    assert pkg.GpuCosineIndex(4).query(G.normalize([1, 0, 0, 0]), k=3) == []
+    with pytest.raises(pkg.ValidationError):
+        pkg.GpuCosineIndex(0)
+
+
+def test_linear_trials_match_reference(pkg, index_golden):
+    for (dim, vectors, queries), gold in zip(G.linear_oracle_trials(), index_golden["linear_trials"]):
+        idx = pkg.GpuCosineIndex(dim)
+        for i, v in vectors.items():
+            idx.insert(i, v)
+        for (q, k, ms), want in zip(queries, gold["results"]):
+            _same(idx.query(q, k=k, min_similarity=ms), want)
+
+
+def test_tie_order(pkg, index_golden):
+    v = G.normalize([1, 2, 3, 4, 5, 6, 7, 8])
+    idx = pkg.GpuCosineIndex(8)
+    for i in (9, 3, 7, 1):
+        idx.insert(i, v)
+    _same(idx.query(v, k=4), index_golden["tie_order"])
+
+
+def test_remove_steps(pkg, index_golden):
+    dim, vectors, steps = G.remove_case()
+    idx = pkg.GpuCosineIndex(dim)
+    for i, v in vectors.items():
+        idx.insert(i, v)
+    for (i, q), gold in zip(steps, index_golden["remove_steps"]):
+        idx.remove(i)
+        _same(idx.query(q, k=10), gold["result"])
+        assert sorted(idx.ids()) == sorted(gold["ids"])
+    assert len(idx) == 35
+
+
+def test_acceptance_9b(pkg, index_golden):
+    dim, stored, queries = G.acceptance_9b_case()
+    idx = pkg.GpuCosineIndex(dim, seed=3)
+    idx.insert_batch(list(stored), np.asarray(list(stored.values())))
+    for q, want in zip(queries, index_golden["acceptance_9b"]["results"]):
+        _same(idx.query(q, 7), want)
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_config_a_exact_modes(pkg, index_golden, scan):
+    """Config A (10k x 384, k=5) at tau 0.9 and -1: fp32 and bf16 scans with
+    the fp64 re-rank both reproduce the reference ids and similarities."""
+    rows, qs = G.config_a()
+    idx = pkg.GpuCosineIndex(rows.shape[1], scan=scan)
+    idx.insert_batch(np.arange(rows.shape[0]), rows)
+    for ms in (0.9, -1.0):
+        gold = index_golden["config_a"]["results"][repr(ms)]
+        ids, sims, counts = idx.query_batch(qs, 5, ms)
+        for j, want in enumerate(gold):
+            assert ids[j, :counts[j]].tolist() == [w[0] for w in want], (ms, j)
+            np.testing.assert_allclose(sims[j, :counts[j]], [float.fromhex(w[1]) for w in want],
+                                       atol=1e-12, rtol=0)
+            assert (ids[j, counts[j]:] == -1).all()
+
+
+def test_config_a_bf16_raw_scores(pkg, index_golden):
+    """bf16 fast mode without re-rank: scores within 2e-2, recall stated."""
+    rows, qs = G.config_a()
+    idx = pkg.GpuCosineIndex(rows.shape[1], scan="bf16", rerank=False)
+    idx.insert_batch(np.arange(rows.shape[0]), rows)
+    gold = index_golden["config_a"]["results"][repr(-1.0)]
+    ids, sims, counts = idx.query_batch(qs, 5, -1.0)
+    exact = rows @ qs.T
+    hit = tot = 0
+    for j, want in enumerate(gold):
+        wids = [w[0] for w in want]
+        hit += len(set(ids[j, :counts[j]].tolist()) & set(wids))
+        tot += len(wids)
+        for i, s in zip(ids[j, :counts[j]], sims[j, :counts[j]]):
+            assert abs(s - exact[i, j]) < 2e-2
+    recall = hit / tot
+    print(f"bf16 (no re-rank) recall@5 on config A: {recall:.4f}")
+    assert recall >= 0.95
+
+
+def test_ties_under_shuffled_ids(pkg, index_golden):
+    d, rows, ids, qs = G.tie_rows()
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(ids, rows)
+        for k, res in index_golden["ties"]["results"].items():
+            for q, want in zip(qs, res):
+                _same(idx.query(q, int(k)), want)
+
+
+def test_batch_equals_independent_queries(pkg):
+    rng = np.random.default_rng(11)
+    n, d = 3000, 96
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((37, d))
+    q[::3] = rows[::300][: len(q[::3])]
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    idx = pkg.GpuCosineIndex(d)
+    idx.insert_batch(rng.permutation(10 * n)[:n], rows)
+    ids, sims, counts = idx.query_batch(q, 9, 0.05)
+    for j in range(q.shape[0]):
+        one = idx.query(q[j], 9, 0.05)
+        assert [c.id for c in one] == ids[j, :counts[j]].tolist()
+        assert [c.similarity for c in one] == sims[j, :counts[j]].tolist()
+
+
+def test_nan_rows_never_match_and_k_larger_than_n(pkg):
+    idx = pkg.GpuCosineIndex(3)
+    # the reference admits a NaN vector (|nan - 1| > tol is False) but it
+    # never passes `sims >= min_similarity`
+    idx.insert(5, [float("nan"), 0.0, 0.0])
+    idx.insert(6, G.normalize([1, 1, 0]))
+    got = idx.query(G.normalize([1, 0, 0]), k=10, min_similarity=-1.0)
+    assert [c.id for c in got] == [6]
+    assert got[0].similarity == pytest.approx(1 / math.sqrt(2), abs=1e-15)
+
+
+def test_removal_compaction_and_reinsert(pkg):
+    rng = np.random.default_rng(3)
+    n, d = 2000, 40
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    idx = pkg.GpuCosineIndex(d)
+    idx.insert_batch(np.arange(n), rows)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    gone = rng.permutation(n)[:1500]          # forces several compactions
+    for i in gone[:700]:
+        idx.remove(int(i))
+        ora.remove(int(i))
+    idx.remove_batch(gone[700:])
+    for i in gone[700:]:
+        ora.remove(int(i))
+    fresh = rng.standard_normal((300, d))
+    fresh /= np.linalg.norm(fresh, axis=1, keepdims=True)
+    idx.insert_batch(np.arange(n, n + 300), fresh)
+    ora.bulk_load(np.arange(n, n + 300), fresh)
+    assert sorted(idx.ids()) == sorted(ora.ids()) and len(idx) == len(ora)
+    for j in range(20):
+        q = rows[j] if j % 2 else fresh[j]
+        got = idx.query(q, 12, -1.0)
+        want = ora.query(q, 12, -1.0)
+        assert [c.id for c in got] == [c.id for c in want]
+        np.testing.assert_allclose([c.similarity for c in got], [c.similarity for c in want], atol=1e-12)
+    with pytest.raises(pkg.ValidationError):
+        idx.remove(int(gone[0]))
+    with pytest.raises(pkg.ValidationError):
+        idx.insert_batch([n + 5], fresh[:1])
+
+
+def test_snapshot_round_trip(pkg, tmp_path):
+    rng = np.random.default_rng(31)
+    idx = pkg.GpuCosineIndex(6, seed=4)
+    vecs = rng.standard_normal((12, 6))
+    vecs /= np.linalg.norm(vecs, axis=1, keepdims=True)
+    idx.insert_batch(np.arange(12), vecs)
+    idx.remove(3)
+    p = str(tmp_path / "x.idx")
+    idx.save(p)
+    loaded = pkg.GpuCosineIndex.load(p)
+    assert loaded.dimension == 6 and loaded.seed == 4
+    assert sorted(loaded.ids()) == sorted(idx.ids())
+    assert loaded.rows([5]).tobytes() == vecs[5].tobytes()  # bit-exact rows
+    q = vecs[0]
+    assert [(c.id, c.similarity) for c in loaded.query(q, 5)] == [(c.id, c.similarity) for c in idx.query(q, 5)]
+    lines = open(p).read().splitlines()
+    assert lines[0] == "exact-cosine-index" and lines[3] == "count: 11"
+
+
+@pytest.mark.parametrize("d", [1, 5, 127, 128, 129, 384, 768, 1024, 1536, 2048])
+def test_dimension_sweep(pkg, d):
+    rng = np.random.default_rng(d)
+    n = 700
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((5, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(np.arange(n), rows)
+        ids, sims, counts = idx.query_batch(q, 7, -1.0)
+        for j in range(5):
+            want = ora.query(q[j], 7, -1.0)
+            assert ids[j, :counts[j]].tolist() == [c.id for c in want], (scan, d, j)
+            np.testing.assert_allclose(sims[j, :counts[j]], [c.similarity for c in want], atol=1e-12)
+
+
+def test_large_batch_groups(pkg):
+    """B > the per-launch query group: several scan launches, same answers."""
+    rng = np.random.default_rng(8)
+    n, d, B = 5000, 128, 70
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((B, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(np.arange(n), rows)
+        ids, sims, counts = idx.query_batch(q, 20, 0.1)
+        for j in range(B):
+            want = ora.query(q[j], 20, 0.1)
+            assert ids[j, :counts[j]].tolist() == [c.id for c in want]
+
+
+def test_full_size_properties(pkg):
+    """BASELINE config B shape (1M x 768, k=10): sampled queries against the
+    float64 oracle; planted duplicates must come back as rank 1 with
+    similarity 1."""
+    import torch
+    n, d, k = 1_000_000, 768, 10
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn((n, d), dtype=torch.float64, device="cuda", generator=g)
+    x /= x.norm(dim=1, keepdim=True)
+    idx = pkg.GpuCosineIndex(d, store_bf16=True, capacity=n)
+    idx.insert_device(np.arange(n), x.data_ptr())
+    rows = x.cpu().numpy()
+    rng = np.random.default_rng(2)
+    pick = rng.integers(0, n, 8)
+    q = np.concatenate([rows[pick], rng.standard_normal((8, d))])
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    for scan in ("fp32", "bf16"):
+        ids, sims, counts = idx.query_batch(q, k, -1.0, scan=scan)
+        for j in range(16):
+            s = rows @ q[j]
+            order = np.lexsort((np.arange(n), -s))[:k]
+            assert ids[j].tolist() == order.tolist(), (scan, j)
+            np.testing.assert_allclose(sims[j], s[order], atol=1e-12)
+            if j < 8:
+                assert ids[j, 0] == pick[j] and sims[j, 0] == pytest.approx(1.0, abs=1e-12)
