@@ -1,0 +1,369 @@
+"""Sine stage-1 benchmark (BASELINE.json metric): lookups/sec on 1M SEs x
+d=768, k=10, as absolute throughput and as a fraction of the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B]
+                    [--scan fp32|bf16] [--impl ours|reference]
+
+One step = one batch of B queries through the full stage-1 pipeline (scan +
+merge + fp64 re-rank), i.e. `ExactCosineIndex.query` for B queries.
+N=1: the whole 1M-row index on one GPU.  N>1 (torchrun): the same 1M rows
+row-sharded over N ranks, every rank scans its shard for the same batch and
+the candidates are merged after an NCCL all-gather (strong scaling).
+
+`--impl reference` times the reference algorithm's CPU path (oracle/, the
+numpy float64 restatement of ExactCosineIndex.query) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ROWS, DIM, K = 1_000_000, 768, 10
+TAU = 0.9  # CacheConfig.tau_sim default, the value every engine call site passes
+METRIC = "Sine lookups/sec (1M SEs, d=768, k=10)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--scan", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=N_ROWS)
+    ap.add_argument("--no-regimes", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def make_rows(n, d, seed=1):
+    """Synthetic SE embeddings: standard-normal rows normalised in float64."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, d))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    return x
+
+
+def make_queries(rows, b, seed):
+    """Half planted near-duplicates (cos in [0.88, 0.99], straddling tau),
+    half fresh random unit vectors."""
+    rng = np.random.default_rng(seed)
+    n, d = rows.shape
+    q = rng.standard_normal((b, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    for j in range(0, b, 2):
+        x = rows[rng.integers(0, n)]
+        g = rng.standard_normal(d)
+        g -= (g @ x) * x
+        g /= np.linalg.norm(g)
+        c = rng.uniform(0.88, 0.99)
+        q[j] = c * x + math.sqrt(1 - c * c) * g
+        q[j] /= np.linalg.norm(q[j])
+    return q
+
+
+def algorithmic_bytes(n, d, b, k, scan):
+    """Bytes one stage-1 batch must move: the index rows once, the validity
+    bitmap, the fp64 queries, and the k results per query."""
+    e = 4 if scan == "fp32" else 2
+    return n * d * e + n / 8 + b * d * 8 + b * k * 16
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for _, _, flags in rows for n, f in zip(names, flags) if f.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- CPU arm
+
+def cpu_lookups(rows, queries, k, tau):
+    """The reference CPU path (oracle restatement of ExactCosineIndex.query:
+    float64 GEMV over all rows + inclusive threshold + (-sim, id) lexsort)."""
+    from oracle import sine_oracle as O
+    idx = O.OracleExactIndex(rows.shape[1], capacity=1)
+    idx._buf = rows  # direct population
+    idx._ids = list(range(rows.shape[0]))
+    t0 = time.perf_counter()
+    for q in queries:
+        idx.query(q, k, tau)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rows = make_rows(args.rows, DIM)
+    b = args.batch
+    per_step = max(1, min(b, 4))  # bounded sample: <= 4 lookups of the batch per step
+    qs = make_queries(rows, per_step * (args.steps + args.warmup), seed=7)
+    for s in range(args.warmup):
+        cpu_lookups(rows, qs[s * per_step:(s + 1) * per_step], K, TAU)
+    t = 0.0
+    for s in range(args.warmup, args.warmup + args.steps):
+        t += cpu_lookups(rows, qs[s * per_step:(s + 1) * per_step], K, TAU)
+    n = per_step * args.steps
+    value = n / t
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: standard-normal rows normalised in float64, seed 1; half planted near-dups",
+            "config": {"workload": f"config B: {args.rows} SEs x d={DIM}, k={K}, min_similarity={TAU}",
+                       "batch": b, "sampled_lookups_per_step": per_step},
+            "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": cores, "kind": "port",
+                             "sample": f"{n} lookups (numpy float64 GEMV + lexsort, all host threads)"},
+            "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args):
+    import torch
+    from paper_2509_17360_b200 import GpuCosineIndex
+    from paper_2509_17360_b200 import _native as Nat
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    hbm_peak, _, peak_kind = peaks()
+
+    rows = make_rows(args.rows, DIM)
+    lo, hi = rank * args.rows // world, (rank + 1) * args.rows // world
+    idx = GpuCosineIndex(DIM, device=local, scan=args.scan, store_f32=True, store_bf16=True,
+                         capacity=hi - lo)
+    idx.insert_batch(np.arange(lo, hi), rows[lo:hi], _checked=True)
+    shard_rows = hi - lo
+
+    b = args.batch
+    nsteps = args.warmup + args.steps
+    qs = make_queries(rows, b * nsteps, seed=11).reshape(nsteps, b, DIM)
+    q_dev = torch.from_numpy(qs).to(f"cuda:{local}")
+    ids_d = torch.empty((b, K), dtype=torch.int64, device=q_dev.device)
+    sims_d = torch.empty((b, K), dtype=torch.float64, device=q_dev.device)
+    cnt_d = torch.empty((b,), dtype=torch.int32, device=q_dev.device)
+
+    if world > 1:
+        from paper_2509_17360_b200.sharded import ShardedCosineIndex
+        sh = ShardedCosineIndex(idx)
+        sh._rows = [(r + 1) * args.rows // world - r * args.rows // world for r in range(world)]
+
+        def step(s):
+            sh.query_device(q_dev[s], K, TAU)
+    else:
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def step(s):
+            idx.query_device(b, q_dev[s].data_ptr(), K, TAU, ids_d.data_ptr(), sims_d.data_ptr(),
+                             cnt_d.data_ptr(), stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        step(s)
+    barrier()
+    launches0 = idx.kernel_launches()
+    idx.set_timing(True)
+    idx.timing_totals(0, reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record()
+        for s in range(args.warmup, nsteps):
+            step(s)
+        ev1.record()
+        barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    scan_ms, scan_n = idx.timing_totals(0, reset=False)
+    merge_ms, merge_n = idx.timing_totals(1, reset=True)
+    idx.set_timing(False)
+    launches = idx.kernel_launches() - launches0
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], device=q_dev.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = b * args.steps / (elapsed_ms / 1e3)
+
+    # dominant kernel: the stage-1 scan, per launch
+    scan_avg_ms = scan_ms / max(scan_n, 1)
+    launches_per_step = scan_n / args.steps
+    q_per_launch = b / launches_per_step
+    bytes_per_launch = algorithmic_bytes(shard_rows, DIM, q_per_launch, K, args.scan)
+    achieved = bytes_per_launch / (scan_avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                "kernel": "scan_kernel", "kernel_ms": scan_avg_ms,
+                "scan_share_of_step": scan_ms / max(elapsed_ms, 1e-9),
+                "bytes_per_launch": bytes_per_launch, "frac_of_nominal_8tbs": achieved / 8000.0}
+
+    # e2e through the public API with pinned host buffers (H2D + D2H inside)
+    e2e = None
+    if world == 1:
+        qh = Nat.PinnedArray((b, DIM), np.float64)
+        oi = Nat.PinnedArray((b, K), np.int64)
+        os_ = Nat.PinnedArray((b, K), np.float64)
+        oc = Nat.PinnedArray((b,), np.int32)
+        for s in range(args.warmup):
+            qh.array[:] = qs[s]
+            idx.query_into(qh.array, K, TAU, oi.array, os_.array, oc.array)
+        t0 = time.perf_counter()
+        for s in range(args.warmup, nsteps):
+            qh.array[:] = qs[s]
+            idx.query_into(qh.array, K, TAU, oi.array, os_.array, oc.array)
+        t_e2e = time.perf_counter() - t0
+        e2e = {"value": b * args.steps / t_e2e, "unit": "lookups/s", "h2d_bytes_per_step": b * DIM * 8,
+               "d2h_bytes_per_step": b * K * 16 + b * 4,
+               "api": "GpuCosineIndex.query_into (sine_query C ABI), pinned host buffers"}
+
+    regimes = []
+    if world == 1 and not args.no_regimes:
+        regimes = measure_regimes(idx, rows, torch, hbm_peak)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sample = make_queries(rows, 48, seed=5)
+        t = cpu_lookups(rows, sample, K, TAU)
+        cpu = {"value": len(sample) / t, "unit": "lookups/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{len(sample)} lookups of config B via oracle/ (numpy float64 GEMV + lexsort, "
+                         "all host threads)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.scan == "fp32" else "bf16",
+                "data": "synthetic: standard-normal rows normalised in float64 (seed 1); queries half planted "
+                        "near-duplicates (cos 0.88-0.99), half random",
+                "config": {"workload": f"config B: {args.rows} SEs x d={DIM}, k={K}, batch {b}, "
+                                       f"min_similarity={TAU} (tau_sim), {args.scan} scan + fp64 re-rank",
+                           "rows": args.rows, "dim": DIM, "k": K, "batch": b, "scan": args.scan,
+                           "rows_per_gpu": shard_rows,
+                           "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
+                           "l2": "no flush: the index (>= 1.5 GB) exceeds the 126 MB L2"},
+                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+                "gpu_launches": int(launches), "regimes": regimes}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def measure_regimes(idx, rows, torch, hbm_peak):
+    """Config B's three batch regimes x both scan modes (device timing)."""
+    out = []
+    stream = torch.cuda.current_stream().cuda_stream
+    for scan in ("fp32", "bf16"):
+        for b, reps in ((1, 20), (64, 5), (4096, 1)):
+            for tau in (TAU, -1.0):
+                if b == 4096 and tau == -1.0:
+                    continue
+                qs = make_queries(rows, b, seed=100 + b)
+                q = torch.from_numpy(qs).cuda()
+                ids = torch.empty((b, K), dtype=torch.int64, device="cuda")
+                sims = torch.empty((b, K), dtype=torch.float64, device="cuda")
+                cnt = torch.empty((b,), dtype=torch.int32, device="cuda")
+                run = lambda: idx.query_device(b, q.data_ptr(), K, tau, ids.data_ptr(), sims.data_ptr(),  # noqa
+                                               cnt.data_ptr(), stream, scan=scan)
+                run()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    run()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                n = rows.shape[0]
+                byt = algorithmic_bytes(n, DIM, b, K, scan)
+                flops = 2.0 * n * DIM * b
+                out.append({"batch": b, "scan": scan, "min_similarity": tau, "ms_per_batch": ms,
+                            "lookups_per_s": b / (ms / 1e3),
+                            "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
+                            "tflops": flops / (ms / 1e3) / 1e12})
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

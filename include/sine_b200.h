@@ -128,6 +128,10 @@ int sine_stream(sine_index_t *h, void **stream);
 int sine_set_timing(sine_index_t *h, int on);
 int sine_last_timing(sine_index_t *h, float *scan_ms, float *merge_ms, float *evict_ms);
 int sine_kernel_launches(sine_index_t *h, int64_t *n);
+/* Sum of device time (ms) and count of the launches of one kernel kind
+ * (0 = stage-1 scan, 1 = merge/re-rank, 2 = tensor-core scan) recorded
+ * while timing was on; reset != 0 clears the record. */
+int sine_timing_totals(sine_index_t *h, int kind, double *total_ms, int64_t *launches, int reset);
 
 int sine_host_alloc(size_t bytes, void **p);
 int sine_host_free(void *p);

@@ -139,6 +139,13 @@ struct sine_index {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
     bool timing = false;
+    // accumulated per-kernel device time (CUDA events on the launch stream)
+    struct Timed {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int kind = 0;
+    };
+    std::vector<Timed> tpool;
+    size_t tused = 0;
     float t_scan = 0.f, t_merge = 0.f, t_evict = 0.f;
     int64_t launches = 0;
     std::mutex mu;
@@ -443,6 +450,24 @@ void record(sine_index* h, int i, cudaStream_t st) {
     if (h->timing) CK(cudaEventRecord(h->ev[i], st));
 }
 
+// kind 0 = scan kernel, 1 = merge kernel, 2 = tensor-core scan
+size_t tbegin(sine_index* h, int kind, cudaStream_t st) {
+    if (!h->timing) return SIZE_MAX;
+    if (h->tused == h->tpool.size()) {
+        sine_index::Timed t;
+        CK(cudaEventCreate(&t.a));
+        CK(cudaEventCreate(&t.b));
+        h->tpool.push_back(t);
+    }
+    auto& t = h->tpool[h->tused];
+    t.kind = kind;
+    CK(cudaEventRecord(t.a, st));
+    return h->tused++;
+}
+void tend(sine_index* h, size_t i, cudaStream_t st) {
+    if (i != SIZE_MAX) CK(cudaEventRecord(h->tpool[i].b, st));
+}
+
 // tcgen05 path (large batches) -- not yet enabled
 bool umma_eligible(const sine_index*, int64_t, bool, uint32_t) { return false; }
 void umma_query(sine_index*, int64_t, const double*, int, int, float, double, bool, int64_t*, double*, int32_t*,
@@ -457,8 +482,8 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
     if (B <= 0) return;
     const bool bf16 = (mode & 0xF) == SINE_SCAN_BF16;
     const bool rerank = (mode & SINE_RERANK_F64) != 0;
-    if (bf16 && !h->rows16) fail(SINE_EINVAL, "index has no bf16 rows (create with SINE_STORE_BF16)");
-    if (!bf16 && !h->rows32) fail(SINE_EINVAL, "index has no fp32 rows (create with SINE_STORE_F32)");
+    if (bf16 && !(h->flags & SINE_STORE_BF16)) fail(SINE_EINVAL, "index has no bf16 rows (create with SINE_STORE_BF16)");
+    if (!bf16 && !(h->flags & SINE_STORE_F32)) fail(SINE_EINVAL, "index has no fp32 rows (create with SINE_STORE_F32)");
     int kp = rerank ? k + kSlack : k;
     if (kp > kMaxKp) {
         if (k > kMaxKp) fail(SINE_EINVAL, "k > 128 is not supported by the device top-k");
@@ -528,6 +553,7 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         if (L.total > 227 * 1024) fail(SINE_EINVAL, "scan shared-memory plan exceeds 227 KB");
         const int threads = (c.CW * c.G + 1) * 32;
         record(h, 0, st);
+        const size_t tk = tbegin(h, 0, st);
         if (bf16) {
             if (c.CPW == 1)
                 launch_scan_nq<__nv_bfloat16, 1>(NQ, p, grid, threads, L.total, st);
@@ -541,6 +567,7 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         }
         ++h->launches;
         CK(cudaGetLastError());
+        tend(h, tk, st);
         record(h, 1, st);
         MergeParams m{};
         m.in_key = h->lkey.p;
@@ -559,7 +586,9 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         m.out_ids = ids_dev + q0 * k;
         m.out_sims = sims_dev + q0 * k;
         m.out_counts = counts_dev + q0;
+        const size_t tm = tbegin(h, 1, st);
         merge_kernel<<<nq, kMergeThreads, 0, st>>>(m);
+        tend(h, tm, st);
         ++h->launches;
         CK(cudaGetLastError());
         record(h, 2, st);
@@ -1018,6 +1047,26 @@ int sine_last_timing(sine_index_t* h, float* scan_ms, float* merge_ms, float* ev
         if (scan_ms) *scan_ms = h->t_scan;
         if (merge_ms) *merge_ms = h->t_merge;
         if (evict_ms) *evict_ms = h->t_evict;
+    });
+}
+
+int sine_timing_totals(sine_index_t* h, int kind, double* total_ms, int64_t* launches, int reset) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        double tot = 0.0;
+        int64_t n = 0;
+        for (size_t i = 0; i < h->tused; ++i) {
+            auto& t = h->tpool[i];
+            if (t.kind != kind) continue;
+            CK(cudaEventSynchronize(t.b));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, t.a, t.b));
+            tot += ms;
+            ++n;
+        }
+        *total_ms = tot;
+        *launches = n;
+        if (reset) h->tused = 0;
     });
 }
 

@@ -100,7 +100,7 @@ __host__ __device__ inline ScanSmemLayout scan_smem_layout(int S, int R, int64_t
     L.qstate_off = off;  // cnt[NQ], worst[NQ], thr[NQ]
     off += align_up(3 * NQ * sizeof(uint32_t), 16);
     L.pend_off = off;  // 2 x { total, cnt[NQ], entries[NQ][R] {slot, key} }
-    off += 2 * align_up((1 + NQ) * sizeof(uint32_t) + static_cast<size_t>(NQ) * R * 8, 16);
+    off += 2 * align_up(align_up((1 + NQ) * sizeof(uint32_t), 16) + static_cast<size_t>(NQ) * R * 8, 16);
     L.total = off;
     return L;
 }
@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(9 * 32, 1) scan_kernel(const ScanParams p) {
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.qstate_off);
     uint32_t* worst = cnt + NQ;
     uint32_t* thr = worst + NQ;
-    const size_t pend_bytes = align_up((1 + NQ) * sizeof(uint32_t) + static_cast<size_t>(NQ) * R * 8, 16);
+    const size_t pend_hdr = align_up((1 + NQ) * sizeof(uint32_t), 16);  // keeps the uint2 entries 8-B aligned
+    const size_t pend_bytes = align_up(pend_hdr + static_cast<size_t>(NQ) * R * 8, 16);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * p.rows_per_cta;
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(9 * 32, 1) scan_kernel(const ScanParams p) {
             uint32_t* pend = reinterpret_cast<uint32_t*>(smem + L.pend_off + (i & 1) * pend_bytes);
             uint32_t* pend_total = pend;
             uint32_t* pend_cnt = pend + 1;
-            uint2* pend_e = reinterpret_cast<uint2*>(pend + 1 + NQ);
+            uint2* pend_e = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(pend) + pend_hdr);
             for (int t = tid; t < rows_i * nq; t += nthreads) {
                 const int r = t / nq, jq = t - r * nq;
                 const float* pr = partial + (r * NQ + jq) * C;

@@ -226,6 +226,13 @@ class GpuCosineIndex:
         N.check(self._lib.sine_last_timing(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return a.value, b.value, c.value
 
+    def timing_totals(self, kind: int = 0, reset: bool = True):
+        """(total device ms, launches) of kernel kind 0=scan, 1=merge, 2=umma."""
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        N.check(self._lib.sine_timing_totals(self._h, kind, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
+        return ms.value, n.value
+
     def kernel_launches(self) -> int:
         n = ctypes.c_int64()
         N.check(self._lib.sine_kernel_launches(self._h, ctypes.byref(n)))
