@@ -38,7 +38,7 @@ METRIC = "Sine lookups/sec (1M SEs, d=768, k=10)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--scan", default="fp32", choices=["fp32", "bf16"])
@@ -105,7 +105,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
@@ -215,6 +215,10 @@ def run_ours(args):
     sims_d = torch.empty((b, K), dtype=torch.float64, device=q_dev.device)
     cnt_d = torch.empty((b,), dtype=torch.int32, device=q_dev.device)
 
+    # all device work runs on one non-default torch stream: the library
+    # launches onto it, and the CUDA events below time exactly that stream
+    work = torch.cuda.Stream()
+    torch.cuda.set_stream(work)
     if world > 1:
         from paper_2509_17360_b200.sharded import ShardedCosineIndex
         sh = ShardedCosineIndex(idx)
@@ -223,7 +227,7 @@ def run_ours(args):
         def step(s):
             sh.query_device(q_dev[s], K, TAU)
     else:
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = work.cuda_stream
 
         def step(s):
             idx.query_device(b, q_dev[s].data_ptr(), K, TAU, ids_d.data_ptr(), sims_d.data_ptr(),
@@ -243,6 +247,13 @@ def run_ours(args):
     idx.timing_totals(0, reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        t_spin = time.perf_counter()
+        while time.perf_counter() - t_spin < 1.0:  # sampler start-up; GPU kept busy, untimed
+            step(s % max(args.warmup, 1))
+            torch.cuda.synchronize()
+        idx.timing_totals(0, reset=True)
+        idx.timing_totals(1, reset=True)
+        launches0 = idx.kernel_launches()
         barrier()
         ev0.record()
         for s in range(args.warmup, nsteps):
@@ -326,6 +337,7 @@ def measure_regimes(idx, rows, torch, hbm_peak):
     """Config B's three batch regimes x both scan modes (device timing)."""
     out = []
     stream = torch.cuda.current_stream().cuda_stream
+    assert stream, "regimes must run on a non-default stream"
     for scan in ("fp32", "bf16"):
         for b, reps in ((1, 20), (64, 5), (4096, 1)):
             for tau in (TAU, -1.0):
@@ -333,6 +345,7 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                     continue
                 qs = make_queries(rows, b, seed=100 + b)
                 q = torch.from_numpy(qs).cuda()
+                torch.cuda.synchronize()
                 ids = torch.empty((b, K), dtype=torch.int64, device="cuda")
                 sims = torch.empty((b, K), dtype=torch.float64, device="cuda")
                 cnt = torch.empty((b,), dtype=torch.int32, device="cuda")

@@ -403,23 +403,30 @@ void compact(sine_index* h) {
 // ------------------------------------------------------------ query pipeline
 
 struct ScanCfg {
-    int C, CPW, CW, G, R, S, NQmax;
+    int C, CPW, CW, G, U, R, NQmax;
     int64_t row_bytes;
 };
 
-ScanCfg scan_cfg(const sine_index* h, bool bf16) {
+int unroll_for(int NQ) { return NQ == 1 ? 8 : NQ == 2 ? 4 : NQ == 4 ? 2 : 1; }
+
+// Launch geometry of the streaming scan for a query group of size NQ
+// (must agree with ScanWarps / ScanUnroll in scan.cuh).
+ScanCfg scan_cfg(const sine_index* h, bool bf16, int NQ) {
     ScanCfg c{};
     c.row_bytes = bf16 ? h->stride16 * 2 : h->stride32 * 4;
     c.C = static_cast<int>((c.row_bytes + 511) / 512);
     c.CPW = c.C <= 8 ? 1 : 2;
     if (c.C > 16) fail(SINE_EINVAL, "dimension too large for the streaming scan (max 2048 fp32 / 4096 bf16)");
     c.CW = (c.C + c.CPW - 1) / c.CPW;
-    c.G = std::max(1, 8 / c.CW);
-    c.R = 32;
-    while (c.R > 1 && c.R * c.row_bytes > 24576) c.R /= 2;
-    c.R = std::max(c.R, c.G);
     const int epl = bf16 ? 8 : 4;
     c.NQmax = std::min(16, 64 / (epl * c.CPW));
+    if (NQ > 0) {
+        const int maxW = NQ >= 8 ? 8 : 16;
+        c.U = unroll_for(NQ);
+        c.G = std::max(1, maxW / c.CW);
+        while (c.G > 1 && c.G * c.U > 64) --c.G;
+        c.R = c.G * c.U;
+    }
     return c;
 }
 
@@ -512,18 +519,19 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         return;
     }
 
-    const ScanCfg c = scan_cfg(h, bf16);
-    const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(h->num_sms, (h->nslots + c.R - 1) / c.R)));
-    const int64_t rows_per_cta = round_up((h->nslots + grid - 1) / grid, c.R);
-    h->lkey.ensure(static_cast<size_t>(grid) * c.NQmax * kp);
-    h->lslot.ensure(static_cast<size_t>(grid) * c.NQmax * kp);
-    h->ln.ensure(static_cast<size_t>(grid) * c.NQmax);
+    const int NQmax = scan_cfg(h, bf16, 0).NQmax;
+    h->lkey.ensure(static_cast<size_t>(h->num_sms) * NQmax * kp);
+    h->lslot.ensure(static_cast<size_t>(h->num_sms) * NQmax * kp);
+    h->ln.ensure(static_cast<size_t>(h->num_sms) * NQmax);
 
-    for (int64_t q0 = 0; q0 < B; q0 += c.NQmax) {
-        const int nq = static_cast<int>(std::min<int64_t>(c.NQmax, B - q0));
+    for (int64_t q0 = 0; q0 < B; q0 += NQmax) {
+        const int nq = static_cast<int>(std::min<int64_t>(NQmax, B - q0));
         int NQ = 1;
         while (NQ < nq) NQ <<= 1;
+        const ScanCfg c = scan_cfg(h, bf16, NQ);
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(h->num_sms, (h->nslots + c.R - 1) / c.R)));
+        const int64_t rows_per_cta = round_up((h->nslots + grid - 1) / grid, c.R);
         ScanParams p{};
         p.rows = bf16 ? reinterpret_cast<const uint8_t*>(h->rows16) : reinterpret_cast<const uint8_t*>(h->rows32);
         p.row_bytes = c.row_bytes;
@@ -540,13 +548,14 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         p.chunks = c.C;
         p.chunk_warps = c.CW;
         p.row_groups = c.G;
+        p.unroll = c.U;
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
         // stages: fill ~200 KB of shared memory
         const ScanSmemLayout L0 = scan_smem_layout(0, c.R, c.row_bytes, NQ, c.C, kp);
         const size_t stage_bytes = static_cast<size_t>(c.R) * c.row_bytes;
-        int S = static_cast<int>(std::min<size_t>(8, (200 * 1024 - L0.total) / stage_bytes));
+        int S = static_cast<int>(std::min<size_t>(8, (208 * 1024 - L0.total) / stage_bytes));
         S = std::max(S, 2);
         p.stages = S;
         const ScanSmemLayout L = scan_smem_layout(S, c.R, c.row_bytes, NQ, c.C, kp);

@@ -35,12 +35,13 @@ struct ScanParams {
     int nq;                 // queries in this launch (<= NQ)
     int kp;                 // per-CTA list capacity
     float thr0;             // admission floor (min_sim, or min_sim - margin)
-    int rows_per_stage;     // R: power of two <= 32
+    int rows_per_stage;     // R = G * U (<= 64)
     int stages;             // S
     int64_t rows_per_cta;   // multiple of R
     int chunks;             // C = ceil(row_bytes / 512)
     int chunk_warps;        // CW = ceil(C / CPW)
     int row_groups;         // G
+    int unroll;             // U: rows per warp per stage (R = G * U)
     uint32_t* out_key;      // [grid][nq][kp] f32_key(score)
     int32_t* out_slot;      // [grid][nq][kp]
     int32_t* out_n;         // [grid][nq]
@@ -154,13 +155,27 @@ __device__ __forceinline__ int list_worst(const uint32_t* lkey, const int32_t* l
     return pos;
 }
 
+// Compute warps per CTA: up to 16 for small query groups (more rows in
+// flight), 8 when the per-thread query slice is large (register budget).
+template <int NQ>
+struct ScanWarps {
+    static constexpr int kMax = NQ >= 8 ? 8 : 16;
+    static constexpr int kThreads = (kMax + 1) * 32;
+};
+// rows each warp keeps in flight per stage (independent FMA/shuffle chains)
+template <int NQ>
+struct ScanUnroll {
+    static constexpr int kU = NQ == 1 ? 8 : NQ == 2 ? 4 : NQ == 4 ? 2 : 1;
+};
+
 template <typename RowT, int NQ, int CPW>
-__global__ void __launch_bounds__(9 * 32, 1) scan_kernel(const ScanParams p) {
+__global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const ScanParams p) {
     using T = RowTraits<RowT>;
     constexpr int EPL = T::kEPL;
     constexpr int M = (NQ == 1) ? 0 : (NQ == 2) ? 1 : (NQ == 4) ? 2 : (NQ == 8) ? 3 : 4;
 
     extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int U = ScanUnroll<NQ>::kU;
     const int S = p.stages, R = p.rows_per_stage, C = p.chunks, CW = p.chunk_warps,
               G = p.row_groups;
     const int W = CW * G;  // compute warps; warp W is the producer
@@ -239,51 +254,81 @@ __global__ void __launch_bounds__(9 * 32, 1) scan_kernel(const ScanParams p) {
             const int s = i % S;
             const int64_t rbase = row0 + static_cast<int64_t>(i) * R;
             const int rows_i = static_cast<int>(min(static_cast<int64_t>(R), row_end - rbase));
-            const uint32_t vword = __ldg(p.valid + (rbase >> 5));  // R | 32 and rbase % R == 0
+            // validity bits of the (row, query) items this thread finalizes,
+            // fetched before the stage lands so the load latency overlaps
+            uint32_t vbits = 0;
+            {
+                int slot_i = 0;
+                for (int t = tid; t < rows_i * nq && slot_i < 32; t += nthreads, ++slot_i) {
+                    const int64_t sl = rbase + t / nq;
+                    vbits |= ((__ldg(p.valid + (sl >> 5)) >> (sl & 31)) & 1u) << slot_i;
+                }
+            }
             mbar_wait(full_bar + s, (i / S) & 1);
             const uint8_t* sp = stage_base + static_cast<size_t>(s) * R * p.row_bytes;
 
             // ---- accumulate: partial[r][jq][c] = chunk sums ----
-            for (int r = g; r < rows_i; r += G) {
+            // warp (g, cw) owns rows [g*U, g*U+U) of the stage and column
+            // chunks cw, cw+CW, ...; the U rows are independent chains.
 #pragma unroll
-                for (int j = 0; j < CPW; ++j) {
-                    const int c = cw + j * CW;
-                    if (c >= C) continue;  // warp-uniform
-                    const int64_t boff = static_cast<int64_t>(c) * 512 + lane * 16;
-                    uint4 raw = make_uint4(0, 0, 0, 0);
-                    if (boff < p.row_bytes)
-                        raw = *reinterpret_cast<const uint4*>(sp + r * p.row_bytes + boff);
+            for (int j = 0; j < CPW; ++j) {
+                const int c = cw + j * CW;
+                if (c >= C) continue;  // warp-uniform
+                const int64_t boff = static_cast<int64_t>(c) * 512 + lane * 16;
+                const bool lane_in = boff < p.row_bytes;
+                uint4 raw[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = g * U + u;
+                    raw[u] = make_uint4(0, 0, 0, 0);
+                    if (lane_in && r < rows_i)
+                        raw[u] = *reinterpret_cast<const uint4*>(sp + r * p.row_bytes + boff);
+                }
+                float acc[U][NQ];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
                     float x[EPL];
-                    T::unpack(raw, x);
-                    float acc[NQ];
+                    T::unpack(raw[u], x);
 #pragma unroll
                     for (int jq = 0; jq < NQ; ++jq) {
                         float a = x[0] * q[j][jq][0];
 #pragma unroll
                         for (int t = 1; t < EPL; ++t) a = fmaf(x[t], q[j][jq][t], a);
-                        acc[jq] = a;
+                        acc[u][jq] = a;
                     }
-                    // transposed butterfly: after M halving steps lane holds
-                    // query (lane >> (5-M)); identical tree to a per-query
-                    // xor-16..1 butterfly.
+                }
+                // transposed butterfly: after M halving steps lane holds
+                // query (lane >> (5-M)); identical tree to a per-query
+                // xor-16..1 butterfly.
 #pragma unroll
-                    for (int st = 0; st < M; ++st) {
-                        const int o = 16 >> st;
-                        const bool upper = (lane & o) != 0;
-                        const int n = NQ >> st;
+                for (int st = 0; st < M; ++st) {
+                    const int o = 16 >> st;
+                    const bool upper = (lane & o) != 0;
+                    const int n = NQ >> st;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
 #pragma unroll
                         for (int e = 0; e < n / 2; ++e) {
-                            const float send = upper ? acc[e] : acc[e + n / 2];
-                            const float keep = upper ? acc[e + n / 2] : acc[e];
-                            acc[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                            const float send = upper ? acc[u][e] : acc[u][e + n / 2];
+                            const float keep = upper ? acc[u][e + n / 2] : acc[u][e];
+                            acc[u][e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                         }
                     }
-                    float v = acc[0];
+                }
+                float v[U];
 #pragma unroll
-                    for (int o = 16 >> M; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if ((lane & ((32 >> M) - 1)) == 0) {
-                        const int jq = lane >> (5 - M);
-                        partial[(r * NQ + jq) * C + c] = v;
+                for (int u = 0; u < U; ++u) v[u] = acc[u][0];
+#pragma unroll
+                for (int o = 16 >> M; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], o);
+                }
+                if ((lane & ((32 >> M) - 1)) == 0) {
+                    const int jq = lane >> (5 - M);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int r = g * U + u;
+                        if (r < rows_i) partial[(r * NQ + jq) * C + c] = v[u];
                     }
                 }
             }
@@ -295,14 +340,17 @@ __global__ void __launch_bounds__(9 * 32, 1) scan_kernel(const ScanParams p) {
             uint32_t* pend_total = pend;
             uint32_t* pend_cnt = pend + 1;
             uint2* pend_e = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(pend) + pend_hdr);
-            for (int t = tid; t < rows_i * nq; t += nthreads) {
+            {
+            int slot_i = 0;
+            for (int t = tid; t < rows_i * nq; t += nthreads, ++slot_i) {
                 const int r = t / nq, jq = t - r * nq;
                 const float* pr = partial + (r * NQ + jq) * C;
                 float sc = pr[0];
                 for (int c = 1; c < C; ++c) sc += pr[c];
                 sc += 0.0f;  // -0 -> +0 (the reference compares numerically)
                 const int64_t slot = rbase + r;
-                if (((vword >> (slot & 31)) & 1u) && sc == sc) {
+                const bool live = slot_i < 32 ? ((vbits >> slot_i) & 1u) : valid_bit(p.valid, slot);
+                if (live && sc == sc) {
                     const uint32_t key = f32_key(sc);
                     if (key >= thr[jq]) {
                         const uint32_t at = atomicAdd(pend_cnt + jq, 1u);
@@ -310,6 +358,7 @@ __global__ void __launch_bounds__(9 * 32, 1) scan_kernel(const ScanParams p) {
                         atomicAdd(pend_total, 1u);
                     }
                 }
+            }
             }
             named_bar_sync(1, nthreads);
             if (i > 0 && tid == 0) {

@@ -140,7 +140,7 @@ def test_batch_equals_independent_queries(pkg):
     rows = rng.standard_normal((n, d))
     rows /= np.linalg.norm(rows, axis=1, keepdims=True)
     q = rng.standard_normal((37, d))
-    q[::3] = rows[::300][: len(q[::3])]
+    q[:10] = rows[::300]
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     idx = pkg.GpuCosineIndex(d)
     idx.insert_batch(rng.permutation(10 * n)[:n], rows)
