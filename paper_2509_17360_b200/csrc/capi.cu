@@ -27,12 +27,14 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cudaTypedefs.h>
 
 #include "../../include/sine_b200.h"
 #include "common.cuh"
 #include "evict.cuh"
 #include "merge.cuh"
 #include "scan.cuh"
+#include "umma.cuh"
 
 using namespace sine;
 
@@ -422,10 +424,16 @@ ScanCfg scan_cfg(const sine_index* h, bool bf16, int NQ) {
     c.NQmax = std::min(16, 64 / (epl * c.CPW));
     if (NQ > 0) {
         const int maxW = NQ >= 8 ? 8 : 16;
-        c.U = unroll_for(NQ);
+        const int U = unroll_for(NQ);
         c.G = std::max(1, maxW / c.CW);
-        while (c.G > 1 && c.G * c.U > 64) --c.G;
-        c.R = c.G * c.U;
+        while (c.G > 1 && c.G * U > 64) --c.G;
+        // ~48 KB of rows per stage, at least U rows per warp, at most 64 rows
+        const int want = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, 49152 / c.row_bytes)));
+        int rpw = std::max(U, (want + c.G - 1) / c.G);
+        rpw = (rpw + U - 1) / U * U;
+        while (rpw > U && c.G * rpw > 64) rpw -= U;
+        c.U = rpw;
+        c.R = c.G * rpw;
     }
     return c;
 }
@@ -475,11 +483,108 @@ void tend(sine_index* h, size_t i, cudaStream_t st) {
     if (i != SIZE_MAX) CK(cudaEventRecord(h->tpool[i].b, st));
 }
 
-// tcgen05 path (large batches) -- not yet enabled
-bool umma_eligible(const sine_index*, int64_t, bool, uint32_t) { return false; }
-void umma_query(sine_index*, int64_t, const double*, int, int, float, double, bool, int64_t*, double*, int32_t*,
-                cudaStream_t) {
-    fail(SINE_EINVAL, "tensor-core path unavailable");
+// ------------------------------------------------------------ tcgen05 path
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !f) fail(SINE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+// 2-D K-major map: inner dim = row elements (box = one 128-B swizzle row),
+// outer dim = rows (box = 128), SWIZZLE_128B, out-of-bounds rows read as 0.
+CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int64_t rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_elems), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * (tf32 ? 4 : 2))};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(tf32 ? 32 : 64), 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = tmap_encoder()(&m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                      const_cast<void*>(base), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SINE_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    return m;
+}
+
+constexpr int kUmmaMinBatch = 8;
+
+bool umma_eligible(const sine_index* h, int64_t B, bool bf16, uint32_t mode, int kp) {
+    if (mode & SINE_SCAN_CUDA_CORE) return false;
+    if (B < kUmmaMinBatch || kp > kUmmaMaxKp) return false;
+    if (!bf16 && !(mode & SINE_RERANK_F64)) return false;  // tf32 products need the fp64 re-rank
+    if (h->nslots >= (1ll << 31)) return false;
+    return true;
+}
+
+void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, int k, double min_sim, bool rerank,
+                  int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st);
+
+void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, double min_sim, bool bf16, bool rerank,
+                int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+    const bool tf32 = !bf16;
+    const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
+    const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
+    // admission floor: tf32 products carry ~2^-11 relative error per term
+    float thr0;
+    if (rerank) {
+        const double margin = tf32 ? 4e-3 : 8e-3;
+        thr0 = std::nextafter(static_cast<float>(min_sim - margin), -INFINITY);
+    } else {
+        thr0 = static_cast<float>(min_sim);
+        if (static_cast<double>(thr0) > min_sim) thr0 = std::nextafter(thr0, -INFINITY);
+    }
+    const int ntiles = static_cast<int>((h->nslots + kUmmaN - 1) / kUmmaN);
+    const int grid = std::max(1, std::min(h->num_sms, ntiles));
+    const UmmaSmem L0 = umma_smem_layout(0, kp);
+    const size_t stage_bytes = static_cast<size_t>(kUmmaM + kUmmaN) * kUmmaKB;
+    const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / stage_bytes));
+    if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
+    const UmmaSmem L = umma_smem_layout(S, kp);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(umma_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    h->qbf.ensure(static_cast<size_t>(kUmmaM) * row_elems * 2);  // bytes/2 units: fp32 needs 2x
+    h->lkey.ensure(static_cast<size_t>(grid) * kUmmaM * kp);
+    h->lslot.ensure(static_cast<size_t>(grid) * kUmmaM * kp);
+    h->ln.ensure(static_cast<size_t>(grid) * kUmmaM);
+    const void* rows = tf32 ? static_cast<const void*>(h->rows32) : static_cast<const void*>(h->rows16);
+    const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots);
+    const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, kUmmaM);
+    for (int64_t q0 = 0; q0 < B; q0 += kUmmaM) {
+        const int nq = static_cast<int>(std::min<int64_t>(kUmmaM, B - q0));
+        umma_prep_queries<<<grid_for(kUmmaM * row_elems, 256, h->num_sms), 256, 0, st>>>(
+            q_dev + q0 * h->dim, nq, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
+        UmmaParams p{};
+        p.nslots = h->nslots;
+        p.ntiles = ntiles;
+        p.kblocks = static_cast<int>(row_bytes / kUmmaKB);
+        p.nq = nq;
+        p.kp = kp;
+        p.thr0 = thr0;
+        p.stages = S;
+        p.tf32 = tf32 ? 1 : 0;
+        p.valid = h->valid;
+        p.ids = h->ids;
+        p.out_key = h->lkey.p;
+        p.out_slot = h->lslot.p;
+        p.out_n = h->ln.p;
+        const size_t tk = tbegin(h, 2, st);
+        umma_scan_kernel<<<grid, kUmmaThreads, L.total, st>>>(qmap, rmap, p);
+        tend(h, tk, st);
+        h->launches += 2;
+        CK(cudaGetLastError());
+        merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
+                     counts_dev + q0, st);
+    }
 }
 
 // Runs the full stage-1 pipeline for B device-resident queries.
@@ -513,9 +618,8 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         if (static_cast<double>(thr0) > min_sim) thr0 = std::nextafter(thr0, -INFINITY);
     }
 
-    const bool use_umma = umma_eligible(h, B, bf16, mode);
-    if (use_umma) {
-        umma_query(h, B, q_dev, k, kp, thr0, min_sim, rerank, ids_dev, sims_dev, counts_dev, st);
+    if (umma_eligible(h, B, bf16, mode, kp)) {
+        umma_query(h, B, q_dev, k, kp, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
         return;
     }
 
@@ -578,30 +682,36 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         CK(cudaGetLastError());
         tend(h, tk, st);
         record(h, 1, st);
-        MergeParams m{};
-        m.in_key = h->lkey.p;
-        m.in_slot = h->lslot.p;
-        m.in_n = h->ln.p;
-        m.ncta = grid;
-        m.nq = nq;
-        m.kp = kp;
-        m.ids = h->ids;
-        m.rows64 = h->rows64;
-        m.q64 = q_dev + q0 * h->dim;
-        m.dim = h->dim;
-        m.k = k;
-        m.min_sim = min_sim;
-        m.rerank = rerank ? 1 : 0;
-        m.out_ids = ids_dev + q0 * k;
-        m.out_sims = sims_dev + q0 * k;
-        m.out_counts = counts_dev + q0;
-        const size_t tm = tbegin(h, 1, st);
-        merge_kernel<<<nq, kMergeThreads, 0, st>>>(m);
-        tend(h, tm, st);
-        ++h->launches;
-        CK(cudaGetLastError());
+        merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
+                     counts_dev + q0, st);
         record(h, 2, st);
     }
+}
+
+void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, int k, double min_sim, bool rerank,
+                  int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+    MergeParams m{};
+    m.in_key = h->lkey.p;
+    m.in_slot = h->lslot.p;
+    m.in_n = h->ln.p;
+    m.ncta = ncta;
+    m.nq = nq;
+    m.kp = kp;
+    m.ids = h->ids;
+    m.rows64 = h->rows64;
+    m.q64 = q64;
+    m.dim = h->dim;
+    m.k = k;
+    m.min_sim = min_sim;
+    m.rerank = rerank ? 1 : 0;
+    m.out_ids = ids_dev;
+    m.out_sims = sims_dev;
+    m.out_counts = counts_dev;
+    const size_t tm = tbegin(h, 1, st);
+    merge_kernel<<<nq, kMergeThreads, 0, st>>>(m);
+    tend(h, tm, st);
+    ++h->launches;
+    CK(cudaGetLastError());
 }
 
 void check_queries_host(const sine_index* h, int64_t B, const double* q) {

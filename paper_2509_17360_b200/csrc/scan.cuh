@@ -35,13 +35,13 @@ struct ScanParams {
     int nq;                 // queries in this launch (<= NQ)
     int kp;                 // per-CTA list capacity
     float thr0;             // admission floor (min_sim, or min_sim - margin)
-    int rows_per_stage;     // R = G * U (<= 64)
+    int rows_per_stage;     // R = G * RPW (<= 64)
     int stages;             // S
     int64_t rows_per_cta;   // multiple of R
     int chunks;             // C = ceil(row_bytes / 512)
     int chunk_warps;        // CW = ceil(C / CPW)
     int row_groups;         // G
-    int unroll;             // U: rows per warp per stage (R = G * U)
+    int unroll;             // RPW: rows per warp per stage (multiple of U; R = G * RPW)
     uint32_t* out_key;      // [grid][nq][kp] f32_key(score)
     int32_t* out_slot;      // [grid][nq][kp]
     int32_t* out_n;         // [grid][nq]
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int U = ScanUnroll<NQ>::kU;
     const int S = p.stages, R = p.rows_per_stage, C = p.chunks, CW = p.chunk_warps,
-              G = p.row_groups;
+              G = p.row_groups, RPW = p.unroll;  // rows per warp per stage (multiple of U)
     const int W = CW * G;  // compute warps; warp W is the producer
     const ScanSmemLayout L = scan_smem_layout(S, R, p.row_bytes, NQ, C, p.kp);
     uint8_t* stage_base = smem + L.stage_off;
@@ -268,8 +268,10 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
             const uint8_t* sp = stage_base + static_cast<size_t>(s) * R * p.row_bytes;
 
             // ---- accumulate: partial[r][jq][c] = chunk sums ----
-            // warp (g, cw) owns rows [g*U, g*U+U) of the stage and column
-            // chunks cw, cw+CW, ...; the U rows are independent chains.
+            // warp (g, cw) owns rows [g*RPW, (g+1)*RPW) of the stage and
+            // column chunks cw, cw+CW, ...; U rows at a time are independent
+            // FMA/shuffle chains.
+            for (int r0 = g * RPW; r0 < min((g + 1) * RPW, rows_i); r0 += U) {
 #pragma unroll
             for (int j = 0; j < CPW; ++j) {
                 const int c = cw + j * CW;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
                 uint4 raw[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int r = g * U + u;
+                    const int r = r0 + u;
                     raw[u] = make_uint4(0, 0, 0, 0);
                     if (lane_in && r < rows_i)
                         raw[u] = *reinterpret_cast<const uint4*>(sp + r * p.row_bytes + boff);
@@ -327,10 +329,11 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
                     const int jq = lane >> (5 - M);
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const int r = g * U + u;
+                        const int r = r0 + u;
                         if (r < rows_i) partial[(r * NQ + jq) * C + c] = v[u];
                     }
                 }
+            }
             }
             named_bar_sync(1, nthreads);
             if (tid == 0) mbar_arrive(empty_bar + s);  // stage consumed

@@ -1,0 +1,363 @@
+// Stage-1 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Batched Sine candidate search: S[q, r] = Q[q, :] . X[r, :] for a group of
+// up to 128 queries against every SE row, fused with the threshold and the
+// per-query top-k' admission (reference: `self._vecs @ arr` + `_rank`,
+// pkg/src/semcache/index.py:101 and :42-46, evaluated for B queries at once).
+//
+// Warp roles (192 threads, one CTA per SM, persistent over 128-row tiles):
+//   warps 0-3  epilogue: thread t owns query t; reads its 128 scores of a
+//              tile from TMEM (tcgen05.ld 32x32b) and keeps its own top-k'
+//              list in shared memory -- no cross-thread merge inside a CTA
+//   warp 4     TMA producer: per 128-byte K block, the query tile (A, 128 x
+//              128 B) and the row tile (B, 128 x 128 B), 128B-swizzled
+//   warp 5     TMEM allocator + MMA issuer (one elected lane):
+//              tcgen05.mma.cta_group::1.kind::{f16|tf32}, M=128 queries,
+//              N=128 rows, fp32 accumulators double-buffered in TMEM so the
+//              epilogue of tile i overlaps the MMAs of tile i+1.
+// kind::f16 reads bf16 rows (fast mode); kind::tf32 reads the fp32 rows
+// (exact mode: tf32 products, widened admission floor, then the fp64
+// re-rank in the merge kernel restores reference-grade similarities).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace sine {
+
+constexpr int kUmmaM = 128;      // queries per group (A rows / TMEM lanes)
+constexpr int kUmmaN = 128;      // SE rows per tile (B rows / TMEM columns)
+constexpr int kUmmaKB = 128;     // bytes of K per pipeline stage (one swizzle atom row)
+constexpr int kUmmaThreads = 192;
+constexpr int kUmmaMaxKp = 64;
+
+struct UmmaParams {
+    int64_t nslots;
+    int ntiles;
+    int kblocks;             // row_bytes / 128
+    int nq;                  // live queries in this group
+    int kp;
+    float thr0;
+    int stages;
+    int tf32;                // 1: kind::tf32 over fp32 rows, 0: kind::f16 over bf16 rows
+    const uint32_t* valid;
+    const int64_t* ids;
+    uint32_t* out_key;       // [grid][nq][kp]
+    int32_t* out_slot;
+    int32_t* out_n;          // [grid][nq]
+};
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// K-major, 128B-swizzled operand tile: 8-row atoms of 1024 B (SBO), LBO
+// unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+// Instruction descriptor: D fp32, A/B = bf16 (1) or tf32 (2), both K-major,
+// N >> 3 at [17,23), M >> 4 at [24,29).
+__host__ __device__ constexpr uint32_t umma_idesc(int tf32, int M, int N) {
+    return (1u << 4) | (static_cast<uint32_t>(tf32 ? 2 : 1) << 7) | (static_cast<uint32_t>(tf32 ? 2 : 1) << 10) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+#define SINE_TMEM_LD32(taddr, r)                                                                              \
+    asm volatile(                                                                                             \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"       \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),           \
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),         \
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),         \
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                              \
+        : "r"(taddr))
+
+struct UmmaSmem {
+    size_t a_off, b_off, bar_off, list_off, total;
+};
+
+__host__ __device__ inline UmmaSmem umma_smem_layout(int S, int kp) {
+    UmmaSmem L;
+    size_t off = 0;
+    L.a_off = off;
+    off += static_cast<size_t>(S) * kUmmaM * kUmmaKB;
+    L.b_off = off;
+    off += static_cast<size_t>(S) * kUmmaN * kUmmaKB;
+    L.bar_off = off;
+    off += (2 * S + 4) * sizeof(uint64_t) + 16;
+    off = (off + 15) / 16 * 16;
+    L.list_off = off;
+    off += static_cast<size_t>(kp) * kUmmaM * 8;
+    L.total = off + 1024;  // slack for the 1024-B alignment of the stage ring
+    return L;
+}
+
+// Thread-private top-k' list (entries strided by 128 in smem).
+struct ThreadList {
+    uint32_t* key;
+    int32_t* slot;
+    int n, kp, worst;
+    uint32_t thr;
+
+    __device__ __forceinline__ uint32_t k(int e) const { return key[e * kUmmaM]; }
+    __device__ __forceinline__ int32_t s(int e) const { return slot[e * kUmmaM]; }
+
+    __device__ void recompute_worst(const int64_t* ids, uint32_t thr0) {
+        uint32_t mk = 0xffffffffu;
+        int pos = 0, nmin = 0;
+        for (int e = 0; e < kp; ++e) {
+            const uint32_t v = k(e);
+            if (v < mk) {
+                mk = v;
+                pos = e;
+                nmin = 1;
+            } else if (v == mk) {
+                ++nmin;
+            }
+        }
+        if (nmin > 1) {  // exact ties at the boundary: largest id is worst
+            int64_t best = INT64_MIN;
+            for (int e = 0; e < kp; ++e)
+                if (k(e) == mk) {
+                    const int64_t id = __ldg(ids + s(e));
+                    if (id > best) {
+                        best = id;
+                        pos = e;
+                    }
+                }
+        }
+        worst = pos;
+        thr = max(thr0, mk);
+    }
+
+    __device__ __forceinline__ void offer(uint32_t kk, int32_t sl, const int64_t* ids, uint32_t thr0) {
+        if (n < kp) {
+            key[n * kUmmaM] = kk;
+            slot[n * kUmmaM] = sl;
+            if (++n == kp) recompute_worst(ids, thr0);
+            return;
+        }
+        const uint32_t wk = k(worst);
+        bool better = kk > wk;
+        if (kk == wk) better = __ldg(ids + sl) < __ldg(ids + s(worst));
+        if (!better) return;
+        key[worst * kUmmaM] = kk;
+        slot[worst * kUmmaM] = sl;
+        recompute_worst(ids, thr0);
+    }
+};
+
+__global__ void __launch_bounds__(kUmmaThreads, 1)
+    umma_scan_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
+                     const UmmaParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    const UmmaSmem L = umma_smem_layout(S, p.kp);
+    uint8_t* sa = smem + L.a_off;
+    uint8_t* sb = smem + L.b_off;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;     // [2]
+    uint64_t* tempty = tfull + 2;    // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint32_t* lkey = reinterpret_cast<uint32_t*>(smem + L.list_off);
+    int32_t* lslot = reinterpret_cast<int32_t*>(lkey + p.kp * kUmmaM);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 4 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * kUmmaN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nkb = p.kblocks;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            const uint64_t pol_rows = l2_evict_first_policy();
+            const uint64_t pol_q = l2_evict_last_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            const int kb_elems = p.tf32 ? kUmmaKB / 4 : kUmmaKB / 2;
+            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(empty + s, ph ^ 1);
+                    mbar_arrive_expect_tx(full + s, (kUmmaM + kUmmaN) * kUmmaKB);
+                    tma_load_2d(sa + static_cast<size_t>(s) * kUmmaM * kUmmaKB, &qmap, full + s, kb * kb_elems, 0,
+                                pol_q);
+                    tma_load_2d(sb + static_cast<size_t>(s) * kUmmaN * kUmmaKB, &rmap, full + s, kb * kb_elems,
+                                t * kUmmaN, pol_rows);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc(p.tf32, kUmmaM, kUmmaN);
+            int s = 0;
+            uint32_t ph = 0;
+            int i = 0;
+            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+                const int acc = i & 1;
+                mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * kUmmaN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full + s, ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + static_cast<size_t>(s) * kUmmaM * kUmmaKB);
+                    const uint32_t b0 = smem_u32(sb + static_cast<size_t>(s) * kUmmaN * kUmmaKB);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B block
+                        const uint64_t ad = umma_smem_desc(a0 + kk * 32);
+                        const uint64_t bd = umma_smem_desc(b0 + kk * 32);
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        if (p.tf32)
+                            umma_tf32(d, ad, bd, idesc, accum);
+                        else
+                            umma_f16(d, ad, bd, idesc, accum);
+                    }
+                    umma_commit(empty + s);  // frees the smem stage when these MMAs retire
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit(tfull + acc);  // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ---------------- epilogue: thread = query ----------------
+        const int qi = threadIdx.x;  // 0..127 == TMEM lane
+        const uint32_t thr0 = f32_key(p.thr0);
+        ThreadList list{lkey + qi, lslot + qi, 0, p.kp, 0, thr0};
+        const bool live_q = qi < p.nq;
+        int i = 0;
+        for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+            const int acc = i & 1;
+            const int64_t row0 = static_cast<int64_t>(t) * kUmmaN;
+            // validity words of this tile (4 x 32 rows), fetched before the wait
+            uint32_t vw[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int64_t r = row0 + 32 * w;
+                vw[w] = r < p.nslots ? __ldg(p.valid + (r >> 5)) : 0u;
+            }
+            mbar_wait(tfull + acc, (i >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kUmmaN / 32; ++c) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * kUmmaN + c * 32;
+                SINE_TMEM_LD32(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!live_q) continue;
+                const uint32_t vbits = vw[c];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float sc = __uint_as_float(r[j]) + 0.0f;
+                    const int64_t slot = row0 + c * 32 + j;
+                    if (((vbits >> j) & 1u) && slot < p.nslots && sc == sc) {
+                        const uint32_t key = f32_key(sc);
+                        if (key >= list.thr) list.offer(key, static_cast<int32_t>(slot), p.ids, thr0);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + acc);
+        }
+        if (live_q) {
+            const size_t base = (static_cast<size_t>(blockIdx.x) * p.nq + qi) * p.kp;
+            for (int e = 0; e < list.n; ++e) {
+                p.out_key[base + e] = list.k(e);
+                p.out_slot[base + e] = list.s(e);
+            }
+            p.out_n[blockIdx.x * p.nq + qi] = list.n;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kUmmaN));
+    }
+}
+
+// q64 [nq][dim] -> zero-padded [128][stride] bf16 or fp32 (TMA source).
+__global__ void umma_prep_queries(const double* q64, int nq, int64_t dim, int64_t stride, int tf32, void* out) {
+    const int64_t total = static_cast<int64_t>(kUmmaM) * stride;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t qrow = t / stride, c = t - qrow * stride;
+        const double v = (qrow < nq && c < dim) ? q64[qrow * dim + c] : 0.0;
+        if (tf32)
+            static_cast<float*>(out)[t] = static_cast<float>(v);
+        else
+            static_cast<__nv_bfloat16*>(out)[t] = __float2bfloat16_rn(static_cast<float>(v));
+    }
+}
+
+}  // namespace sine

@@ -109,12 +109,14 @@ class GpuCosineIndex:
     def handle(self) -> ctypes.c_void_p:
         return self._h
 
-    def _mode(self, scan: str | None = None, rerank: bool | None = None) -> int:
+    def _mode(self, scan: str | None = None, rerank: bool | None = None, cuda_core: bool = False) -> int:
         scan = scan or self.scan
         rerank = self.rerank if rerank is None else rerank
         m = N.SCAN_BF16 if scan == "bf16" else N.SCAN_F32
         if rerank:
             m |= N.RERANK_F64
+        if cuda_core:
+            m |= N.SCAN_CUDA_CORE
         return m | N.NO_NORM_CHECK
 
     # ------------------------------------------------------------ queries
@@ -179,7 +181,7 @@ class GpuCosineIndex:
         return [Candidate(int(ids[0, j]), float(sims[0, j])) for j in range(n)]
 
     def query_batch(self, queries, k: int, min_similarity: float = -1.0, *, scan: str | None = None,
-                    rerank: bool | None = None, check: bool = True):
+                    rerank: bool | None = None, check: bool = True, cuda_core: bool = False):
         """B independent queries in one pass over the index.
 
         Returns (ids int64[B, k] padded with -1, sims float64[B, k],
@@ -187,7 +189,7 @@ class GpuCosineIndex:
         q = check_matrix(queries, self.dimension) if check else N.f64(queries)
         if k < 1:
             raise ValidationError("k must be >= 1")
-        return self._query(q, k, min_similarity, self._mode(scan, rerank))
+        return self._query(q, k, min_similarity, self._mode(scan, rerank, cuda_core))
 
     def _query(self, q: np.ndarray, k: int, min_similarity: float, mode: int):
         B = q.shape[0]
@@ -209,10 +211,10 @@ class GpuCosineIndex:
 
     def query_device(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                      counts_ptr: int, stream: int | None = None, *, scan: str | None = None,
-                     rerank: bool | None = None) -> None:
+                     rerank: bool | None = None, cuda_core: bool = False) -> None:
         """Device-pointer variant (torch tensors); enqueued on `stream`."""
         N.check(self._lib.sine_query_device(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
-                                            float(min_similarity), self._mode(scan, rerank),
+                                            float(min_similarity), self._mode(scan, rerank, cuda_core),
                                             ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
                                             ctypes.c_void_p(counts_ptr),
                                             ctypes.c_void_p(stream) if stream else None))

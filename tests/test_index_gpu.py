@@ -278,3 +278,40 @@ def test_full_size_properties(pkg):
             np.testing.assert_allclose(sims[j], s[order], atol=1e-12)
             if j < 8:
                 assert ids[j, 0] == pick[j] and sims[j, 0] == pytest.approx(1.0, abs=1e-12)
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_tensor_core_and_cuda_core_paths_agree(pkg, index_golden, scan):
+    """Config A through both stage-1 engines (tcgen05 for B >= 8, the
+    CUDA-core streaming scan forced): identical ids and fp64 similarities."""
+    rows, qs = G.config_a()
+    idx = pkg.GpuCosineIndex(rows.shape[1], scan=scan)
+    idx.insert_batch(np.arange(rows.shape[0]), rows)
+    for ms in (0.9, -1.0, 0.2):
+        a = idx.query_batch(qs, 5, ms)
+        b = idx.query_batch(qs, 5, ms, cuda_core=True)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_tensor_core_bf16_raw_scores_within_tolerance(pkg):
+    rng = np.random.default_rng(21)
+    n, d, B = 20000, 768, 160
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((B, d))
+    q[::2] = rows[rng.integers(0, n, B // 2)] + 0.1 * rng.standard_normal((B // 2, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    idx = pkg.GpuCosineIndex(d, scan="bf16", rerank=False)
+    idx.insert_batch(np.arange(n), rows)
+    ids, sims, counts = idx.query_batch(q, 10, -1.0)
+    exact = rows @ q.T
+    hit = 0
+    for j in range(B):
+        assert counts[j] == 10
+        true = np.lexsort((np.arange(n), -exact[:, j]))[:10]
+        hit += len(set(true.tolist()) & set(ids[j].tolist()))
+        assert np.all(np.abs(sims[j] - exact[ids[j], j]) < 2e-2)
+        assert np.all(np.diff(sims[j]) <= 0)
+    print(f"tcgen05 bf16 (no re-rank) recall@10: {hit / (10 * B):.4f}")
+    assert hit / (10 * B) >= 0.9
