@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--rows", type=int, default=N_ROWS)
     ap.add_argument("--no-regimes", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-evict", action="store_true")
+    ap.add_argument("--evict-rows", type=int, default=10_000_000)
     return ap.parse_args()
 
 
@@ -305,6 +307,11 @@ def run_ours(args):
     regimes = []
     if world == 1 and not args.no_regimes:
         regimes = measure_regimes(idx, rows, torch, hbm_peak)
+    eviction = None
+    if world == 1 and not args.no_evict:
+        del idx
+        torch.cuda.empty_cache()
+        eviction = measure_eviction(args.evict_rows, hbm_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -327,7 +334,7 @@ def run_ours(args):
                            "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
                            "l2": "no flush: the index (>= 1.5 GB) exceeds the 126 MB L2"},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": int(launches), "regimes": regimes}
+                "gpu_launches": int(launches), "regimes": regimes, "eviction": eviction}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -368,6 +375,104 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                             "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
                             "tflops": flops / (ms / 1e3) / 1e12})
     return out
+
+
+# ------------------------------------------------------- config D: eviction
+
+def evict_metadata(n, seed=4):
+    """Config D metadata: config-A draws, created_at uniform in
+    [0, 1e4), 1/7 short TTL so the purge path runs."""
+    rng = np.random.default_rng(seed)
+    meta = dict(staticity=rng.integers(1, 11, n), freq=rng.integers(0, 8, n),
+                lat=rng.choice(np.array([50.0, 400.0, 1500.0]), n),
+                cost=rng.choice(np.array([0.0, 0.0005, 0.005, 0.02]), n),
+                size=rng.integers(1, 30, n), created=rng.random(n) * 1e4)
+    ttl = np.where(rng.random(n) < 1 / 7, 10.0, 2.0e4)
+    meta["expiration"] = meta["created"] + ttl
+    return meta
+
+
+def _exact_log(v):
+    u, inv = np.unique(v, return_inverse=True)
+    return np.array([math.log(float(x)) for x in u])[inv]
+
+
+def measure_eviction(n, hbm_peak, cpu_sample=300_000):
+    """evict_until_fits on n device-resident SEs at capacity = 0.9 * usage:
+    TTL purge (ascending ids) + the LCFU victim prefix, through the C ABI
+    with host output buffers; CPU baseline = the reference algorithm
+    (oracle: per-element cal_score + tuple sort) on a bounded sample."""
+    import ctypes
+
+    import torch
+    from paper_2509_17360_b200 import GpuCosineIndex
+    from paper_2509_17360_b200 import _native as Nat
+
+    meta = evict_metadata(n)
+    now = 1.0e4
+    cols = {"log_freq": _exact_log((meta["freq"] + 1).astype(np.float64)),
+            "log_cost": _exact_log(meta["cost"] * 1000.0 + 1),
+            "log_lat": _exact_log(meta["lat"] + 1), "log_stat": _exact_log((meta["staticity"] + 1).astype(float)),
+            "frequency": meta["freq"], "size_tokens": meta["size"], "created_at": meta["created"],
+            "expiration_time": meta["expiration"], "last_access": meta["created"]}
+    d = 4
+    rows = torch.zeros((n, d), dtype=torch.float64, device="cuda")
+    rows[:, 0] = 1.0
+    idx = GpuCosineIndex(d, metadata=True, capacity=n)
+    idx.insert_device(np.arange(1, n + 1), rows.data_ptr(), meta=cols)
+    del rows
+    usage = int(meta["size"].sum())
+    expired_mask = (meta["expiration"] - now) <= 0.0
+    live_usage = int(meta["size"][~expired_mask].sum())
+    cap = int(0.9 * usage)
+    excess = live_usage - cap
+    out = Nat.PinnedArray((n,), np.int64)
+    cnt = ctypes.c_int64()
+    lib = idx._lib
+    # victims only (the select), repeated: no mutation
+    times = []
+    idx.set_timing(True)
+    for _ in range(4):
+        t0 = time.perf_counter()
+        Nat.check(lib.sine_select_victims(idx.handle, 0, now, excess, out.array.ctypes.data_as(
+            ctypes.POINTER(ctypes.c_int64)), n, ctypes.byref(cnt)))
+        times.append(time.perf_counter() - t0)
+    dev_ms = idx.last_timing()[2]
+    n_victims = cnt.value
+    victims = out.array[:n_victims].copy()
+    sel_s = min(times[1:])
+    # expiry scan + tombstone (the purge half of evict_until_fits), once
+    t0 = time.perf_counter()
+    Nat.check(lib.sine_expired(idx.handle, now, 1, out.array.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n,
+                               ctypes.byref(cnt)))
+    exp_s = time.perf_counter() - t0
+    n_expired = cnt.value
+    # parity spot-check against the oracle on the full population
+    from oracle import sine_oracle as O
+    want = O.evict_until_fits_np(np.arange(1, n + 1), meta["freq"], meta["cost"], meta["lat"],
+                                 meta["staticity"], meta["size"], meta["created"], meta["expiration"], now, cap)
+    parity = bool(np.array_equal(want[n_expired:], victims) and want.shape[0] == n_expired + n_victims)
+    # CPU baseline: the reference algorithm (Python cal_score + tuple sort) on a sample
+    m = min(cpu_sample, n)
+    els = {i + 1: O.OracleElement(int(meta["staticity"][i]), int(meta["freq"][i]), float(meta["lat"][i]),
+                                  float(meta["cost"][i]), int(meta["size"][i]), float(meta["created"][i]),
+                                  float(meta["expiration"][i])) for i in range(m)}
+    ucap = int(0.9 * sum(int(x) for x in meta["size"][:m]))
+    t0 = time.perf_counter()
+    O.evict_until_fits(els, now, ucap)
+    cpu_s = time.perf_counter() - t0
+    bytes_per_se = 60.0
+    total_s = sel_s + exp_s
+    return {"workload": f"config D: {n} SEs, capacity = 0.9 x usage ({cap} tokens), now={now}",
+            "expired": n_expired, "victims": n_victims, "parity_vs_oracle": parity,
+            "select_ms_e2e": sel_s * 1e3, "select_ms_device": dev_ms, "expire_ms_e2e": exp_s * 1e3,
+            "evict_until_fits_ms": total_s * 1e3, "ses_per_s": n / total_s,
+            "roofline": {"bound": "hbm", "bytes_per_se": bytes_per_se,
+                         "achieved": n * bytes_per_se / (dev_ms / 1e3) / 1e9 if dev_ms else None,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (n * bytes_per_se / (dev_ms / 1e3) / 1e9 / hbm_peak) if dev_ms else None},
+            "cpu_baseline": {"value": m / cpu_s, "unit": "SEs/s", "cores": 1, "kind": "port",
+                             "sample": f"{m} SEs: oracle evict_until_fits (Python cal_score + tuple sort)"}}
 
 
 def main():
