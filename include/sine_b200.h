@@ -56,6 +56,7 @@ extern "C" {
 #define SINE_RERANK_F64    0x10u /* re-score final candidates in fp64        */
 #define SINE_NO_NORM_CHECK 0x100u/* caller already validated (|norm-1|<=1e-6)*/
 #define SINE_SCAN_CUDA_CORE 0x200u /* force the CUDA-core streaming scan      */
+#define SINE_SCAN_UMMA_V1  0x400u /* force the query-streaming tcgen05 kernel */
 
 /* ---- eviction policies (CacheConfig.eviction_policy, model.py:15) -------- */
 #define SINE_POLICY_LCFU 0

@@ -499,11 +499,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 // 2-D K-major map: inner dim = row elements (box = one 128-B swizzle row),
 // outer dim = rows (box = 128), SWIZZLE_128B, out-of-bounds rows read as 0.
-CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int64_t rows) {
+CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int64_t rows, int box_rows = 128) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_elems), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * (tf32 ? 4 : 2))};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(tf32 ? 32 : 64), 128};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(tf32 ? 32 : 64), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = tmap_encoder()(&m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                       const_cast<void*>(base), dims, strides, box, estr,
@@ -526,8 +526,81 @@ bool umma_eligible(const sine_index* h, int64_t B, bool bf16, uint32_t mode, int
 void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, int k, double min_sim, bool rerank,
                   int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st);
 
+// widest resident query group (Q <= 96 KB of shared memory), 0 if < 16
+int res_nq_max(int64_t row_bytes) {
+    const int64_t n = (96 * 1024) / row_bytes;
+    return n >= 64 ? 64 : n >= 32 ? 32 : n >= 16 ? 16 : 0;
+}
+
+template <int NQ>
+void launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int grid, size_t smem,
+                cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(umma_res_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    umma_res_kernel<NQ><<<grid, kUmmaThreads, smem, st>>>(qmap, rmap, p);
+}
+
+// Query-resident tensor-core scan, groups of NQ queries (one HBM pass each).
+void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                    bool bf16, bool rerank, int NQmax, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                    cudaStream_t st) {
+    const bool tf32 = !bf16;
+    const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
+    const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
+    const int kblocks = static_cast<int>(row_bytes / kUmmaKB);
+    const int ntiles = static_cast<int>((h->nslots + kUmmaN - 1) / kUmmaN);
+    const int grid = std::max(1, std::min(h->num_sms, ntiles));
+    h->qbf.ensure(static_cast<size_t>(NQmax) * row_elems * 2);
+    h->lkey.ensure(static_cast<size_t>(grid) * NQmax * kp);
+    h->lslot.ensure(static_cast<size_t>(grid) * NQmax * kp);
+    h->ln.ensure(static_cast<size_t>(grid) * NQmax);
+    const void* rows = tf32 ? static_cast<const void*>(h->rows32) : static_cast<const void*>(h->rows16);
+    const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots);
+    for (int64_t q0 = 0; q0 < B; q0 += NQmax) {
+        const int nq = static_cast<int>(std::min<int64_t>(NQmax, B - q0));
+        const int NQ = nq <= 16 ? 16 : nq <= 32 ? 32 : 64;
+        const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp);
+        const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
+        if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
+        const ResSmem L = res_smem_layout(S, NQ, kblocks, kp);
+        res_prep_queries<<<grid_for(static_cast<int64_t>(NQ) * row_elems, 256, h->num_sms), 256, 0, st>>>(
+            q_dev + q0 * h->dim, nq, NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
+        const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, NQ, NQ);
+        ResParams p{};
+        p.nslots = h->nslots;
+        p.ntiles = ntiles;
+        p.kblocks = kblocks;
+        p.nq = nq;
+        p.Nq = NQ;
+        p.kp = kp;
+        p.thr0 = thr0;
+        p.stages = S;
+        p.tf32 = tf32 ? 1 : 0;
+        p.valid = h->valid;
+        p.ids = h->ids;
+        p.out_key = h->lkey.p;
+        p.out_slot = h->lslot.p;
+        p.out_n = h->ln.p;
+        const size_t tk = tbegin(h, 2, st);
+        if (NQ == 16)
+            launch_res<16>(qmap, rmap, p, grid, L.total, st);
+        else if (NQ == 32)
+            launch_res<32>(qmap, rmap, p, grid, L.total, st);
+        else
+            launch_res<64>(qmap, rmap, p, grid, L.total, st);
+        tend(h, tk, st);
+        h->launches += 2;
+        CK(cudaGetLastError());
+        merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
+                     counts_dev + q0, st);
+    }
+}
+
 void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, double min_sim, bool bf16, bool rerank,
-                int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+                int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, uint32_t mode) {
     const bool tf32 = !bf16;
     const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
     const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
@@ -539,6 +612,18 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
     } else {
         thr0 = static_cast<float>(min_sim);
         if (static_cast<double>(thr0) > min_sim) thr0 = std::nextafter(thr0, -INFINITY);
+    }
+    // query-resident kernel (v2) when the group fits shared memory and costs
+    // no more HBM passes than the query-streaming kernel (v1, 128 per pass)
+    {
+        const int nq2 = res_nq_max(row_bytes);
+        const int64_t passes2 = nq2 ? (B + nq2 - 1) / nq2 : INT64_MAX;
+        const int64_t passes1 = (B + kUmmaM - 1) / kUmmaM;
+        const bool force_v1 = (mode & 0x400u) != 0;
+        if (!force_v1 && nq2 && (passes2 <= passes1 || bf16)) {
+            umma_res_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, nq2, ids_dev, sims_dev, counts_dev, st);
+            return;
+        }
     }
     const int ntiles = static_cast<int>((h->nslots + kUmmaN - 1) / kUmmaN);
     const int grid = std::max(1, std::min(h->num_sms, ntiles));
@@ -619,7 +704,7 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
     }
 
     if (umma_eligible(h, B, bf16, mode, kp)) {
-        umma_query(h, B, q_dev, k, kp, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
+        umma_query(h, B, q_dev, k, kp, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st, mode);
         return;
     }
 

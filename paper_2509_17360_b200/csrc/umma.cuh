@@ -361,3 +361,340 @@ __global__ void umma_prep_queries(const double* q64, int nq, int64_t dim, int64_
 }
 
 }  // namespace sine
+
+namespace sine {
+
+// ===========================================================================
+// v2: query-resident tensor-core scan (the HBM-bound regime, B <= 64).
+//
+// A = SE rows (M = 128 per tile, streamed: one 16-KB TMA box per 128-B K
+// block), B = the query group (N = Nq <= 64, loaded into shared memory ONCE
+// per CTA and reused by every tile), D = 128 rows x Nq fp32 in TMEM, double
+// buffered.  Shared-memory traffic per HBM byte: TMA write 1 + MMA read of A
+// 1 + MMA read of B Nq/128  (v1 re-loaded the query tile per row tile).
+// Epilogue warps 0-3: thread = row of the tile; scores are compared with
+// per-query admission thresholds (shared), passing (query, row) pairs go
+// through small per-query queues into per-query top-k' lists (warp-parallel
+// insertion, as in the CUDA-core scan).
+// ===========================================================================
+
+constexpr int kResMaxNq = 64;
+constexpr int kResQPer = 16;  // pending entries per query per round
+
+struct ResParams {
+    int64_t nslots;
+    int ntiles;
+    int kblocks;
+    int nq, Nq;       // live queries, padded group width (multiple of 16)
+    int kp;
+    float thr0;
+    int stages;
+    int tf32;
+    const uint32_t* valid;
+    const int64_t* ids;
+    uint32_t* out_key;
+    int32_t* out_slot;
+    int32_t* out_n;
+};
+
+struct ResSmem {
+    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, total;
+};
+
+__host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, int kp) {
+    ResSmem L;
+    size_t off = 0;
+    L.q_off = off;
+    off += static_cast<size_t>(kblocks) * Nq * kUmmaKB;
+    L.a_off = off;
+    off += static_cast<size_t>(S) * kUmmaN * kUmmaKB;
+    L.bar_off = off;
+    off += (2 * S + 5) * sizeof(uint64_t) + 16;
+    off = (off + 15) / 16 * 16;
+    L.list_key_off = off;
+    off += static_cast<size_t>(Nq) * kp * 4;
+    L.list_slot_off = off;
+    off += static_cast<size_t>(Nq) * kp * 4;
+    L.qstate_off = off;  // cnt, worst, thr(float) per query
+    off += static_cast<size_t>(3 * Nq) * 4;
+    off = (off + 15) / 16 * 16;
+    L.pend_off = off;  // pcnt[Nq] + entries[Nq][kResQPer] (uint2)
+    off += static_cast<size_t>(Nq) * 4 + 16;
+    off = (off + 15) / 16 * 16;
+    off += static_cast<size_t>(Nq) * kResQPer * 8;
+    L.total = off + 1024;
+    return L;
+}
+
+__device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool v) {
+    uint32_t r;
+    asm volatile(
+        "{\n.reg .pred pi, po;\nsetp.ne.u32 pi, %1, 0;\n"
+        "barrier.red.or.pred po, %2, %3, pi;\nselp.u32 %0, 1, 0, po;\n}\n"
+        : "=r"(r)
+        : "r"(v ? 1u : 0u), "r"(id), "r"(nthreads)
+        : "memory");
+    return r != 0;
+}
+
+#define SINE_TMEM_LD16(taddr, r)                                                                              \
+    asm volatile(                                                                                             \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"      \
+        " [%16];"                                                                                             \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),           \
+          "=r"(r[15])                                                                                        \
+        : "r"(taddr))
+
+template <int NQ>
+__global__ void __launch_bounds__(kUmmaThreads, 1)
+    umma_res_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
+                    const ResParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages, nkb = p.kblocks, kp = p.kp;
+    const ResSmem L = res_smem_layout(S, NQ, nkb, kp);
+    uint8_t* sq = smem + L.q_off;
+    uint8_t* sa = smem + L.a_off;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* qfull = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qfull + 1);
+    uint32_t* lkey = reinterpret_cast<uint32_t*>(smem + L.list_key_off);
+    int32_t* lslot = reinterpret_cast<int32_t*>(smem + L.list_slot_off);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.qstate_off);
+    uint32_t* worst = cnt + NQ;
+    float* thr = reinterpret_cast<float*>(worst + NQ);
+    uint32_t* pcnt = reinterpret_cast<uint32_t*>(smem + L.pend_off);
+    uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
+    constexpr uint32_t kTmemCols = NQ <= 16 ? 32 : (2 * NQ <= 64 ? 64 : 128);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 4);
+        }
+        mbar_init(qfull, 1);
+        fence_mbar_init();
+    }
+    for (int j = threadIdx.x; j < NQ; j += blockDim.x) {
+        cnt[j] = 0;
+        worst[j] = 0;
+        thr[j] = p.thr0;
+        pcnt[j] = 0;
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int kb_elems = p.tf32 ? kUmmaKB / 4 : kUmmaKB / 2;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
+            const uint64_t pol_rows = l2_evict_first_policy();
+            const uint64_t pol_q = l2_evict_last_policy();
+            // the whole query group, once
+            mbar_arrive_expect_tx(qfull, static_cast<uint32_t>(nkb) * NQ * kUmmaKB);
+            for (int kb = 0; kb < nkb; ++kb)
+                tma_load_2d(sq + static_cast<size_t>(kb) * NQ * kUmmaKB, &qmap, qfull, kb * kb_elems, 0, pol_q);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(empty + s, ph ^ 1);
+                    mbar_arrive_expect_tx(full + s, kUmmaN * kUmmaKB);
+                    tma_load_2d(sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB, &rmap, full + s, kb * kb_elems,
+                                t * kUmmaN, pol_rows);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer: D[128 rows, NQ] += A(rows) . B(queries)^T ----------------
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc(p.tf32, kUmmaN, NQ);
+            mbar_wait(qfull, 0);
+            int s = 0;
+            uint32_t ph = 0;
+            int i = 0;
+            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+                const int acc = i & 1;
+                mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * NQ;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full + s, ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB);
+                    const uint32_t b0 = smem_u32(sq + static_cast<size_t>(kb) * NQ * kUmmaKB);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ad = umma_smem_desc(a0 + kk * 32);
+                        const uint64_t bd = umma_smem_desc(b0 + kk * 32);
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        if (p.tf32)
+                            umma_tf32(d, ad, bd, idesc, accum);
+                        else
+                            umma_f16(d, ad, bd, idesc, accum);
+                    }
+                    umma_commit(empty + s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit(tfull + acc);
+            }
+        }
+    } else {
+        // ---------------- epilogue: thread = row ----------------
+        const int tid = threadIdx.x;  // 0..127 == TMEM lane == row within tile
+        int i = 0;
+        for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+            const int acc = i & 1;
+            const int64_t slot = static_cast<int64_t>(t) * kUmmaN + tid;
+            const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
+            const bool live = ((vw >> (slot & 31)) & 1u) != 0;
+            mbar_wait(tfull + acc, (i >> 1) & 1);
+            tc_fence_after();
+            float sc[NQ];
+#pragma unroll
+            for (int c = 0; c < NQ / 16; ++c) {
+                uint32_t r[16];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * NQ + c * 16;
+                SINE_TMEM_LD16(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sc[c * 16 + j] = __uint_as_float(r[j]) + 0.0f;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + acc);  // TMEM buffer free for tile i+2
+
+            uint64_t mask = 0;
+            if (live) {
+#pragma unroll
+                for (int j = 0; j < NQ; ++j)
+                    if (j < p.nq && sc[j] >= thr[j]) mask |= 1ull << j;
+            }
+            while (bar_red_or(1, 128, mask != 0)) {
+                // queue what fits, then insert warp-per-query
+                uint64_t m = mask;
+                while (m) {
+                    const int j = __ffsll(m) - 1;
+                    m &= m - 1;
+                    const uint32_t pos = atomicAdd(pcnt + j, 1u);
+                    if (pos < kResQPer) {
+                        pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
+                        mask &= ~(1ull << j);
+                    }
+                }
+                named_bar_sync(2, 128);
+                for (int j = warp; j < p.nq; j += 4) {
+                    const uint32_t np = min(pcnt[j], static_cast<uint32_t>(kResQPer));
+                    uint32_t* lk = lkey + j * kp;
+                    int32_t* ls = lslot + j * kp;
+                    for (uint32_t e = 0; e < np; ++e) {
+                        const uint2 cand = pend[j * kResQPer + e];
+                        const uint32_t key = cand.y;
+                        const int32_t sl = static_cast<int32_t>(cand.x);
+                        uint32_t n = cnt[j];
+                        if (n < static_cast<uint32_t>(kp)) {
+                            if (lane == 0) {
+                                lk[n] = key;
+                                ls[n] = sl;
+                            }
+                            __syncwarp();
+                            ++n;
+                            if (lane == 0) cnt[j] = n;
+                            if (n == static_cast<uint32_t>(kp)) {
+                                const int w = list_worst(lk, ls, kp, p.ids, lane);
+                                if (lane == 0) {
+                                    worst[j] = w;
+                                    thr[j] = fmaxf(p.thr0, key_f32(lk[w]));
+                                }
+                            }
+                            __syncwarp();
+                            continue;
+                        }
+                        const uint32_t w = worst[j];
+                        const uint32_t wk = lk[w];
+                        bool better = key > wk;
+                        if (key == wk) better = __ldg(p.ids + sl) < __ldg(p.ids + ls[w]);
+                        if (!better) continue;
+                        if (lane == 0) {
+                            lk[w] = key;
+                            ls[w] = sl;
+                        }
+                        __syncwarp();
+                        const int nw = list_worst(lk, ls, kp, p.ids, lane);
+                        if (lane == 0) {
+                            worst[j] = nw;
+                            thr[j] = fmaxf(p.thr0, key_f32(lk[nw]));
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) pcnt[j] = 0;
+                }
+                named_bar_sync(2, 128);
+                // thresholds only rise: drop pairs that no longer qualify
+                if (mask) {
+#pragma unroll
+                    for (int j = 0; j < NQ; ++j)
+                        if (((mask >> j) & 1ull) && !(sc[j] >= thr[j])) mask &= ~(1ull << j);
+                }
+            }
+        }
+        named_bar_sync(2, 128);
+        for (int j = 0; j < p.nq; ++j) {
+            const uint32_t n = cnt[j];
+            const size_t base = (static_cast<size_t>(blockIdx.x) * p.nq + j) * kp;
+            for (int e = tid; e < static_cast<int>(n); e += 128) {
+                p.out_key[base + e] = lkey[j * kp + e];
+                p.out_slot[base + e] = lslot[j * kp + e];
+            }
+            if (tid == 0) p.out_n[blockIdx.x * p.nq + j] = static_cast<int>(n);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// q64 [nq][dim] -> zero-padded [Nq][stride] bf16 or fp32 (TMA source).
+__global__ void res_prep_queries(const double* q64, int nq, int Nq, int64_t dim, int64_t stride, int tf32,
+                                 void* out) {
+    const int64_t total = static_cast<int64_t>(Nq) * stride;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t qrow = t / stride, c = t - qrow * stride;
+        const double v = (qrow < nq && c < dim) ? q64[qrow * dim + c] : 0.0;
+        if (tf32)
+            static_cast<float*>(out)[t] = static_cast<float>(v);
+        else
+            static_cast<__nv_bfloat16*>(out)[t] = __float2bfloat16_rn(static_cast<float>(v));
+    }
+}
+
+}  // namespace sine

@@ -290,8 +290,14 @@ def test_tensor_core_and_cuda_core_paths_agree(pkg, index_golden, scan):
     for ms in (0.9, -1.0, 0.2):
         a = idx.query_batch(qs, 5, ms)
         b = idx.query_batch(qs, 5, ms, cuda_core=True)
-        for x, y in zip(a, b):
+        c = idx.query_batch(qs, 5, ms, umma_v1=True)
+        for x, y, z in zip(a, b, c):
             np.testing.assert_array_equal(x, y)
+            np.testing.assert_array_equal(x, z)
+        for B in (8, 16, 33, 64):  # every resident group width
+            d = idx.query_batch(qs[:B], 5, ms)
+            for x, y in zip(d, b):
+                np.testing.assert_array_equal(x, y[:B])
 
 
 def test_tensor_core_bf16_raw_scores_within_tolerance(pkg):
