@@ -345,11 +345,17 @@ def measure_regimes(idx, rows, torch, hbm_peak):
     out = []
     stream = torch.cuda.current_stream().cuda_stream
     assert stream, "regimes must run on a non-default stream"
+    cases = []
     for scan in ("fp32", "bf16"):
-        for b, reps in ((1, 20), (64, 5), (4096, 1)):
+        for b, reps in ((1, 20), (8, 10), (64, 5), (4096, 1)):
             for tau in (TAU, -1.0):
                 if b == 4096 and tau == -1.0:
                     continue
+                cases.append((scan, b, reps, tau, "auto"))
+        cases.append((scan, 64, 5, TAU, "umma_v1"))
+        cases.append((scan, 64, 3, TAU, "cuda_core"))
+    for scan, b, reps, tau, path in cases:
+            if True:
                 qs = make_queries(rows, b, seed=100 + b)
                 q = torch.from_numpy(qs).cuda()
                 torch.cuda.synchronize()
@@ -357,7 +363,8 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                 sims = torch.empty((b, K), dtype=torch.float64, device="cuda")
                 cnt = torch.empty((b,), dtype=torch.int32, device="cuda")
                 run = lambda: idx.query_device(b, q.data_ptr(), K, tau, ids.data_ptr(), sims.data_ptr(),  # noqa
-                                               cnt.data_ptr(), stream, scan=scan)
+                                               cnt.data_ptr(), stream, scan=scan, cuda_core=path == "cuda_core",
+                                               umma_v1=path == "umma_v1")
                 run()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -370,7 +377,7 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                 n = rows.shape[0]
                 byt = algorithmic_bytes(n, DIM, b, K, scan)
                 flops = 2.0 * n * DIM * b
-                out.append({"batch": b, "scan": scan, "min_similarity": tau, "ms_per_batch": ms,
+                out.append({"batch": b, "scan": scan, "min_similarity": tau, "path": path, "ms_per_batch": ms,
                             "lookups_per_s": b / (ms / 1e3),
                             "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
                             "tflops": flops / (ms / 1e3) / 1e12})

@@ -215,10 +215,10 @@ class GpuCosineIndex:
 
     def query_device(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                      counts_ptr: int, stream: int | None = None, *, scan: str | None = None,
-                     rerank: bool | None = None, cuda_core: bool = False) -> None:
+                     rerank: bool | None = None, cuda_core: bool = False, umma_v1: bool = False) -> None:
         """Device-pointer variant (torch tensors); enqueued on `stream`."""
         N.check(self._lib.sine_query_device(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
-                                            float(min_similarity), self._mode(scan, rerank, cuda_core),
+                                            float(min_similarity), self._mode(scan, rerank, cuda_core, umma_v1),
                                             ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
                                             ctypes.c_void_p(counts_ptr),
                                             ctypes.c_void_p(stream) if stream else None))
