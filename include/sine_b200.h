@@ -57,6 +57,10 @@ extern "C" {
 #define SINE_NO_NORM_CHECK 0x100u/* caller already validated (|norm-1|<=1e-6)*/
 #define SINE_SCAN_CUDA_CORE 0x200u /* force the CUDA-core streaming scan      */
 #define SINE_SCAN_UMMA_V1  0x400u /* force the query-streaming tcgen05 kernel */
+#define SINE_CERTIFY       0x800u /* sine_query_device: check the per-query exactness
+                                     certificate and re-run failures on the fp32
+                                     CUDA-core scan (synchronises the stream);
+                                     sine_query always does this when re-ranking */
 
 /* ---- eviction policies (CacheConfig.eviction_policy, model.py:15) -------- */
 #define SINE_POLICY_LCFU 0
@@ -129,6 +133,8 @@ int sine_stream(sine_index_t *h, void **stream);
 int sine_set_timing(sine_index_t *h, int on);
 int sine_last_timing(sine_index_t *h, float *scan_ms, float *merge_ms, float *evict_ms);
 int sine_kernel_launches(sine_index_t *h, int64_t *n);
+/* Queries the last certified call had to re-run on the fp32 scan. */
+int sine_uncertified(sine_index_t *h, int64_t *n);
 /* Sum of device time (ms) and count of the launches of one kernel kind
  * (0 = stage-1 scan, 1 = merge/re-rank, 2 = tensor-core scan) recorded
  * while timing was on; reset != 0 clears the record. */

@@ -20,7 +20,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 SINE_OK, SINE_EINVAL, SINE_ECUDA, SINE_ENCCL, SINE_ENOMEM, SINE_ENOTFOUND, SINE_EDUP, SINE_ENORM = range(8)
 
 STORE_F32, STORE_BF16, STORE_META = 0x1, 0x2, 0x4
-SCAN_F32, SCAN_BF16, RERANK_F64, NO_NORM_CHECK, SCAN_CUDA_CORE, SCAN_UMMA_V1 = 0x0, 0x1, 0x10, 0x100, 0x200, 0x400
+SCAN_F32, SCAN_BF16, RERANK_F64, NO_NORM_CHECK, SCAN_CUDA_CORE, SCAN_UMMA_V1, CERTIFY = \
+    0x0, 0x1, 0x10, 0x100, 0x200, 0x400, 0x800
 POLICIES = {"lcfu": 0, "lru": 1, "lfu": 2}
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -65,6 +66,7 @@ _SIGS = {
     "sine_last_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
                                         ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "sine_kernel_launches": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
+    "sine_uncertified": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
     "sine_timing_totals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _f64p, _i64p, ctypes.c_int]),
     "sine_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "sine_host_free": (ctypes.c_int, [ctypes.c_void_p]),

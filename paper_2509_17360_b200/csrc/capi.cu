@@ -159,6 +159,10 @@ struct sine_index {
     DevBuf<int64_t> o_ids;
     DevBuf<double> o_sims;
     DevBuf<int32_t> o_cnt;
+    DevBuf<uint8_t> cert;         // per-query exactness certificates
+    int64_t uncertified = 0;      // queries re-run by the last certify pass
+    float cur_thr0 = 0.f;         // admission floor of the running query
+    double cur_err = 0.0;         // its filter error bound
     DevBuf<uint64_t> k1;
     DevBuf<uint64_t> vkeys;
     DevBuf<int32_t> vslots, cand, scratch_i32;
@@ -307,13 +311,38 @@ void check_rows_host(const sine_index* h, int64_t n, const double* rows) {
     }
 }
 
+// id -> live slot.  Ids appended in ascending order (the engine's monotone
+// element ids) are found by binary search over the slot-ordered id column;
+// otherwise through the hash map.
+int64_t find_slot(const sine_index* h, int64_t id) {
+    if (h->ids_ascending) {
+        auto it = std::lower_bound(h->ids_h.begin(), h->ids_h.end(), id);
+        if (it == h->ids_h.end() || *it != id) return -1;
+        const int64_t s = it - h->ids_h.begin();
+        return h->live_h[s] ? s : -1;
+    }
+    auto it = h->pos.find(id);
+    return it == h->pos.end() ? -1 : it->second;
+}
+
 void check_new_ids(const sine_index* h, int64_t n, const int64_t* ids) {
+    // fast path: a strictly ascending batch above every stored id
+    bool asc = h->nslots == 0 || ids[0] > h->max_id;
+    for (int64_t i = 1; asc && i < n; ++i) asc = ids[i] > ids[i - 1];
+    if (asc) return;
     std::unordered_set<int64_t> seen;
     seen.reserve(n * 2);
     for (int64_t i = 0; i < n; ++i) {
-        if (h->pos.count(ids[i]) || !seen.insert(ids[i]).second)
+        if (find_slot(h, ids[i]) >= 0 || !seen.insert(ids[i]).second)
             fail(SINE_EDUP, "duplicate id " + std::to_string(ids[i]));
     }
+}
+
+void build_pos_map(sine_index* h) {
+    h->pos.clear();
+    h->pos.reserve(h->nslots * 2);
+    for (int64_t s = 0; s < h->nslots; ++s)
+        if (h->live_h[s]) h->pos[h->ids_h[s]] = s;
 }
 
 void copy_meta(sine_index* h, int64_t s0, int64_t n, const sine_meta_cols_t* m) {
@@ -346,12 +375,19 @@ void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bo
     set_range_kernel<<<grid_for(n, 256, h->num_sms), 256, 0, h->stream>>>(h->valid, s0, n);
     ++h->launches;
     CK(cudaGetLastError());
+    const bool was_ascending = h->ids_ascending;
     for (int64_t i = 0; i < n; ++i) {
-        h->pos[ids[i]] = s0 + i;
         h->ids_h.push_back(ids[i]);
         h->live_h.push_back(1);
         if (ids[i] <= h->max_id) h->ids_ascending = false;
         h->max_id = std::max(h->max_id, ids[i]);
+    }
+    if (!h->ids_ascending) {
+        if (was_ascending) {
+            build_pos_map(h);
+        } else {
+            for (int64_t i = 0; i < n; ++i) h->pos[ids[i]] = s0 + i;
+        }
     }
     h->nslots += n;
     h->nlive += n;
@@ -392,13 +428,11 @@ void compact(sine_index* h) {
     ++h->launches;
     CK(cudaStreamSynchronize(h->stream));
     std::vector<int64_t> nid(n);
-    for (int64_t i = 0; i < n; ++i) {
-        nid[i] = h->ids_h[from[i]];
-        h->pos[nid[i]] = i;
-    }
+    for (int64_t i = 0; i < n; ++i) nid[i] = h->ids_h[from[i]];
     h->ids_h.swap(nid);
     h->live_h.assign(n, 1);
     h->nslots = n;
+    if (!h->ids_ascending) build_pos_map(h);
     dfrom.release();
 }
 
@@ -513,7 +547,7 @@ CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int6
     return m;
 }
 
-constexpr int kUmmaMinBatch = 8;
+constexpr int kUmmaMinBatch = 1;
 
 bool umma_eligible(const sine_index* h, int64_t B, bool bf16, uint32_t mode, int kp) {
     if (mode & SINE_SCAN_CUDA_CORE) return false;
@@ -524,7 +558,7 @@ bool umma_eligible(const sine_index* h, int64_t B, bool bf16, uint32_t mode, int
 }
 
 void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, int k, double min_sim, bool rerank,
-                  int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st);
+                  int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, int64_t cert_off);
 
 // widest resident query group (Q <= 96 KB of shared memory), 0 if < 16
 int res_nq_max(int64_t row_bytes) {
@@ -595,7 +629,7 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         h->launches += 2;
         CK(cudaGetLastError());
         merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
-                     counts_dev + q0, st);
+                     counts_dev + q0, st, q0);
     }
 }
 
@@ -613,6 +647,10 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         thr0 = static_cast<float>(min_sim);
         if (static_cast<double>(thr0) > min_sim) thr0 = std::nextafter(thr0, -INFINITY);
     }
+    // filter error bounds: tf32 operands keep 10 mantissa bits (|rel| <
+    // 2^-10 each), bf16 operands 8 bits rounded (2^-9 each); |q|=|x|=1
+    h->cur_thr0 = thr0;
+    h->cur_err = tf32 ? 2.0e-3 : 4.0e-3;
     // query-resident kernel (v2) when the group fits shared memory and costs
     // no more HBM passes than the query-streaming kernel (v1, 128 per pass)
     {
@@ -668,7 +706,7 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         h->launches += 2;
         CK(cudaGetLastError());
         merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
-                     counts_dev + q0, st);
+                     counts_dev + q0, st, q0);
     }
 }
 
@@ -702,6 +740,10 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         thr0 = static_cast<float>(min_sim);
         if (static_cast<double>(thr0) > min_sim) thr0 = std::nextafter(thr0, -INFINITY);
     }
+    // fp32 scan: two input roundings + <= 25 accumulation roundings of 2^-24
+    h->cur_thr0 = thr0;
+    h->cur_err = bf16 ? 4.0e-3 : 2.0e-6;
+    h->cert.ensure(std::max<int64_t>(B, 1));
 
     if (umma_eligible(h, B, bf16, mode, kp)) {
         umma_query(h, B, q_dev, k, kp, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st, mode);
@@ -768,13 +810,13 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         tend(h, tk, st);
         record(h, 1, st);
         merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
-                     counts_dev + q0, st);
+                     counts_dev + q0, st, q0);
         record(h, 2, st);
     }
 }
 
 void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, int k, double min_sim, bool rerank,
-                  int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+                  int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, int64_t cert_off) {
     MergeParams m{};
     m.in_key = h->lkey.p;
     m.in_slot = h->lslot.p;
@@ -789,6 +831,9 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.k = k;
     m.min_sim = min_sim;
     m.rerank = rerank ? 1 : 0;
+    m.thr0 = h->cur_thr0;
+    m.err = h->cur_err;
+    m.cert = h->cert.p ? h->cert.p + (cert_off) : nullptr;
     m.out_ids = ids_dev;
     m.out_sims = sims_dev;
     m.out_counts = counts_dev;
@@ -797,6 +842,33 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     tend(h, tm, st);
     ++h->launches;
     CK(cudaGetLastError());
+}
+
+// Queries whose certificate failed (fast filter too close to the k-th
+// similarity) are re-run through the fp32 CUDA-core scan, whose 2e-6 error
+// bound is inside the north star's 1e-5 tie window.  Synchronises `st`.
+int64_t certify_and_fix(sine_index* h, int64_t B, const double* q_dev, int k, double min_sim, uint32_t mode,
+                        int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+    if (!(mode & SINE_RERANK_F64) || !(h->flags & SINE_STORE_F32) || h->nlive == 0) return 0;
+    const bool bf16 = (mode & 0xF) == SINE_SCAN_BF16;
+    std::vector<uint8_t> cert(B);
+    CK(cudaMemcpyAsync(cert.data(), h->cert.p, B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const bool exact_path_used = !bf16 && (mode & SINE_SCAN_CUDA_CORE);
+    if (exact_path_used) return 0;
+    int64_t fixed = 0;
+    DevBuf<double> one_q;
+    one_q.ensure(h->dim);
+    for (int64_t b = 0; b < B; ++b) {
+        if (cert[b]) continue;
+        CK(cudaMemcpyAsync(one_q.p, q_dev + b * h->dim, h->dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        const uint32_t m2 = SINE_SCAN_F32 | SINE_RERANK_F64 | SINE_SCAN_CUDA_CORE;
+        query_device_impl(h, 1, one_q.p, k, min_sim, m2, ids_dev + b * k, sims_dev + b * k, counts_dev + b, st);
+        ++fixed;
+    }
+    if (fixed) CK(cudaStreamSynchronize(st));
+    one_q.release();
+    return fixed;
 }
 
 void check_queries_host(const sine_index* h, int64_t B, const double* q) {
@@ -965,7 +1037,7 @@ void remove_slots(sine_index* h, const std::vector<int64_t>& slots) {
     CK(cudaStreamSynchronize(h->stream));
     d.release();
     for (int64_t s : slots) {
-        h->pos.erase(h->ids_h[s]);
+        if (!h->ids_ascending) h->pos.erase(h->ids_h[s]);
         h->live_h[s] = 0;
     }
     h->nlive -= static_cast<int64_t>(slots.size());
@@ -1065,12 +1137,14 @@ int sine_remove(sine_index_t* h, int64_t n, const int64_t* ids) {
         CK(cudaSetDevice(h->device));
         std::vector<int64_t> slots;
         slots.reserve(n);
+        bool asc = true;
+        for (int64_t i = 1; asc && i < n; ++i) asc = ids[i] > ids[i - 1];
         std::unordered_set<int64_t> seen;
         for (int64_t i = 0; i < n; ++i) {
-            auto it = h->pos.find(ids[i]);
-            if (it == h->pos.end() || !seen.insert(ids[i]).second)
+            const int64_t sl = find_slot(h, ids[i]);
+            if (sl < 0 || (!asc && !seen.insert(ids[i]).second))
                 fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
-            slots.push_back(it->second);
+            slots.push_back(sl);
         }
         remove_slots(h, slots);
     });
@@ -1102,9 +1176,9 @@ int sine_get_rows(sine_index_t* h, int64_t n, const int64_t* ids, double* out) {
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
         for (int64_t i = 0; i < n; ++i) {
-            auto it = h->pos.find(ids[i]);
-            if (it == h->pos.end()) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
-            CK(cudaMemcpyAsync(out + i * h->dim, h->rows64 + it->second * h->dim, h->dim * sizeof(double),
+            const int64_t sl = find_slot(h, ids[i]);
+            if (sl < 0) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
+            CK(cudaMemcpyAsync(out + i * h->dim, h->rows64 + sl * h->dim, h->dim * sizeof(double),
                                cudaMemcpyDeviceToHost, h->stream));
         }
         CK(cudaStreamSynchronize(h->stream));
@@ -1125,6 +1199,8 @@ int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_si
         h->o_cnt.ensure(B);
         CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
+        h->uncertified = certify_and_fix(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p,
+                                         h->stream);
         CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
@@ -1143,6 +1219,8 @@ int sine_query_device(sine_index_t* h, int64_t B, const double* q_dev, int k, do
         CK(cudaSetDevice(h->device));
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
         query_device_impl(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
+        if (mode & SINE_CERTIFY)
+            h->uncertified = certify_and_fix(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
     });
 }
 
@@ -1155,9 +1233,8 @@ int sine_update_meta(sine_index_t* h, int64_t n, const int64_t* ids, const doubl
         CK(cudaSetDevice(h->device));
         std::vector<int64_t> slots(n);
         for (int64_t i = 0; i < n; ++i) {
-            auto it = h->pos.find(ids[i]);
-            if (it == h->pos.end()) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
-            slots[i] = it->second;
+            slots[i] = find_slot(h, ids[i]);
+            if (slots[i] < 0) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
         }
         if (n == 1) {
             const int64_t s = slots[0];
@@ -1272,6 +1349,10 @@ int sine_timing_totals(sine_index_t* h, int kind, double* total_ms, int64_t* lau
         *launches = n;
         if (reset) h->tused = 0;
     });
+}
+
+int sine_uncertified(sine_index_t* h, int64_t* n) {
+    return guarded([&] { *n = h->uncertified; });
 }
 
 int sine_kernel_launches(sine_index_t* h, int64_t* n) {

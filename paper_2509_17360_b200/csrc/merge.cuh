@@ -27,6 +27,9 @@ struct MergeParams {
     int k;
     double min_sim;
     int rerank;
+    float thr0;              // admission floor the scan used
+    double err;              // bound on |filter score - exact similarity|
+    uint8_t* cert;           // [nq] 1 = provably the exact top-k (nullable)
     int64_t* out_ids;        // [nq][k]
     double* out_sims;
     int32_t* out_counts;     // [nq]
@@ -123,7 +126,19 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     const uint32_t total = scratch[12];
     __syncthreads();
 
+    // every row that is not a candidate has a filter score <= bound_key
+    // (the selection cut, or the worst entry of a CTA's full list), or was
+    // below the admission floor
+    __shared__ uint32_t bound_key;
+    if (threadIdx.x == 0) bound_key = 0;
+    __syncthreads();
     if (total <= static_cast<uint32_t>(kp)) {
+        for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) {
+            if (ns[c] != kp) continue;
+            uint32_t mk = 0xffffffffu;
+            for (int e = 0; e < kp; ++e) mk = min(mk, key_at(c, e));
+            atomicMax(&bound_key, mk);
+        }
         for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
             int c, e;
             if (!flat_ok(f, c, e)) continue;
@@ -141,6 +156,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
                 return true;
             },
             nflat, static_cast<uint32_t>(kp), true, 32, hist, scratch, &nbefore, &nequal);
+        if (threadIdx.x == 0) bound_key = kstar;
         const uint32_t need_eq = kp - nbefore;
         // ties at the cut: keep the need_eq smallest ids
         uint64_t idcut = ~0ull;
@@ -216,6 +232,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             p.out_sims[static_cast<size_t>(qi) * p.k + r] = 0.0;
         }
         p.out_counts[qi] = outn;
+        if (p.cert) {
+            // certificate: no excluded row can reach the k-th similarity (or
+            // the threshold when fewer than k passed)
+            double bound = static_cast<double>(p.thr0);
+            if (bound_key) bound = fmax(bound, static_cast<double>(key_f32(bound_key)));
+            const double need = outn == p.k ? p.out_sims[static_cast<size_t>(qi) * p.k + p.k - 1] : p.min_sim;
+            p.cert[qi] = (!p.rerank || bound + p.err < need) ? 1 : 0;
+        }
     }
 }
 

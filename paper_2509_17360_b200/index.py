@@ -215,10 +215,16 @@ class GpuCosineIndex:
 
     def query_device(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                      counts_ptr: int, stream: int | None = None, *, scan: str | None = None,
-                     rerank: bool | None = None, cuda_core: bool = False, umma_v1: bool = False) -> None:
-        """Device-pointer variant (torch tensors); enqueued on `stream`."""
+                     rerank: bool | None = None, cuda_core: bool = False, umma_v1: bool = False,
+                     certify: bool = True) -> None:
+        """Device-pointer variant (torch tensors); enqueued on `stream`.
+
+        With `certify` (default) the per-query exactness certificate is
+        checked and failing queries are re-run on the fp32 scan; this
+        synchronises the stream once per call."""
+        mode = self._mode(scan, rerank, cuda_core, umma_v1) | (N.CERTIFY if certify else 0)
         N.check(self._lib.sine_query_device(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
-                                            float(min_similarity), self._mode(scan, rerank, cuda_core, umma_v1),
+                                            float(min_similarity), mode,
                                             ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
                                             ctypes.c_void_p(counts_ptr),
                                             ctypes.c_void_p(stream) if stream else None))
@@ -238,6 +244,12 @@ class GpuCosineIndex:
         n = ctypes.c_int64()
         N.check(self._lib.sine_timing_totals(self._h, kind, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
         return ms.value, n.value
+
+    def uncertified(self) -> int:
+        """Queries the last (certified) call re-ran on the fp32 scan."""
+        n = ctypes.c_int64()
+        N.check(self._lib.sine_uncertified(self._h, ctypes.byref(n)))
+        return n.value
 
     def kernel_launches(self) -> int:
         n = ctypes.c_int64()

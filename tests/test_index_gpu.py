@@ -321,3 +321,35 @@ def test_tensor_core_bf16_raw_scores_within_tolerance(pkg):
         assert np.all(np.diff(sims[j]) <= 0)
     print(f"tcgen05 bf16 (no re-rank) recall@10: {hit / (10 * B):.4f}")
     assert hit / (10 * B) >= 0.9
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_certificate_falls_back_on_dense_clusters(pkg, scan):
+    """Rows whose similarities are spaced ~1e-4 apart (far inside the tf32 /
+    bf16 filter error, far outside the fp32 one): the fast filter cannot be
+    certified, the query is re-run on the fp32 scan, and the answer is the
+    reference's exactly."""
+    rng = np.random.default_rng(5)
+    d, n = 256, 4000
+    base = rng.standard_normal(d)
+    base /= np.linalg.norm(base)
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    for i in range(300):                       # a tight cluster around the query
+        g = rows[i] - (rows[i] @ base) * base
+        g /= np.linalg.norm(g)
+        c = 0.999 - i * 1e-4
+        rows[i] = c * base + np.sqrt(1 - c * c) * g
+    ids = rng.permutation(10 * n)[:n]
+    idx = pkg.GpuCosineIndex(d, scan=scan, store_f32=True, store_bf16=True)
+    idx.insert_batch(ids, rows)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(ids, rows)
+    q = np.stack([base, rows[3000]])
+    for k in (5, 40):
+        got_ids, got_sims, cnt = idx.query_batch(q, k, -1.0)
+        for j in range(2):
+            want = ora.query(q[j], k, -1.0)
+            assert got_ids[j, :cnt[j]].tolist() == [c.id for c in want]
+            np.testing.assert_allclose(got_sims[j, :cnt[j]], [c.similarity for c in want], atol=1e-12)
+        assert idx.uncertified() >= 1
