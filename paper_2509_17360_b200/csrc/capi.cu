@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -834,6 +835,7 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.thr0 = h->cur_thr0;
     m.err = h->cur_err;
     m.cert = h->cert.p ? h->cert.p + (cert_off) : nullptr;
+    m.debug = getenv("SINE_DEBUG_CERT") ? 1 : 0;
     m.out_ids = ids_dev;
     m.out_sims = sims_dev;
     m.out_counts = counts_dev;

@@ -30,6 +30,7 @@ struct MergeParams {
     float thr0;              // admission floor the scan used
     double err;              // bound on |filter score - exact similarity|
     uint8_t* cert;           // [nq] 1 = provably the exact top-k (nullable)
+    int debug;
     int64_t* out_ids;        // [nq][k]
     double* out_sims;
     int32_t* out_counts;     // [nq]
@@ -239,6 +240,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             if (bound_key) bound = fmax(bound, static_cast<double>(key_f32(bound_key)));
             const double need = outn == p.k ? p.out_sims[static_cast<size_t>(qi) * p.k + p.k - 1] : p.min_sim;
             p.cert[qi] = (!p.rerank || bound + p.err < need) ? 1 : 0;
+            if (p.debug)
+                printf("cert q%d total=%u kp=%d bound_key=%08x bound=%.6f err=%g need=%.6f thr0=%f -> %d\n", qi,
+                       total, kp, bound_key, bound, p.err, need, p.thr0, p.cert[qi]);
         }
     }
 }

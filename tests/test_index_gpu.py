@@ -325,7 +325,7 @@ def test_tensor_core_bf16_raw_scores_within_tolerance(pkg):
 
 @pytest.mark.parametrize("scan", ["fp32", "bf16"])
 def test_certificate_falls_back_on_dense_clusters(pkg, scan):
-    """Rows whose similarities are spaced ~1e-4 apart (far inside the tf32 /
+    """Rows whose similarities are spaced 2e-5 apart (inside the tf32 /
     bf16 filter error, far outside the fp32 one): the fast filter cannot be
     certified, the query is re-run on the fp32 scan, and the answer is the
     reference's exactly."""
@@ -338,7 +338,7 @@ def test_certificate_falls_back_on_dense_clusters(pkg, scan):
     for i in range(300):                       # a tight cluster around the query
         g = rows[i] - (rows[i] @ base) * base
         g /= np.linalg.norm(g)
-        c = 0.999 - i * 1e-4
+        c = 0.999 - i * 2e-5
         rows[i] = c * base + np.sqrt(1 - c * c) * g
     ids = rng.permutation(10 * n)[:n]
     idx = pkg.GpuCosineIndex(d, scan=scan, store_f32=True, store_bf16=True)
