@@ -469,7 +469,8 @@ def measure_eviction(n, hbm_peak, cpu_sample=300_000):
     els = {i + 1: O.OracleElement(int(meta["staticity"][i]), int(meta["freq"][i]), float(meta["lat"][i]),
                                   float(meta["cost"][i]), int(meta["size"][i]), float(meta["created"][i]),
                                   float(meta["expiration"][i])) for i in range(m)}
-    ucap = int(0.9 * sum(int(x) for x in meta["size"][:m]))
+    live_m = (meta["expiration"][:m] - now) > 0.0
+    ucap = int(0.9 * int(meta["size"][:m][live_m].sum()))  # same 10%-of-live cut as the GPU run
     t0 = time.perf_counter()
     O.evict_until_fits(els, now, ucap)
     cpu_s = time.perf_counter() - t0
