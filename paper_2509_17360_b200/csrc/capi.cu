@@ -614,6 +614,7 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.thr0 = thr0;
         p.stages = S;
         p.tf32 = tf32 ? 1 : 0;
+        p.slot_ids = h->ids_ascending ? 1 : 0;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;
@@ -781,6 +782,7 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         p.chunk_warps = c.CW;
         p.row_groups = c.G;
         p.unroll = c.U;
+        p.slot_ids = h->ids_ascending ? 1 : 0;
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
@@ -839,8 +841,15 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.out_ids = ids_dev;
     m.out_sims = sims_dev;
     m.out_counts = counts_dev;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        attr = true;
+    }
+    const size_t pool_bytes = static_cast<size_t>(ncta) * kp * sizeof(uint32_t);
+    if (pool_bytes > 160 * 1024) fail(SINE_EINVAL, "candidate pool exceeds the merge kernel's shared memory");
     const size_t tm = tbegin(h, 1, st);
-    merge_kernel<<<nq, kMergeThreads, 0, st>>>(m);
+    merge_kernel<<<nq, kMergeThreads, pool_bytes, st>>>(m);
     tend(h, tm, st);
     ++h->launches;
     CK(cudaGetLastError());

@@ -116,6 +116,36 @@ __device__ __forceinline__ double warp_sum64(double v) {
     return v;
 }
 
+// Candidate (slot, key) order: key desc, then id asc.  When slots are in
+// id order (ids appended ascending) the slot decides ties without a load.
+__device__ __forceinline__ bool cand_better(uint2 a, uint2 b, const int64_t* ids, bool slot_ids) {
+    if (a.y != b.y) return a.y > b.y;
+    return slot_ids ? a.x < b.x : __ldg(ids + a.x) < __ldg(ids + b.x);
+}
+
+// Merge np pending (slot, key) candidates into one query's best-first list
+// (n entries, capacity kp) in a single warp step: every entry of list U
+// pending is ranked against all others and lands at its rank if < kp.
+// `scratch` holds n + np uint2.  Returns the new list length.
+__device__ __forceinline__ int warp_rank_merge(uint32_t* lk, int32_t* ls, int n, int kp, const uint2* pend, int np,
+                                               uint2* scratch, const int64_t* ids, bool slot_ids, int lane) {
+    const int tot = n + np;
+    for (int e = lane; e < tot; e += 32)
+        scratch[e] = e < n ? make_uint2(static_cast<uint32_t>(ls[e]), lk[e]) : pend[e - n];
+    __syncwarp();
+    for (int e = lane; e < tot; e += 32) {
+        const uint2 me = scratch[e];
+        int r = 0;
+        for (int f = 0; f < tot; ++f) r += cand_better(scratch[f], me, ids, slot_ids) ? 1 : 0;
+        if (r < kp) {
+            lk[r] = me.y;
+            ls[r] = static_cast<int32_t>(me.x);
+        }
+    }
+    __syncwarp();
+    return min(tot, kp);
+}
+
 __device__ __forceinline__ bool valid_bit(const uint32_t* valid, int64_t slot) {
     return (__ldg(valid + (slot >> 5)) >> (slot & 31)) & 1u;
 }

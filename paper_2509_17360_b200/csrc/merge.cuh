@@ -103,19 +103,26 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     __shared__ double sel_sim[kMaxKp];
     __shared__ uint32_t nsel;
 
+    extern __shared__ uint32_t pool[];  // [ncta * kp] candidate keys, 0 = empty
     const int qi = blockIdx.x;
     const int kp = p.kp, nq = p.nq;
     const int nflat = p.ncta * kp;
     for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) ns[c] = p.in_n[c * nq + qi];
     if (threadIdx.x == 0) nsel = 0;
     __syncthreads();
+    // stage the pooled keys once: every radix pass below reads shared memory
+    for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
+        const int c = f / kp, e = f - c * kp;
+        pool[f] = e < ns[c] ? p.in_key[(static_cast<size_t>(c) * nq + qi) * kp + e] : 0u;
+    }
+    __syncthreads();
 
     auto flat_ok = [&](int f, int& c, int& e) {
         c = f / kp;
         e = f - c * kp;
-        return e < ns[c];
+        return pool[f] != 0u;
     };
-    auto key_at = [&](int c, int e) { return p.in_key[(static_cast<size_t>(c) * nq + qi) * kp + e]; };
+    auto key_at = [&](int c, int e) { return pool[c * kp + e]; };
     auto slot_at = [&](int c, int e) { return p.in_slot[(static_cast<size_t>(c) * nq + qi) * kp + e]; };
 
     // total candidates

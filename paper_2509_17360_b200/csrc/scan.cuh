@@ -42,6 +42,7 @@ struct ScanParams {
     int chunk_warps;        // CW = ceil(C / CPW)
     int row_groups;         // G
     int unroll;             // RPW: rows per warp per stage (multiple of U; R = G * RPW)
+    int slot_ids;           // slot order == id order
     uint32_t* out_key;      // [grid][nq][kp] f32_key(score)
     int32_t* out_slot;      // [grid][nq][kp]
     int32_t* out_n;         // [grid][nq]
@@ -79,7 +80,7 @@ struct RowTraits<__nv_bfloat16> {
 };
 
 struct ScanSmemLayout {
-    size_t stage_off, bar_off, partial_off, list_key_off, list_slot_off, qstate_off, pend_off, total;
+    size_t stage_off, bar_off, partial_off, list_key_off, list_slot_off, qstate_off, pend_off, scratch_off, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -102,6 +103,8 @@ __host__ __device__ inline ScanSmemLayout scan_smem_layout(int S, int R, int64_t
     off += align_up(3 * NQ * sizeof(uint32_t), 16);
     L.pend_off = off;  // 2 x { total, cnt[NQ], entries[NQ][R] {slot, key} }
     off += 2 * align_up(align_up((1 + NQ) * sizeof(uint32_t), 16) + static_cast<size_t>(NQ) * R * 8, 16);
+    L.scratch_off = off;  // per compute warp: (kp + R) uint2 for the rank merge
+    off += static_cast<size_t>(16) * (kp + R) * 8;
     L.total = off;
     return L;
 }
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.qstate_off);
     uint32_t* worst = cnt + NQ;
     uint32_t* thr = worst + NQ;
+    uint2* merge_scratch = reinterpret_cast<uint2*>(smem + L.scratch_off);
     const size_t pend_hdr = align_up((1 + NQ) * sizeof(uint32_t), 16);  // keeps the uint2 entries 8-B aligned
     const size_t pend_bytes = align_up(pend_hdr + static_cast<size_t>(NQ) * R * 8, 16);
 
@@ -371,51 +375,19 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
             }
             if (*pend_total == 0) continue;  // uniform: written before the barrier
 
-            // ---- insertions: one warp per query ----
+            // ---- insertions: one warp per query, one rank-merge per stage ----
             for (int jq = warp; jq < nq; jq += W) {
+                const int np = static_cast<int>(pend_cnt[jq]);
+                if (np == 0) continue;
                 uint32_t* lk = lkey + jq * kp;
                 int32_t* ls = lslot + jq * kp;
-                const uint32_t np = pend_cnt[jq];
-                for (uint32_t e = 0; e < np; ++e) {
-                    const uint2 cand = pend_e[jq * R + e];
-                    const uint32_t key = cand.y;
-                    const int32_t slot = static_cast<int32_t>(cand.x);
-                    uint32_t n = cnt[jq];
-                    if (n < static_cast<uint32_t>(kp)) {
-                        if (lane == 0) {
-                            lk[n] = key;
-                            ls[n] = slot;
-                        }
-                        __syncwarp();
-                        ++n;
-                        if (lane == 0) cnt[jq] = n;
-                        if (n == static_cast<uint32_t>(kp)) {
-                            const int w = list_worst(lk, ls, kp, p.ids, lane);
-                            if (lane == 0) {
-                                worst[jq] = w;
-                                thr[jq] = max(thr0, lk[w]);
-                            }
-                        }
-                        __syncwarp();
-                        continue;
-                    }
-                    const uint32_t w = worst[jq];
-                    const uint32_t wk = lk[w];
-                    bool better = key > wk;
-                    if (key == wk) better = __ldg(p.ids + slot) < __ldg(p.ids + ls[w]);
-                    if (!better) continue;  // warp-uniform
-                    if (lane == 0) {
-                        lk[w] = key;
-                        ls[w] = slot;
-                    }
-                    __syncwarp();
-                    const int nw = list_worst(lk, ls, kp, p.ids, lane);
-                    if (lane == 0) {
-                        worst[jq] = nw;
-                        thr[jq] = max(thr0, lk[nw]);
-                    }
-                    __syncwarp();
+                const int n = warp_rank_merge(lk, ls, static_cast<int>(cnt[jq]), kp, pend_e + jq * R, np,
+                                              merge_scratch + warp * (kp + R), p.ids, p.slot_ids != 0, lane);
+                if (lane == 0) {
+                    cnt[jq] = n;
+                    if (n == kp) thr[jq] = max(thr0, lk[kp - 1]);
                 }
+                __syncwarp();
             }
             named_bar_sync(1, nthreads);
         }

@@ -379,7 +379,7 @@ namespace sine {
 // ===========================================================================
 
 constexpr int kResMaxNq = 64;
-constexpr int kResQPer = 16;  // pending entries per query per round
+constexpr int kResQPer = 32;  // pending entries per query per round
 
 struct ResParams {
     int64_t nslots;
@@ -390,6 +390,7 @@ struct ResParams {
     float thr0;
     int stages;
     int tf32;
+    int slot_ids;     // slot order == id order (ties resolved without loads)
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -422,6 +423,7 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     off += static_cast<size_t>(Nq) * 4 + 16;
     off = (off + 15) / 16 * 16;
     off += static_cast<size_t>(Nq) * kResQPer * 8;
+    off += static_cast<size_t>(4) * (kMaxKp + kResQPer) * 8;  // per-warp merge scratch
     L.total = off + 1024;
     return L;
 }
@@ -469,6 +471,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     float* thr = reinterpret_cast<float*>(worst + NQ);
     uint32_t* pcnt = reinterpret_cast<uint32_t*>(smem + L.pend_off);
     uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
+    uint2* merge_scratch = pend + NQ * kResQPer;
     constexpr uint32_t kTmemCols = NQ <= 16 ? 32 : (2 * NQ <= 64 ? 64 : 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -609,49 +612,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 }
                 named_bar_sync(2, 128);
                 for (int j = warp; j < p.nq; j += 4) {
-                    const uint32_t np = min(pcnt[j], static_cast<uint32_t>(kResQPer));
-                    uint32_t* lk = lkey + j * kp;
-                    int32_t* ls = lslot + j * kp;
-                    for (uint32_t e = 0; e < np; ++e) {
-                        const uint2 cand = pend[j * kResQPer + e];
-                        const uint32_t key = cand.y;
-                        const int32_t sl = static_cast<int32_t>(cand.x);
-                        uint32_t n = cnt[j];
-                        if (n < static_cast<uint32_t>(kp)) {
-                            if (lane == 0) {
-                                lk[n] = key;
-                                ls[n] = sl;
-                            }
-                            __syncwarp();
-                            ++n;
-                            if (lane == 0) cnt[j] = n;
-                            if (n == static_cast<uint32_t>(kp)) {
-                                const int w = list_worst(lk, ls, kp, p.ids, lane);
-                                if (lane == 0) {
-                                    worst[j] = w;
-                                    thr[j] = fmaxf(p.thr0, key_f32(lk[w]));
-                                }
-                            }
-                            __syncwarp();
-                            continue;
-                        }
-                        const uint32_t w = worst[j];
-                        const uint32_t wk = lk[w];
-                        bool better = key > wk;
-                        if (key == wk) better = __ldg(p.ids + sl) < __ldg(p.ids + ls[w]);
-                        if (!better) continue;
+                    const int np = static_cast<int>(min(pcnt[j], static_cast<uint32_t>(kResQPer)));
+                    if (np > 0) {
+                        uint32_t* lk = lkey + j * kp;
+                        int32_t* ls = lslot + j * kp;
+                        const int n = warp_rank_merge(lk, ls, static_cast<int>(cnt[j]), kp, pend + j * kResQPer, np,
+                                                      merge_scratch + warp * (kMaxKp + kResQPer), p.ids,
+                                                      p.slot_ids != 0, lane);
                         if (lane == 0) {
-                            lk[w] = key;
-                            ls[w] = sl;
+                            cnt[j] = n;
+                            if (n == kp) thr[j] = fmaxf(p.thr0, key_f32(lk[kp - 1]));
                         }
-                        __syncwarp();
-                        const int nw = list_worst(lk, ls, kp, p.ids, lane);
-                        if (lane == 0) {
-                            worst[j] = nw;
-                            thr[j] = fmaxf(p.thr0, key_f32(lk[nw]));
-                        }
-                        __syncwarp();
                     }
+                    __syncwarp();
                     if (lane == 0) pcnt[j] = 0;
                 }
                 named_bar_sync(2, 128);
