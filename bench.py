@@ -283,8 +283,14 @@ def run_ours(args):
     q_per_launch = b / launches_per_step
     bytes_per_launch = algorithmic_bytes(shard_rows, DIM, q_per_launch, K, args.scan)
     achieved = bytes_per_launch / (scan_avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):  # dram bytes per launch from the committed ncu --set full capture
+        t = json.load(open(tpath)).get(kernel_name)
+        if t and args.scan == "fp32" and b == 1 and args.rows == N_ROWS:
+            traffic = t["dram_bytes_per_launch"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                 "kernel": kernel_name, "kernel_ms": scan_avg_ms,
                 "scan_share_of_step": scan_ms / max(elapsed_ms, 1e-9),
                 "bytes_per_launch": bytes_per_launch, "frac_of_nominal_8tbs": achieved / 8000.0}
