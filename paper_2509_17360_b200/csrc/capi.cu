@@ -567,18 +567,49 @@ int res_nq_max(int64_t row_bytes) {
     return n >= 64 ? 64 : n >= 32 ? 32 : n >= 16 ? 16 : 0;
 }
 
-template <int NQ>
-void launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int grid, size_t smem,
-                cudaStream_t st) {
+template <int NQ, int CS>
+int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters, size_t smem,
+               cudaStream_t st) {
+    auto kern = umma_res_kernel<NQ, CS>;
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(umma_res_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
-    umma_res_kernel<NQ><<<grid, kUmmaThreads, smem, st>>>(qmap, rmap, p);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kUmmaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(max_clusters * CS);
+    int active = 0;  // clusters the GPU can hold at once (persistent grid: one wave)
+    CK(cudaOccupancyMaxActiveClusters(&active, kern, &cfg));
+    const int ncl = std::max(1, std::min(max_clusters, active));
+    cfg.gridDim = dim3(ncl * CS);
+    CK(cudaLaunchKernelEx(&cfg, kern, qmap, rmap, p));
+    return ncl;
 }
 
-// Query-resident tensor-core scan, groups of NQ queries (one HBM pass each).
+template <int NQ>
+int launch_res_cs(int CS, const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters,
+                  size_t smem, cudaStream_t st) {
+    switch (CS) {
+        case 1: return launch_res<NQ, 1>(qmap, rmap, p, max_clusters, smem, st);
+        case 2: return launch_res<NQ, 2>(qmap, rmap, p, max_clusters, smem, st);
+        case 4: return launch_res<NQ, 4>(qmap, rmap, p, max_clusters, smem, st);
+        default: return launch_res<NQ, 8>(qmap, rmap, p, max_clusters, smem, st);
+    }
+}
+
+// Query-resident tensor-core scan.  One launch = one HBM pass serving up to
+// 8 clusters-ranks x NQ queries (each CTA of a cluster keeps its own query
+// group; the row tiles are TMA-multicast across the cluster).
 void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
                     bool bf16, bool rerank, int NQmax, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
                     cudaStream_t st) {
@@ -587,23 +618,27 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
     const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
     const int kblocks = static_cast<int>(row_bytes / kUmmaKB);
     const int ntiles = static_cast<int>((h->nslots + kUmmaN - 1) / kUmmaN);
-    const int grid = std::max(1, std::min(h->num_sms, ntiles));
-    h->qbf.ensure(static_cast<size_t>(NQmax) * row_elems * 2);
-    h->lkey.ensure(static_cast<size_t>(grid) * NQmax * kp);
-    h->lslot.ensure(static_cast<size_t>(grid) * NQmax * kp);
-    h->ln.ensure(static_cast<size_t>(grid) * NQmax);
+    constexpr int kMaxCS = 8;
+    h->qbf.ensure(static_cast<size_t>(kMaxCS) * NQmax * row_elems * 2);
+    h->lkey.ensure(static_cast<size_t>(h->num_sms) * kMaxCS * NQmax * kp);
+    h->lslot.ensure(static_cast<size_t>(h->num_sms) * kMaxCS * NQmax * kp);
+    h->ln.ensure(static_cast<size_t>(h->num_sms) * kMaxCS * NQmax);
     const void* rows = tf32 ? static_cast<const void*>(h->rows32) : static_cast<const void*>(h->rows16);
-    const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots);
-    for (int64_t q0 = 0; q0 < B; q0 += NQmax) {
-        const int nq = static_cast<int>(std::min<int64_t>(NQmax, B - q0));
-        const int NQ = nq <= 16 ? 16 : nq <= 32 ? 32 : 64;
+    for (int64_t q0 = 0; q0 < B;) {
+        const int64_t rem = B - q0;
+        int CS = 1;
+        while (CS < kMaxCS && CS * NQmax < rem) CS <<= 1;
+        const int64_t per = (rem + CS - 1) / CS;
+        const int NQ = per <= 16 ? 16 : per <= 32 ? 32 : 64;
+        const int nq = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(CS) * NQ, rem));
         const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp);
         const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
         if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
         const ResSmem L = res_smem_layout(S, NQ, kblocks, kp);
-        res_prep_queries<<<grid_for(static_cast<int64_t>(NQ) * row_elems, 256, h->num_sms), 256, 0, st>>>(
-            q_dev + q0 * h->dim, nq, NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
-        const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, NQ, NQ);
+        res_prep_queries<<<grid_for(static_cast<int64_t>(CS) * NQ * row_elems, 256, h->num_sms), 256, 0, st>>>(
+            q_dev + q0 * h->dim, nq, CS * NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
+        const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, static_cast<int64_t>(CS) * NQ, NQ);
+        const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots, kUmmaN / CS);
         ResParams p{};
         p.nslots = h->nslots;
         p.ntiles = ntiles;
@@ -620,18 +655,21 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
+        const int max_clusters = std::max(1, std::min(h->num_sms / CS, ntiles));
         const size_t tk = tbegin(h, 2, st);
+        int ncl;
         if (NQ == 16)
-            launch_res<16>(qmap, rmap, p, grid, L.total, st);
+            ncl = launch_res_cs<16>(CS, qmap, rmap, p, max_clusters, L.total, st);
         else if (NQ == 32)
-            launch_res<32>(qmap, rmap, p, grid, L.total, st);
+            ncl = launch_res_cs<32>(CS, qmap, rmap, p, max_clusters, L.total, st);
         else
-            launch_res<64>(qmap, rmap, p, grid, L.total, st);
+            ncl = launch_res_cs<64>(CS, qmap, rmap, p, max_clusters, L.total, st);
         tend(h, tk, st);
         h->launches += 2;
         CK(cudaGetLastError());
-        merge_launch(h, grid, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
+        merge_launch(h, ncl, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k, sims_dev + q0 * k,
                      counts_dev + q0, st, q0);
+        q0 += nq;
     }
 }
 
@@ -660,7 +698,9 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         const int64_t passes2 = nq2 ? (B + nq2 - 1) / nq2 : INT64_MAX;
         const int64_t passes1 = (B + kUmmaM - 1) / kUmmaM;
         const bool force_v1 = (mode & 0x400u) != 0;
-        if (!force_v1 && nq2 && (passes2 <= passes1 || bf16)) {
+        (void)passes1;
+        (void)passes2;
+        if (!force_v1 && nq2) {
             umma_res_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, nq2, ids_dev, sims_dev, counts_dev, st);
             return;
         }

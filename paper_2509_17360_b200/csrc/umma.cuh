@@ -448,7 +448,51 @@ __device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool v) {
           "=r"(r[15])                                                                                        \
         : "r"(taddr))
 
-template <int NQ>
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_count_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// TMA 2-D load whose bytes land at the same shared-memory offset in every
+// CTA of `mask`, signalling complete_tx on each CTA's mbarrier at `bar`'s
+// offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+        : "memory");
+}
+
+// tcgen05.commit arriving on the mbarrier at `bar`'s offset in every CTA of `mask`.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+// CS = thread-block cluster size.  The CS CTAs of a cluster hold CS
+// different query groups (NQ each) and share every 128-row tile: each CTA
+// TMA-loads 128/CS rows of it and multicasts them to the whole cluster, so
+// one HBM pass over the index serves CS * NQ queries.
+template <int NQ, int CS>
 __global__ void __launch_bounds__(kUmmaThreads, 1)
     umma_res_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
                     const ResParams p) {
@@ -478,7 +522,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, CS);  // released by the MMA commits of every CTA in the cluster
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
@@ -493,13 +537,22 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         thr[j] = p.thr0;
         pcnt[j] = 0;
     }
+    const int crank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const int cid = CS > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+    const int ncl = CS > 1 ? static_cast<int>(cluster_count_x()) : static_cast<int>(gridDim.x);
+    const int nq_local = max(0, min(NQ, p.nq - crank * NQ));
+    constexpr uint16_t kMask = static_cast<uint16_t>((1u << CS) - 1u);
+    constexpr int kSliceRows = kUmmaN / CS;
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CS > 1)
+        cluster_sync_all();  // every CTA's barriers exist before any multicast lands
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int kb_elems = p.tf32 ? kUmmaKB / 4 : kUmmaKB / 2;
@@ -511,18 +564,23 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
             const uint64_t pol_rows = l2_evict_first_policy();
             const uint64_t pol_q = l2_evict_last_policy();
-            // the whole query group, once
+            // this CTA's query group, once
             mbar_arrive_expect_tx(qfull, static_cast<uint32_t>(nkb) * NQ * kUmmaKB);
             for (int kb = 0; kb < nkb; ++kb)
-                tma_load_2d(sq + static_cast<size_t>(kb) * NQ * kUmmaKB, &qmap, qfull, kb * kb_elems, 0, pol_q);
+                tma_load_2d(sq + static_cast<size_t>(kb) * NQ * kUmmaKB, &qmap, qfull, kb * kb_elems, crank * NQ,
+                            pol_q);
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+            for (int t = cid; t < p.ntiles; t += ncl) {
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(empty + s, ph ^ 1);
                     mbar_arrive_expect_tx(full + s, kUmmaN * kUmmaKB);
-                    tma_load_2d(sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB, &rmap, full + s, kb * kb_elems,
-                                t * kUmmaN, pol_rows);
+                    uint8_t* dst = sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB + crank * kSliceRows * kUmmaKB;
+                    if constexpr (CS > 1)
+                        tma_load_2d_mc(dst, &rmap, full + s, kb * kb_elems, t * kUmmaN + crank * kSliceRows, kMask,
+                                       pol_rows);
+                    else
+                        tma_load_2d(dst, &rmap, full + s, kb * kb_elems, t * kUmmaN, pol_rows);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -538,7 +596,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             int s = 0;
             uint32_t ph = 0;
             int i = 0;
-            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+            for (int t = cid; t < p.ntiles; t += ncl, ++i) {
                 const int acc = i & 1;
                 mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -558,7 +616,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                         else
                             umma_f16(d, ad, bd, idesc, accum);
                     }
-                    umma_commit(empty + s);
+                    if constexpr (CS > 1)
+                        umma_commit_mc(empty + s, kMask);  // the stage is free in this CTA's view
+                    else
+                        umma_commit(empty + s);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -571,7 +632,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         // ---------------- epilogue: thread = row ----------------
         const int tid = threadIdx.x;  // 0..127 == TMEM lane == row within tile
         int i = 0;
-        for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+        for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
             const int64_t slot = static_cast<int64_t>(t) * kUmmaN + tid;
             const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
@@ -596,7 +657,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             if (live) {
 #pragma unroll
                 for (int j = 0; j < NQ; ++j)
-                    if (j < p.nq && sc[j] >= thr[j]) mask |= 1ull << j;
+                    if (j < nq_local && sc[j] >= thr[j]) mask |= 1ull << j;
             }
             while (bar_red_or(1, 128, mask != 0)) {
                 // queue what fits, then insert warp-per-query
@@ -611,7 +672,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     }
                 }
                 named_bar_sync(2, 128);
-                for (int j = warp; j < p.nq; j += 4) {
+                for (int j = warp; j < nq_local; j += 4) {
                     const int np = static_cast<int>(min(pcnt[j], static_cast<uint32_t>(kResQPer)));
                     if (np > 0) {
                         uint32_t* lk = lkey + j * kp;
@@ -637,18 +698,22 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
         }
         named_bar_sync(2, 128);
-        for (int j = 0; j < p.nq; ++j) {
+        for (int j = 0; j < nq_local; ++j) {
+            const int qg = crank * NQ + j;  // query index within the launch
             const uint32_t n = cnt[j];
-            const size_t base = (static_cast<size_t>(blockIdx.x) * p.nq + j) * kp;
+            const size_t base = (static_cast<size_t>(cid) * p.nq + qg) * kp;
             for (int e = tid; e < static_cast<int>(n); e += 128) {
                 p.out_key[base + e] = lkey[j * kp + e];
                 p.out_slot[base + e] = lslot[j * kp + e];
             }
-            if (tid == 0) p.out_n[blockIdx.x * p.nq + j] = static_cast<int>(n);
+            if (tid == 0) p.out_n[cid * p.nq + qg] = static_cast<int>(n);
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CS > 1)
+        cluster_sync_all();  // no CTA leaves while peers may still multicast into it
+    else
+        __syncthreads();
     if (warp == 5) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));

@@ -294,7 +294,7 @@ def test_tensor_core_and_cuda_core_paths_agree(pkg, index_golden, scan):
         for x, y, z in zip(a, b, c):
             np.testing.assert_array_equal(x, y)
             np.testing.assert_array_equal(x, z)
-        for B in (8, 16, 33, 64):  # every resident group width
+        for B in (8, 16, 33, 64, 100, 129):  # resident group widths and cluster sizes 1, 2, 4
             d = idx.query_batch(qs[:B], 5, ms)
             for x, y in zip(d, b):
                 np.testing.assert_array_equal(x, y[:B])
