@@ -629,9 +629,10 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         int CS = 1;
         while (CS < kMaxCS && CS * NQmax < rem) CS <<= 1;
         const int64_t per = (rem + CS - 1) / CS;
-        const int NQ = per <= 16 ? 16 : per <= 32 ? 32 : 64;
+        const int NQ = std::min(NQmax, per <= 16 ? 16 : per <= 32 ? 32 : 64);
         const int nq = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(CS) * NQ, rem));
         const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp);
+        if (L0.total + 2 * kUmmaN * kUmmaKB > 227 * 1024) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
         const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
         if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
         const ResSmem L = res_smem_layout(S, NQ, kblocks, kp);

@@ -237,7 +237,7 @@ def test_dimension_sweep(pkg, d):
 def test_large_batch_groups(pkg):
     """B > the per-launch query group: several scan launches, same answers."""
     rng = np.random.default_rng(8)
-    n, d, B = 5000, 128, 70
+    n, d, B = 5000, 128, 1100
     rows = rng.standard_normal((n, d))
     rows /= np.linalg.norm(rows, axis=1, keepdims=True)
     q = rng.standard_normal((B, d))
