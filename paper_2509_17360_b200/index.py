@@ -110,7 +110,7 @@ class GpuCosineIndex:
         return self._h
 
     def _mode(self, scan: str | None = None, rerank: bool | None = None, cuda_core: bool = False,
-              umma_v1: bool = False) -> int:
+              umma_v1: bool = False, cluster: bool = False) -> int:
         scan = scan or self.scan
         rerank = self.rerank if rerank is None else rerank
         m = N.SCAN_BF16 if scan == "bf16" else N.SCAN_F32
@@ -120,6 +120,8 @@ class GpuCosineIndex:
             m |= N.SCAN_CUDA_CORE
         if umma_v1:
             m |= N.SCAN_UMMA_V1
+        if cluster:
+            m |= N.SCAN_CLUSTER
         return m | N.NO_NORM_CHECK
 
     # ------------------------------------------------------------ queries
@@ -185,7 +187,7 @@ class GpuCosineIndex:
 
     def query_batch(self, queries, k: int, min_similarity: float = -1.0, *, scan: str | None = None,
                     rerank: bool | None = None, check: bool = True, cuda_core: bool = False,
-                    umma_v1: bool = False):
+                    umma_v1: bool = False, cluster: bool = False):
         """B independent queries in one pass over the index.
 
         Returns (ids int64[B, k] padded with -1, sims float64[B, k],
@@ -193,7 +195,7 @@ class GpuCosineIndex:
         q = check_matrix(queries, self.dimension) if check else N.f64(queries)
         if k < 1:
             raise ValidationError("k must be >= 1")
-        return self._query(q, k, min_similarity, self._mode(scan, rerank, cuda_core, umma_v1))
+        return self._query(q, k, min_similarity, self._mode(scan, rerank, cuda_core, umma_v1, cluster))
 
     def _query(self, q: np.ndarray, k: int, min_similarity: float, mode: int):
         B = q.shape[0]

@@ -247,10 +247,11 @@ def test_large_batch_groups(pkg):
     for scan in ("fp32", "bf16"):
         idx = pkg.GpuCosineIndex(d, scan=scan)
         idx.insert_batch(np.arange(n), rows)
-        ids, sims, counts = idx.query_batch(q, 20, 0.1)
-        for j in range(B):
-            want = ora.query(q[j], 20, 0.1)
-            assert ids[j, :counts[j]].tolist() == [c.id for c in want]
+        for cl in (False, True):  # cluster size 8 with multicast rows
+            ids, sims, counts = idx.query_batch(q, 20, 0.1, cluster=cl)
+            for j in range(B):
+                want = ora.query(q[j], 20, 0.1)
+                assert ids[j, :counts[j]].tolist() == [c.id for c in want]
 
 
 def test_full_size_properties(pkg):
@@ -294,10 +295,11 @@ def test_tensor_core_and_cuda_core_paths_agree(pkg, index_golden, scan):
         for x, y, z in zip(a, b, c):
             np.testing.assert_array_equal(x, y)
             np.testing.assert_array_equal(x, z)
-        for B in (8, 16, 33, 64, 100, 129):  # resident group widths and cluster sizes 1, 2, 4
-            d = idx.query_batch(qs[:B], 5, ms)
-            for x, y in zip(d, b):
-                np.testing.assert_array_equal(x, y[:B])
+        for B in (8, 16, 33, 64, 100, 129):  # resident group widths; cluster sizes 1, 2, 4
+            for cl in (False, True):
+                d = idx.query_batch(qs[:B], 5, ms, cluster=cl)
+                for x, y in zip(d, b):
+                    np.testing.assert_array_equal(x, y[:B])
 
 
 def test_tensor_core_bf16_raw_scores_within_tolerance(pkg):
