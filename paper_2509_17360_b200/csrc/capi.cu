@@ -169,7 +169,12 @@ struct sine_index {
     DevBuf<int32_t> vslots, cand, scratch_i32;
     DevBuf<int64_t> vids;
     DevBuf<uint8_t> cub_tmp;
-    DevBuf<unsigned long long> hist;  // hw[256] hc[256] hand[3] hor[3] + counter
+    DevBuf<unsigned long long> hist;  // hw[256] hc[256] hand[3] hor[3] counter kand[3] kor[3]
+    DevBuf<Pack2> vpack, vpack_out;
+    DevBuf<Key3> vkey_out;
+    DevBuf<int32_t> vslots_out;
+    DevBuf<int64_t> exp_off;
+    HostBuf<unsigned long long> sel_h;  // counter + kand + kor
     DevBuf<SelectState> st;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
     HostBuf<SelectState> st_h;
@@ -203,6 +208,14 @@ __global__ void set_bits_kernel(uint32_t* valid, const int64_t* slots, int64_t n
             atomicOr(valid + (s >> 5), bit);
         else
             atomicAnd(valid + (s >> 5), ~bit);
+    }
+}
+
+__global__ void set_bits32_kernel(uint32_t* valid, const int32_t* slots, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = slots[i];
+        atomicAnd(valid + (s >> 5), ~(1u << (s & 31)));
     }
 }
 
@@ -954,6 +967,10 @@ EvictCols evict_cols(const sine_index* h) {
     return c;
 }
 
+struct PackDecomposer {
+    __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&> operator()(Pack2& k) const { return {k.hi, k.lo}; }
+};
+
 struct KeyDecomposer {
     __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&, uint64_t&> operator()(Key3& k) const {
         return {k.a, k.b, k.c};
@@ -967,15 +984,17 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     cudaStream_t st = h->stream;
     record(h, 3, st);
     h->k1.ensure(std::max<int64_t>(h->cap, 1));
-    h->hist.ensure(256 * 2 + 6 + 2);
+    h->hist.ensure(256 * 2 + 6 + 1 + 6);
     h->st.ensure(1);
     h->st_h.ensure(1);
-    h->n_h.ensure(1);
+    h->sel_h.ensure(7);
     unsigned long long* hw = h->hist.p;
     unsigned long long* hc = hw + 256;
     unsigned long long* hand = hc + 256;
     unsigned long long* hor = hand + 3;
     unsigned long long* counter = hor + 3;
+    unsigned long long* kand = counter + 1;
+    unsigned long long* kor = kand + 3;
     CK(cudaMemsetAsync(hw, 0, 512 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(hand, 0xff, 3 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(hor, 0, 3 * sizeof(unsigned long long), st));
@@ -986,7 +1005,9 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     CK(cudaMemcpyAsync(h->st.p, h->st_h.p, sizeof(SelectState), cudaMemcpyHostToDevice, st));
 
     const EvictCols cols = evict_cols(h);
-    const int64_t cand_max = std::max<int64_t>(1 << 20, h->nlive / 8);
+    // shrink the working set to the prefix-matching slots once they are at
+    // most ~60% of the live ones: later passes then gather only those
+    const int64_t cand_max = std::max<int64_t>(1 << 20, h->nlive * 6 / 10);
     const int32_t* cand = nullptr;
     int64_t ncand = 0;
     bool first = true;
@@ -1013,7 +1034,6 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         const SelectState s = *h->st_h.p;
         if (s.done) break;
         if (!cand && s.count <= cand_max) {
-            // shrink the working set to the slots that match the prefix
             h->cand.ensure(s.count);
             CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
             CollectArgs ca{};
@@ -1031,10 +1051,11 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
             ncand = s.count;
         }
     }
-    // collect victims (key prefix <= T) and order them
-    const SelectState s = *h->st_h.p;
-    const int64_t vmax = s.done == 2 ? h->nlive : h->nlive;  // upper bound
+    // collect the victims (key prefix <= T) with the AND / OR of their keys
+    const int64_t vmax = h->nlive;
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(kand, 0xff, 3 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(kor, 0, 3 * sizeof(unsigned long long), st));
     h->vkeys.ensure(3 * std::max<int64_t>(vmax, 1));
     h->vslots.ensure(std::max<int64_t>(vmax, 1));
     CollectArgs ca{};
@@ -1046,12 +1067,19 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     ca.out_slot = h->vslots.p;
     ca.out_n = counter;
     ca.cap = vmax;
+    ca.kand = kand;
+    ca.kor = kor;
     evict_collect_kernel<<<grid_all, 256, 0, st>>>(ca);
     ++h->launches;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h->n_h.p, counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->sel_h.p, counter, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const int64_t V = static_cast<int64_t>(*h->n_h.p);
+    const int64_t V = static_cast<int64_t>(h->sel_h.p[0]);
+    int nvary = 0;
+    for (int d = 0; d < 24; ++d) {
+        const int w = d >> 3, sh = 8 * (7 - (d & 7));
+        if (((h->sel_h.p[1 + w] >> sh) & 0xff) != ((h->sel_h.p[4 + w] >> sh) & 0xff)) ++nvary;
+    }
     h->vids.ensure(std::max<int64_t>(V, 1));
     if (V <= 2048) {
         evict_small_sort_kernel<<<1, 1024, 3 * V * sizeof(uint64_t), st>>>(h->vkeys.p, h->vslots.p, h->ids,
@@ -1059,23 +1087,31 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         ++h->launches;
         CK(cudaGetLastError());
     } else {
-        Key3* keys_in = reinterpret_cast<Key3*>(h->vkeys.p);
-        DevBuf<Key3> keys_out;
-        DevBuf<int32_t> slots_out;
-        keys_out.ensure(V);
-        slots_out.ensure(V);
+        h->vslots_out.ensure(V);
         size_t tmp = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, keys_out.p, h->vslots.p, slots_out.p, V,
-                                           KeyDecomposer{}, st));
-        h->cub_tmp.ensure(tmp);
-        CK(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, keys_in, keys_out.p, h->vslots.p, slots_out.p, V,
-                                           KeyDecomposer{}, st));
-        gather_ids_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(slots_out.p, h->ids, V, h->vids.p);
-        h->launches += 2;
+        if (nvary <= 16) {
+            // sort only the bytes that vary over the victim set
+            h->vpack.ensure(V);
+            h->vpack_out.ensure(V);
+            evict_pack_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(h->vkeys.p, V, kand, kor, h->vpack.p);
+            const int end_bit = std::max(8, 8 * nvary);
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->vpack.p, h->vpack_out.p, h->vslots.p,
+                                               h->vslots_out.p, V, PackDecomposer{}, 0, end_bit, st));
+            h->cub_tmp.ensure(tmp);
+            CK(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, h->vpack.p, h->vpack_out.p, h->vslots.p,
+                                               h->vslots_out.p, V, PackDecomposer{}, 0, end_bit, st));
+        } else {
+            Key3* keys_in = reinterpret_cast<Key3*>(h->vkeys.p);
+            h->vkey_out.ensure(V);
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, h->vkey_out.p, h->vslots.p, h->vslots_out.p,
+                                               V, KeyDecomposer{}, st));
+            h->cub_tmp.ensure(tmp);
+            CK(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, keys_in, h->vkey_out.p, h->vslots.p,
+                                               h->vslots_out.p, V, KeyDecomposer{}, st));
+        }
+        gather_ids_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(h->vslots_out.p, h->ids, V, h->vids.p);
+        h->launches += 3;
         CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(st));
-        keys_out.release();
-        slots_out.release();
     }
     out.resize(V);
     CK(cudaMemcpyAsync(out.data(), h->vids.p, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -1149,6 +1185,8 @@ int sine_destroy(sine_index_t* h) {
         h->o_ids.release(), h->o_sims.release(), h->o_cnt.release(), h->k1.release();
         h->vkeys.release(), h->vslots.release(), h->cand.release(), h->scratch_i32.release();
         h->vids.release(), h->cub_tmp.release(), h->hist.release(), h->st.release(), h->qbf.release();
+        h->vpack.release(), h->vpack_out.release(), h->vkey_out.release(), h->vslots_out.release();
+        h->exp_off.release(), h->sel_h.release();
         h->st_h.release(), h->n_h.release(), h->cnt_h.release();
         for (auto& e : h->ev) cudaEventDestroy(e);
         cudaStreamDestroy(h->stream);
@@ -1324,37 +1362,47 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
         CK(cudaSetDevice(h->device));
         *n = 0;
         if (h->nlive == 0) return;
-        const int64_t chunk = 1 << 16;
-        const int nb = static_cast<int>((h->nslots + chunk - 1) / chunk);
+        const int nb = static_cast<int>((h->nslots + kExpChunk - 1) / kExpChunk);
         h->scratch_i32.ensure(nb);
-        h->cnt_h.ensure(nb);
-        expire_count_kernel<<<nb, 256, 0, h->stream>>>(h->expiration, h->valid, h->nslots, now, chunk,
-                                                       h->scratch_i32.p);
-        ++h->launches;
+        h->exp_off.ensure(nb + 1);
+        h->cnt_h.ensure(2);
+        expire_count_kernel<<<nb, 256, 0, h->stream>>>(h->expiration, h->valid, h->nslots, now, h->scratch_i32.p);
+        expire_scan_kernel<<<1, 1024, 0, h->stream>>>(h->scratch_i32.p, nb, h->exp_off.p);
+        h->launches += 2;
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(h->cnt_h.p, h->scratch_i32.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
         int64_t total = 0;
-        for (int b = 0; b < nb; ++b) total += h->cnt_h.p[b];
+        CK(cudaMemcpyAsync(&total, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
         *n = total;
         if (total == 0) return;
+        if (total > cap) fail(SINE_EINVAL, "output buffer too small for expired ids");
         h->vids.ensure(total);
         h->vslots.ensure(total);
-        expire_write_kernel<<<nb, 256, 0, h->stream>>>(h->expiration, h->valid, h->ids, h->nslots, now, chunk,
-                                                       h->scratch_i32.p, h->vids.p, h->vslots.p);
+        expire_write_kernel<<<nb, 256, 0, h->stream>>>(h->expiration, h->valid, h->ids, h->nslots, now,
+                                                       h->exp_off.p, h->vids.p, h->vslots.p);
         ++h->launches;
         CK(cudaGetLastError());
-        std::vector<int64_t> ids(total);
-        std::vector<int32_t> slots(total);
-        CK(cudaMemcpyAsync(ids.data(), h->vids.p, total * 8, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaMemcpyAsync(slots.data(), h->vslots.p, total * 4, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        if (!h->ids_ascending) std::sort(ids.begin(), ids.end());
-        if (total > cap) fail(SINE_EINVAL, "output buffer too small for expired ids");
-        std::copy(ids.begin(), ids.end(), out);
+        CK(cudaMemcpyAsync(out, h->vids.p, total * 8, cudaMemcpyDeviceToHost, h->stream));
+        std::vector<int32_t> slots;
         if (remove) {
-            std::vector<int64_t> s64(slots.begin(), slots.end());
-            remove_slots(h, s64);
+            slots.resize(total);
+            CK(cudaMemcpyAsync(slots.data(), h->vslots.p, total * 4, cudaMemcpyDeviceToHost, h->stream));
+        }
+        CK(cudaStreamSynchronize(h->stream));
+        if (!h->ids_ascending) std::sort(out, out + total);
+        if (remove) {
+            // tombstone on the device straight from the slot list
+            set_bits32_kernel<<<grid_for(total, 256, h->num_sms), 256, 0, h->stream>>>(h->valid, h->vslots.p, total);
+            ++h->launches;
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(h->stream));
+            for (int32_t sl : slots) {
+                if (!h->ids_ascending) h->pos.erase(h->ids_h[sl]);
+                h->live_h[sl] = 0;
+            }
+            h->nlive -= total;
+            const int64_t dead = h->nslots - h->nlive;
+            if (dead > std::max<int64_t>(64, h->nlive / 4)) compact(h);
         }
     });
 }

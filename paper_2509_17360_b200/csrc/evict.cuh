@@ -96,26 +96,54 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
     uint64_t pre[3] = {a.st->prefix[0], a.st->prefix[1], a.st->prefix[2]};
     uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
     const int64_t n = a.cand ? a.ncand : a.c.nslots;
-    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
-        const int64_t s = a.cand ? a.cand[i] : i;
-        if (!a.cand && !valid_bit(a.c.valid, s)) continue;
-        uint64_t k[3];
-        if (a.first) {
-            k[0] = primary_key(a.c, s, a.policy, a.now);
-            a.k1[s] = k[0];
-        } else {
-            k[0] = a.k1[s];
-        }
-        k[1] = f64_key(a.c.created[s]);
-        k[2] = i64_key(a.c.ids[s]);
-        if (prefix_cmp(k, pre, nd) != 0) continue;
-        const uint32_t dg = key_digit(k, nd);
-        atomicAdd(&sw[dg], static_cast<unsigned long long>(a.c.size[s]));
-        atomicAdd(&sc[dg], 1ull);
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = 256ll * gridDim.x;
+    // warp-uniform trip count so the whole warp takes part in the aggregation
+    for (int64_t i0 = blockIdx.x * 256ll + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const int64_t i = i0 + lane;
+        bool act = false;
+        uint32_t dg = 0;
+        uint64_t sz = 0;
+        if (i < n) {
+            const int64_t s = a.cand ? a.cand[i] : i;
+            if (a.cand || valid_bit(a.c.valid, s)) {
+                uint64_t k[3];
+                if (a.first) {
+                    k[0] = primary_key(a.c, s, a.policy, a.now);
+                    a.k1[s] = k[0];
+                } else {
+                    k[0] = a.k1[s];
+                }
+                k[1] = f64_key(a.c.created[s]);
+                k[2] = i64_key(a.c.ids[s]);
+                if (prefix_cmp(k, pre, nd) == 0) {
+                    act = true;
+                    dg = key_digit(k, nd);
+                    sz = static_cast<uint64_t>(a.c.size[s]);
 #pragma unroll
-        for (int w = 0; w < 3; ++w) {
-            vand[w] &= k[w];
-            vor[w] |= k[w];
+                    for (int w = 0; w < 3; ++w) {
+                        vand[w] &= k[w];
+                        vor[w] |= k[w];
+                    }
+                }
+            }
+        }
+        // one shared-memory atomic per (warp, digit): a third of all SEs
+        // score exactly 0, so per-lane atomics would serialise on one bin
+        uint32_t rem = __ballot_sync(0xffffffffu, act);
+        while (rem) {
+            const int leader = __ffs(rem) - 1;
+            const uint32_t ldg = __shfl_sync(0xffffffffu, dg, leader);
+            const bool mine = act && dg == ldg;
+            const uint32_t grp = __ballot_sync(0xffffffffu, mine);
+            unsigned long long v = mine ? sz : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == leader) {
+                atomicAdd(&sw[ldg], v);
+                atomicAdd(&sc[ldg], static_cast<unsigned long long>(__popc(grp)));
+            }
+            rem &= ~grp;
         }
     }
 #pragma unroll
@@ -216,6 +244,8 @@ struct CollectArgs {
     int32_t* out_slot;    // [cap]
     unsigned long long* out_n;
     int64_t cap;
+    unsigned long long* kand;  // mode 0: AND / OR of the victims' keys (nullable)
+    unsigned long long* kor;
 };
 
 __global__ void __launch_bounds__(256) evict_collect_kernel(const CollectArgs a) {
@@ -223,22 +253,98 @@ __global__ void __launch_bounds__(256) evict_collect_kernel(const CollectArgs a)
     const bool all = a.st->done == 2;
     const uint64_t pre[3] = {a.st->prefix[0], a.st->prefix[1], a.st->prefix[2]};
     const int64_t n = a.cand ? a.ncand : a.c.nslots;
-    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
-        const int64_t s = a.cand ? a.cand[i] : i;
-        if (!a.cand && !valid_bit(a.c.valid, s)) continue;
-        uint64_t k[3] = {a.k1[s], f64_key(a.c.created[s]), i64_key(a.c.ids[s])};
-        const int cmp = all ? -1 : prefix_cmp(k, pre, nd);
-        const bool take = a.mode == 0 ? cmp <= 0 : cmp == 0;
+    const int lane = threadIdx.x & 31;
+    uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
+    for (int64_t i0 = blockIdx.x * 256ll + (threadIdx.x & ~31); i0 < n; i0 += 256ll * gridDim.x) {
+        const int64_t i = i0 + lane;
+        bool take = false;
+        int64_t s = 0;
+        uint64_t k[3] = {0, 0, 0};
+        if (i < n) {
+            s = a.cand ? a.cand[i] : i;
+            if (a.cand || valid_bit(a.c.valid, s)) {
+                k[0] = a.k1[s];
+                k[1] = f64_key(a.c.created[s]);
+                k[2] = i64_key(a.c.ids[s]);
+                const int cmp = all ? -1 : prefix_cmp(k, pre, nd);
+                take = a.mode == 0 ? cmp <= 0 : cmp == 0;
+            }
+        }
+        // one global atomic per warp for the output position
+        const uint32_t m = __ballot_sync(0xffffffffu, take);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.out_n, static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(0xffffffffu, base, 0);
         if (!take) continue;
-        const unsigned long long at = atomicAdd(a.out_n, 1ull);
+        const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
         if (static_cast<int64_t>(at) < a.cap) {
             a.out_slot[at] = static_cast<int32_t>(s);
             if (a.mode == 0) {
                 a.out_k[3 * at] = k[0];
                 a.out_k[3 * at + 1] = k[1];
                 a.out_k[3 * at + 2] = k[2];
+#pragma unroll
+                for (int w = 0; w < 3; ++w) {
+                    vand[w] &= k[w];
+                    vor[w] |= k[w];
+                }
             }
         }
+    }
+    if (a.mode == 0 && a.kand) {
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                vand[w] &= __shfl_xor_sync(0xffffffffu, vand[w], o);
+                vor[w] |= __shfl_xor_sync(0xffffffffu, vor[w], o);
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                atomicAnd(a.kand + w, static_cast<unsigned long long>(vand[w]));
+                atomicOr(a.kor + w, static_cast<unsigned long long>(vor[w]));
+            }
+        }
+    }
+}
+
+// Victim keys -> compact 128-bit keys made of only the bytes that vary over
+// the victim set (MSB-first, right-aligned).  Constant bytes cannot change
+// the order, so a radix sort over 8 * nvary bits orders the victims exactly
+// like the full 192-bit (primary, created_at, id) key.
+struct Pack2 {
+    uint64_t hi, lo;
+};
+
+__device__ __forceinline__ int varying_bytes(const unsigned long long* kand, const unsigned long long* kor, int* pos) {
+    int c = 0;
+    for (int d = 0; d < 24; ++d) {
+        const int w = d >> 3, sh = 8 * (7 - (d & 7));
+        if (((kand[w] >> sh) & 0xff) != ((kor[w] >> sh) & 0xff)) pos[c++] = d;
+    }
+    return c;
+}
+
+__global__ void __launch_bounds__(256) evict_pack_kernel(const uint64_t* keys, int64_t n,
+                                                         const unsigned long long* kand,
+                                                         const unsigned long long* kor, Pack2* out) {
+    __shared__ int pos[24];
+    __shared__ int nv;
+    if (threadIdx.x == 0) nv = varying_bytes(kand, kor, pos);
+    __syncthreads();
+    const int c = min(nv, 16);
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {
+        const uint64_t* k = keys + 3 * i;
+        uint64_t hi = 0, lo = 0;
+        for (int j = 0; j < c; ++j) {
+            const int d = pos[j], w = d >> 3, sh = 8 * (7 - (d & 7));
+            hi = (hi << 8) | (lo >> 56);
+            lo = (lo << 8) | ((k[w] >> sh) & 0xff);
+        }
+        out[i] = Pack2{hi, lo};
     }
 }
 
@@ -271,57 +377,90 @@ __global__ void __launch_bounds__(1024) evict_small_sort_kernel(const uint64_t* 
 
 // ------------------------------------------------------------------ expiry
 
-__global__ void __launch_bounds__(256) expire_count_kernel(const double* expiration, const uint32_t* valid,
-                                                           int64_t nslots, double now, int64_t chunk,
-                                                           int32_t* counts) {
-    __shared__ int32_t s;
-    if (threadIdx.x == 0) s = 0;
-    __syncthreads();
-    const int64_t b = blockIdx.x * chunk, e = min(b + chunk, nslots);
-    int32_t c = 0;
-    for (int64_t i = b + threadIdx.x; i < e; i += 256)
-        c += (valid_bit(valid, i) && __dsub_rn(expiration[i], now) <= 0.0) ? 1 : 0;
-    c = __reduce_add_sync(0xffffffffu, c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s, c);
-    __syncthreads();
-    if (threadIdx.x == 0) counts[blockIdx.x] = s;
+constexpr int kExpChunk = 4096;  // slots per block; 16 per thread
+
+__device__ __forceinline__ bool is_expired_slot(const double* expiration, const uint32_t* valid, int64_t i,
+                                                double now) {
+    return valid_bit(valid, i) && __dsub_rn(expiration[i], now) <= 0.0;
 }
 
-// Ordered write: block b writes its expired slots (ascending) at offsets[b].
+__global__ void __launch_bounds__(256) expire_count_kernel(const double* expiration, const uint32_t* valid,
+                                                           int64_t nslots, double now, int32_t* counts) {
+    __shared__ int32_t wsum[8];
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * kExpChunk;
+    const int64_t e = min(b + kExpChunk, nslots);
+    int32_t c = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) c += is_expired_slot(expiration, valid, i, now) ? 1 : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += wsum[w];
+        counts[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of the per-block counts in one block; offsets[nb] = total
+__global__ void __launch_bounds__(1024) expire_scan_kernel(const int32_t* counts, int nb, int64_t* offsets) {
+    __shared__ int64_t carry;
+    __shared__ int64_t wtot[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < nb; b0 += 1024) {
+        const int b = b0 + threadIdx.x;
+        const int64_t v = b < nb ? counts[b] : 0;
+        int64_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) wtot[warp] = inc;
+        __syncthreads();
+        int64_t off = carry;
+        for (int w = 0; w < warp; ++w) off += wtot[w];
+        if (b < nb) offsets[b] = off + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = off + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offsets[nb] = carry;
+}
+
+// ordered write: thread t of block b owns slots [b*4096 + 16t, +16)
 __global__ void __launch_bounds__(256) expire_write_kernel(const double* expiration, const uint32_t* valid,
                                                            const int64_t* ids, int64_t nslots, double now,
-                                                           int64_t chunk, const int32_t* counts,
-                                                           int64_t* out_ids, int32_t* out_slots) {
-    __shared__ int32_t warp_tot[8];
-    __shared__ int32_t base;
-    if (threadIdx.x == 0) {
-        int32_t o = 0;
-        for (int j = 0; j < static_cast<int>(blockIdx.x); ++j) o += counts[j];
-        base = o;
-    }
-    __syncthreads();
-    const int64_t b = blockIdx.x * chunk, e = min(b + chunk, nslots);
+                                                           const int64_t* offsets, int64_t* out_ids,
+                                                           int32_t* out_slots) {
+    __shared__ int32_t wtot[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t i0 = b; i0 < e; i0 += 256) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool f = i < e && valid_bit(valid, i) && __dsub_rn(expiration[i], now) <= 0.0;
-        const uint32_t m = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) warp_tot[warp] = __popc(m);
-        __syncthreads();
-        int32_t off = base;
-        for (int w = 0; w < warp; ++w) off += warp_tot[w];
-        off += __popc(m & ((1u << lane) - 1));
-        if (f) {
-            out_ids[off] = ids[i];
-            out_slots[off] = static_cast<int32_t>(i);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int32_t t = 0;
-            for (int w = 0; w < 8; ++w) t += warp_tot[w];
-            base += t;
-        }
-        __syncthreads();
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kExpChunk + threadIdx.x * 16;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int64_t i = s0 + j;
+        if (i < nslots && is_expired_slot(expiration, valid, i, now)) bits |= 1u << j;
+    }
+    const int32_t c = __popc(bits);
+    int32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    int64_t off = offsets[blockIdx.x];
+    for (int w = 0; w < warp; ++w) off += wtot[w];
+    off += inc - c;
+    while (bits) {
+        const int j = __ffs(bits) - 1;
+        bits &= bits - 1;
+        out_ids[off] = ids[s0 + j];
+        out_slots[off] = static_cast<int32_t>(s0 + j);
+        ++off;
     }
 }
 
