@@ -977,6 +977,26 @@ struct KeyDecomposer {
     }
 };
 
+// Ordered collection of the slots matching the selection state (mode 0:
+// key prefix <= T, mode 1: == T).  Returns the count (one host sync).
+int64_t collect_ordered(sine_index* h, const EvictCols& cols, int mode, uint64_t* out_k, int32_t* out_slot,
+                        unsigned long long* kand, unsigned long long* kor, int64_t cap) {
+    cudaStream_t st = h->stream;
+    const int nb = static_cast<int>((h->nslots + kColChunk - 1) / kColChunk);
+    h->scratch_i32.ensure(nb);
+    h->exp_off.ensure(nb + 1);
+    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st.p, mode, h->scratch_i32.p);
+    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (total > cap) fail(SINE_ECUDA, "collection exceeds its buffer");
+    collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st.p, mode, h->exp_off.p, out_k, out_slot, kand, kor);
+    h->launches += 3;
+    CK(cudaGetLastError());
+    return total;
+}
+
 void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, std::vector<int64_t>& out) {
     out.clear();
     if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata (SINE_STORE_META)");
@@ -1035,46 +1055,20 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         if (s.done) break;
         if (!cand && s.count <= cand_max) {
             h->cand.ensure(s.count);
-            CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
-            CollectArgs ca{};
-            ca.c = cols;
-            ca.k1 = h->k1.p;
-            ca.st = h->st.p;
-            ca.mode = 1;
-            ca.out_slot = h->cand.p;
-            ca.out_n = counter;
-            ca.cap = s.count;
-            evict_collect_kernel<<<grid_all, 256, 0, st>>>(ca);
-            ++h->launches;
-            CK(cudaGetLastError());
+            ncand = collect_ordered(h, cols, 1, nullptr, h->cand.p, nullptr, nullptr, s.count);
             cand = h->cand.p;
-            ncand = s.count;
         }
     }
     // collect the victims (key prefix <= T) with the AND / OR of their keys
     const int64_t vmax = h->nlive;
-    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(kand, 0xff, 3 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(kor, 0, 3 * sizeof(unsigned long long), st));
     h->vkeys.ensure(3 * std::max<int64_t>(vmax, 1));
     h->vslots.ensure(std::max<int64_t>(vmax, 1));
-    CollectArgs ca{};
-    ca.c = cols;
-    ca.k1 = h->k1.p;
-    ca.st = h->st.p;
-    ca.mode = 0;
-    ca.out_k = h->vkeys.p;
-    ca.out_slot = h->vslots.p;
-    ca.out_n = counter;
-    ca.cap = vmax;
-    ca.kand = kand;
-    ca.kor = kor;
-    evict_collect_kernel<<<grid_all, 256, 0, st>>>(ca);
-    ++h->launches;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h->sel_h.p, counter, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    const int64_t V = collect_ordered(h, cols, 0, h->vkeys.p, h->vslots.p, kand, kor, vmax);
+    (void)counter;
+    CK(cudaMemcpyAsync(h->sel_h.p + 1, kand, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const int64_t V = static_cast<int64_t>(h->sel_h.p[0]);
     int nvary = 0;
     for (int d = 0; d < 24; ++d) {
         const int w = d >> 3, sh = 8 * (7 - (d & 7));

@@ -311,6 +311,128 @@ __global__ void __launch_bounds__(256) evict_collect_kernel(const CollectArgs a)
     }
 }
 
+// ---- ordered (atomic-free) collection: count per 4096-slot chunk, scan,
+// write.  Same predicate as evict_collect_kernel; output in slot order.
+
+struct CollectPred {
+    EvictCols c;
+    const uint64_t* k1;
+    int nd;
+    int all;
+    int mode;  // 0: prefix <= T (victims), 1: prefix == T (candidates)
+    uint64_t pre[3];
+
+    __device__ __forceinline__ bool operator()(int64_t s, uint64_t* k) const {
+        if (!valid_bit(c.valid, s)) return false;
+        k[0] = k1[s];
+        k[1] = f64_key(c.created[s]);
+        k[2] = i64_key(c.ids[s]);
+        const int cmp = all ? -1 : prefix_cmp(k, pre, nd);
+        return mode == 0 ? cmp <= 0 : cmp == 0;
+    }
+};
+
+__device__ __forceinline__ CollectPred make_pred(const EvictCols& c, const uint64_t* k1, const SelectState* st,
+                                                 int mode) {
+    CollectPred p;
+    p.c = c;
+    p.k1 = k1;
+    p.nd = st->ndigits;
+    p.all = st->done == 2;
+    p.mode = mode;
+    p.pre[0] = st->prefix[0];
+    p.pre[1] = st->prefix[1];
+    p.pre[2] = st->prefix[2];
+    return p;
+}
+
+constexpr int kColChunk = 4096;  // slots per block; 16 per thread
+
+__global__ void __launch_bounds__(256) collect_count_kernel(EvictCols c, const uint64_t* k1, const SelectState* st,
+                                                            int mode, int32_t* counts) {
+    __shared__ int32_t wsum[8];
+    const CollectPred pred = make_pred(c, k1, st, mode);
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * kColChunk;
+    const int64_t e = min(b + kColChunk, c.nslots);
+    int32_t cnt = 0;
+    uint64_t k[3];
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) cnt += pred(i, k) ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += wsum[w];
+        counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const uint64_t* k1, const SelectState* st,
+                                                            int mode, const int64_t* offsets, uint64_t* out_k,
+                                                            int32_t* out_slot, unsigned long long* kand,
+                                                            unsigned long long* kor) {
+    __shared__ int32_t wtot[8];
+    const CollectPred pred = make_pred(c, k1, st, mode);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kColChunk + threadIdx.x * 16;
+    uint32_t bits = 0;
+    uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
+    uint64_t k[3];
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+        const int64_t i = s0 + j;
+        if (i < c.nslots && pred(i, k)) {
+            bits |= 1u << j;
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                vand[w] &= k[w];
+                vor[w] |= k[w];
+            }
+        }
+    }
+    const int32_t cnt = __popc(bits);
+    int32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    int64_t off = offsets[blockIdx.x];
+    for (int w = 0; w < warp; ++w) off += wtot[w];
+    off += inc - cnt;
+    while (bits) {
+        const int j = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int64_t i = s0 + j;
+        out_slot[off] = static_cast<int32_t>(i);
+        if (out_k) {
+            out_k[3 * off] = k1[i];
+            out_k[3 * off + 1] = f64_key(c.created[i]);
+            out_k[3 * off + 2] = i64_key(c.ids[i]);
+        }
+        ++off;
+    }
+    if (kand) {
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                vand[w] &= __shfl_xor_sync(0xffffffffu, vand[w], o);
+                vor[w] |= __shfl_xor_sync(0xffffffffu, vor[w], o);
+            }
+        }
+        if (lane == 0 && vor[0] | vor[1] | vor[2]) {
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                atomicAnd(kand + w, static_cast<unsigned long long>(vand[w]));
+                atomicOr(kor + w, static_cast<unsigned long long>(vor[w]));
+            }
+        }
+    }
+}
+
 // Victim keys -> compact 128-bit keys made of only the bytes that vary over
 // the victim set (MSB-first, right-aligned).  Constant bytes cannot change
 // the order, so a radix sort over 8 * nvary bits orders the victims exactly
