@@ -1069,8 +1069,11 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     (void)counter;
     CK(cudaMemcpyAsync(h->sel_h.p + 1, kand, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    // bytes of the composite key that vary over the victims; with slot order
+    // == id order the id bytes are left to the (stable) sort's input order
+    const bool skip_id = h->ids_ascending;
     int nvary = 0;
-    for (int d = 0; d < 24; ++d) {
+    for (int d = 0; d < (skip_id ? 16 : 24); ++d) {
         const int w = d >> 3, sh = 8 * (7 - (d & 7));
         if (((h->sel_h.p[1 + w] >> sh) & 0xff) != ((h->sel_h.p[4 + w] >> sh) & 0xff)) ++nvary;
     }
@@ -1087,7 +1090,8 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
             // sort only the bytes that vary over the victim set
             h->vpack.ensure(V);
             h->vpack_out.ensure(V);
-            evict_pack_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(h->vkeys.p, V, kand, kor, h->vpack.p);
+            evict_pack_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(h->vkeys.p, V, kand, kor,
+                                                                            skip_id ? 1 : 0, h->vpack.p);
             const int end_bit = std::max(8, 8 * nvary);
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->vpack.p, h->vpack_out.p, h->vslots.p,
                                                h->vslots_out.p, V, PackDecomposer{}, 0, end_bit, st));

@@ -128,9 +128,19 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
                 }
             }
         }
-        // one shared-memory atomic per (warp, digit): a third of all SEs
-        // score exactly 0, so per-lane atomics would serialise on one bin
+        // one shared-memory atomic per (warp, digit) when few digits are
+        // present (a third of all SEs score exactly 0: per-lane atomics would
+        // serialise on one bin); spread digits take plain per-lane atomics
         uint32_t rem = __ballot_sync(0xffffffffu, act);
+        const uint32_t peers = __match_any_sync(0xffffffffu, act ? dg : 0xffffffffu);
+        const bool group_leader = act && (__ffs(peers) - 1) == lane;
+        if (__popc(__ballot_sync(0xffffffffu, group_leader)) > 4) {
+            if (act) {
+                atomicAdd(&sw[dg], static_cast<unsigned long long>(sz));
+                atomicAdd(&sc[dg], 1ull);
+            }
+            rem = 0;
+        }
         while (rem) {
             const int leader = __ffs(rem) - 1;
             const uint32_t ldg = __shfl_sync(0xffffffffu, dg, leader);
@@ -450,12 +460,18 @@ __device__ __forceinline__ int varying_bytes(const unsigned long long* kand, con
     return c;
 }
 
+// skip_id: the victims arrive in slot order and slots are in id order, so a
+// stable sort over the (primary, created_at) bytes already yields id order.
 __global__ void __launch_bounds__(256) evict_pack_kernel(const uint64_t* keys, int64_t n,
                                                          const unsigned long long* kand,
-                                                         const unsigned long long* kor, Pack2* out) {
+                                                         const unsigned long long* kor, int skip_id, Pack2* out) {
     __shared__ int pos[24];
     __shared__ int nv;
-    if (threadIdx.x == 0) nv = varying_bytes(kand, kor, pos);
+    if (threadIdx.x == 0) {
+        nv = varying_bytes(kand, kor, pos);
+        if (skip_id)
+            while (nv > 0 && pos[nv - 1] >= 16) --nv;
+    }
     __syncthreads();
     const int c = min(nv, 16);
     for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * gridDim.x) {

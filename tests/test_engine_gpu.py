@@ -199,3 +199,47 @@ def test_lookup_batch_matches_sequential_when_no_purge(pkg):
         assert (s.kind, s.element_id, s.similarity, s.candidates_considered, s.judged) == \
                (t.kind, t.element_id, t.similarity, t.candidates_considered, t.judged)
     assert a.stats() == b.stats()
+
+
+@pytest.mark.parametrize("shuffled", [False, True])
+def test_large_purge_and_select_match_oracle(pkg, shuffled):
+    """1M SEs, config-D metadata: the device purge (ascending ids) followed
+    by the LCFU prefix at 0.9 x live usage equals the oracle's
+    evict_until_fits -- ascending ids take the packed (primary, created)
+    sort, shuffled ids the full 192-bit key sort."""
+    import ctypes
+
+    import torch
+
+    import bench
+    from paper_2509_17360_b200 import _native as N
+
+    n = 1_000_000
+    meta = bench.evict_metadata(n, seed=9)
+    now = 1.0e4
+    rng = np.random.default_rng(1)
+    ids = rng.permutation(4 * n)[:n] + 1 if shuffled else np.arange(1, n + 1)
+    cols = {"log_freq": bench._exact_log((meta["freq"] + 1).astype(np.float64)),
+            "log_cost": bench._exact_log(meta["cost"] * 1000.0 + 1),
+            "log_lat": bench._exact_log(meta["lat"] + 1),
+            "log_stat": bench._exact_log((meta["staticity"] + 1).astype(float)),
+            "frequency": meta["freq"], "size_tokens": meta["size"], "created_at": meta["created"],
+            "expiration_time": meta["expiration"], "last_access": meta["created"]}
+    rows = torch.zeros((n, 4), dtype=torch.float64, device="cuda")
+    rows[:, 0] = 1.0
+    idx = pkg.GpuCosineIndex(4, metadata=True, capacity=n)
+    idx.insert_device(ids, rows.data_ptr(), meta=cols)
+    live = (meta["expiration"] - now) > 0.0
+    live_usage = int(meta["size"][live].sum())
+    cap = int(0.9 * live_usage)
+    out = np.empty(n, dtype=np.int64)
+    cnt = ctypes.c_int64()
+    p = N.ptr(out, ctypes.c_int64)
+    N.check(idx._lib.sine_expired(idx.handle, now, 1, p, n, ctypes.byref(cnt)))
+    expired = out[:cnt.value].copy()
+    N.check(idx._lib.sine_select_victims(idx.handle, 0, now, live_usage - cap, p, n, ctypes.byref(cnt)))
+    victims = out[:cnt.value].copy()
+    want = O.evict_until_fits_np(ids, meta["freq"], meta["cost"], meta["lat"], meta["staticity"], meta["size"],
+                                 meta["created"], meta["expiration"], now, cap)
+    assert np.array_equal(np.concatenate([expired, victims]), want)
+    assert len(idx) == n - expired.shape[0]
