@@ -174,6 +174,7 @@ struct sine_index {
     DevBuf<Key3> vkey_out;
     DevBuf<int32_t> vslots_out;
     DevBuf<int64_t> exp_off;
+    DevBuf<uint32_t> gbound;        // chip-wide admission bounds of the running launch
     HostBuf<unsigned long long> sel_h;  // counter + kand + kor
     DevBuf<SelectState> st;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
@@ -664,6 +665,9 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.stages = S;
         p.tf32 = tf32 ? 1 : 0;
         p.slot_ids = h->ids_ascending ? 1 : 0;
+        h->gbound.ensure(static_cast<size_t>(kMaxCS) * NQmax);
+        CK(cudaMemsetAsync(h->gbound.p, 0, static_cast<size_t>(CS) * NQ * sizeof(uint32_t), st));
+        p.gbound = h->gbound.p;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;
@@ -757,6 +761,9 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         p.thr0 = thr0;
         p.stages = S;
         p.tf32 = tf32 ? 1 : 0;
+        h->gbound.ensure(512);
+        CK(cudaMemsetAsync(h->gbound.p, 0, kUmmaM * sizeof(uint32_t), st));
+        p.gbound = h->gbound.p;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;
@@ -843,6 +850,9 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         p.row_groups = c.G;
         p.unroll = c.U;
         p.slot_ids = h->ids_ascending ? 1 : 0;
+        h->gbound.ensure(512);
+        CK(cudaMemsetAsync(h->gbound.p, 0, 16 * sizeof(uint32_t), st));
+        p.gbound = h->gbound.p;
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
@@ -1184,7 +1194,7 @@ int sine_destroy(sine_index_t* h) {
         h->vkeys.release(), h->vslots.release(), h->cand.release(), h->scratch_i32.release();
         h->vids.release(), h->cub_tmp.release(), h->hist.release(), h->st.release(), h->qbf.release();
         h->vpack.release(), h->vpack_out.release(), h->vkey_out.release(), h->vslots_out.release();
-        h->exp_off.release(), h->sel_h.release();
+        h->exp_off.release(), h->sel_h.release(), h->gbound.release();
         h->st_h.release(), h->n_h.release(), h->cnt_h.release();
         for (auto& e : h->ev) cudaEventDestroy(e);
         cudaStreamDestroy(h->stream);

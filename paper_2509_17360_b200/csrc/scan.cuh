@@ -43,6 +43,7 @@ struct ScanParams {
     int row_groups;         // G
     int unroll;             // RPW: rows per warp per stage (multiple of U; R = G * RPW)
     int slot_ids;           // slot order == id order
+    uint32_t* gbound;       // [nq] chip-wide admission bound (f32 keys, zeroed per launch)
     uint32_t* out_key;      // [grid][nq][kp] f32_key(score)
     int32_t* out_slot;      // [grid][nq][kp]
     int32_t* out_n;         // [grid][nq]
@@ -339,6 +340,11 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
                 }
             }
             }
+            // chip-wide admission bound (any CTA's k'-th best <= the global one)
+            if (tid < nq) {
+                const uint32_t g = *reinterpret_cast<volatile uint32_t*>(p.gbound + tid);
+                if (g > thr[tid]) thr[tid] = g;
+            }
             named_bar_sync(1, nthreads);
             if (tid == 0) mbar_arrive(empty_bar + s);  // stage consumed
 
@@ -385,7 +391,10 @@ __global__ void __launch_bounds__(ScanWarps<NQ>::kThreads, 1) scan_kernel(const 
                                               merge_scratch + warp * (kp + R), p.ids, p.slot_ids != 0, lane);
                 if (lane == 0) {
                     cnt[jq] = n;
-                    if (n == kp) thr[jq] = max(thr0, lk[kp - 1]);
+                    if (n == kp) {
+                        thr[jq] = max(thr[jq], lk[kp - 1]);
+                        atomicMax(p.gbound + jq, lk[kp - 1]);
+                    }
                 }
                 __syncwarp();
             }

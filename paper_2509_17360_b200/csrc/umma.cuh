@@ -41,6 +41,7 @@ struct UmmaParams {
     float thr0;
     int stages;
     int tf32;                // 1: kind::tf32 over fp32 rows, 0: kind::f16 over bf16 rows
+    uint32_t* gbound;        // [nq] chip-wide admission bound (f32 keys, zeroed per launch)
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;       // [grid][nq][kp]
@@ -165,7 +166,7 @@ struct ThreadList {
                 }
         }
         worst = pos;
-        thr = max(thr0, mk);
+        thr = max(thr, max(thr0, mk));
     }
 
     __device__ __forceinline__ void offer(uint32_t kk, int32_t sl, const int64_t* ids, uint32_t thr0) {
@@ -305,6 +306,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 const int64_t r = row0 + 32 * w;
                 vw[w] = r < p.nslots ? __ldg(p.valid + (r >> 5)) : 0u;
             }
+            if (live_q) {  // chip-wide bound: any CTA's k'-th best <= the global k'-th best
+                const uint32_t g = *reinterpret_cast<volatile uint32_t*>(p.gbound + qi);
+                if (g > list.thr) list.thr = g;
+            }
             mbar_wait(tfull + acc, (i >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
@@ -321,7 +326,14 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     const int64_t slot = row0 + c * 32 + j;
                     if (((vbits >> j) & 1u) && slot < p.nslots && sc == sc) {
                         const uint32_t key = f32_key(sc);
-                        if (key >= list.thr) list.offer(key, static_cast<int32_t>(slot), p.ids, thr0);
+                        if (key >= list.thr) {
+                            const uint32_t before = list.n == list.kp ? list.k(list.worst) : 0u;
+                            list.offer(key, static_cast<int32_t>(slot), p.ids, thr0);
+                            if (list.n == list.kp) {
+                                const uint32_t wk = list.k(list.worst);
+                                if (wk != before) atomicMax(p.gbound + qi, wk);
+                            }
+                        }
                     }
                 }
             }
@@ -391,6 +403,7 @@ struct ResParams {
     int stages;
     int tf32;
     int slot_ids;     // slot order == id order (ties resolved without loads)
+    uint32_t* gbound;  // [nq] chip-wide admission bound per query (f32 keys, zeroed per launch)
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -631,12 +644,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     } else {
         // ---------------- epilogue: thread = row ----------------
         const int tid = threadIdx.x;  // 0..127 == TMEM lane == row within tile
+        const bool slot_ids = p.slot_ids != 0;
         int i = 0;
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
             const int64_t slot = static_cast<int64_t>(t) * kUmmaN + tid;
             const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
             const bool live = ((vw >> (slot & 31)) & 1u) != 0;
+            // refresh the admission thresholds with the chip-wide bound: the
+            // k'-th best of any CTA's rows is <= the global k'-th best
+            if (tid < nq_local) {
+                const uint32_t g = *reinterpret_cast<volatile uint32_t*>(p.gbound + crank * NQ + tid);
+                if (g) thr[tid] = fmaxf(thr[tid], key_f32(g));
+            }
+            named_bar_sync(2, 128);
             mbar_wait(tfull + acc, (i >> 1) & 1);
             tc_fence_after();
             float sc[NQ];
@@ -679,10 +700,14 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                         int32_t* ls = lslot + j * kp;
                         const int n = warp_rank_merge(lk, ls, static_cast<int>(cnt[j]), kp, pend + j * kResQPer, np,
                                                       merge_scratch + warp * (kMaxKp + kResQPer), p.ids,
-                                                      p.slot_ids != 0, lane);
+                                                      slot_ids, lane);
                         if (lane == 0) {
                             cnt[j] = n;
-                            if (n == kp) thr[j] = fmaxf(p.thr0, key_f32(lk[kp - 1]));
+                            if (n == kp) {
+                                const uint32_t wk = lk[kp - 1];
+                                thr[j] = fmaxf(thr[j], key_f32(wk));
+                                atomicMax(p.gbound + crank * NQ + j, wk);
+                            }
                         }
                     }
                     __syncwarp();
