@@ -668,20 +668,34 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         h->gbound.ensure(static_cast<size_t>(kMaxCS) * NQmax);
         CK(cudaMemsetAsync(h->gbound.p, 0, static_cast<size_t>(CS) * NQ * sizeof(uint32_t), st));
         p.gbound = h->gbound.p;
+        p.tile_stride = 1;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
         const int max_clusters = std::max(1, std::min(h->num_sms / CS, ntiles));
+        auto launch = [&](const ResParams& pp, int maxc) {
+            if (NQ == 16) return launch_res_cs<16>(CS, qmap, rmap, pp, maxc, L.total, st);
+            if (NQ == 32) return launch_res_cs<32>(CS, qmap, rmap, pp, maxc, L.total, st);
+            return launch_res_cs<64>(CS, qmap, rmap, pp, maxc, L.total, st);
+        };
+        // Low admission floors admit most rows until each CTA's list warms up;
+        // a sample pass (one strided tile per cluster) seeds the chip-wide
+        // bound with the kp-th best sampled key -- a valid lower bound on the
+        // global kp-th best -- so the main pass admits almost nothing extra.
+        const int sample_tiles = std::min(max_clusters, ntiles / 16);
+        if (thr0 < 0.5f && sample_tiles >= 16) {
+            ResParams sp = p;
+            sp.ntiles = sample_tiles;
+            sp.tile_stride = ntiles / sample_tiles;
+            const int scl = launch(sp, sample_tiles);
+            sample_bound_kernel<<<nq, 256, 0, st>>>(h->lkey.p, h->ln.p, scl, nq, kp, h->gbound.p);
+            h->launches += 2;
+            CK(cudaGetLastError());
+        }
         const size_t tk = tbegin(h, 2, st);
-        int ncl;
-        if (NQ == 16)
-            ncl = launch_res_cs<16>(CS, qmap, rmap, p, max_clusters, L.total, st);
-        else if (NQ == 32)
-            ncl = launch_res_cs<32>(CS, qmap, rmap, p, max_clusters, L.total, st);
-        else
-            ncl = launch_res_cs<64>(CS, qmap, rmap, p, max_clusters, L.total, st);
+        const int ncl = launch(p, max_clusters);
         tend(h, tk, st);
         h->launches += 2;
         CK(cudaGetLastError());
@@ -908,6 +922,7 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.err = h->cur_err;
     m.cert = h->cert.p ? h->cert.p + (cert_off) : nullptr;
     m.debug = getenv("SINE_DEBUG_CERT") ? 1 : 0;
+    m.gbound = h->gbound.p;  // every stage-1 kernel publishes its admission bounds here
     m.out_ids = ids_dev;
     m.out_sims = sims_dev;
     m.out_counts = counts_dev;

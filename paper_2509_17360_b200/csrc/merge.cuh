@@ -30,6 +30,7 @@ struct MergeParams {
     float thr0;              // admission floor the scan used
     double err;              // bound on |filter score - exact similarity|
     uint8_t* cert;           // [nq] 1 = provably the exact top-k (nullable)
+    const uint32_t* gbound;  // [nq] chip-wide admission bound the scan used (nullable)
     int debug;
     int64_t* out_ids;        // [nq][k]
     double* out_sims;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             // the threshold when fewer than k passed)
             double bound = static_cast<double>(p.thr0);
             if (bound_key) bound = fmax(bound, static_cast<double>(key_f32(bound_key)));
+            if (p.gbound && p.gbound[qi]) bound = fmax(bound, static_cast<double>(key_f32(p.gbound[qi])));
             const double need = outn == p.k ? p.out_sims[static_cast<size_t>(qi) * p.k + p.k - 1] : p.min_sim;
             p.cert[qi] = (!p.rerank || bound + p.err < need) ? 1 : 0;
             if (p.debug)

@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "merge.cuh"
 
 namespace sine {
 
@@ -403,7 +404,8 @@ struct ResParams {
     int stages;
     int tf32;
     int slot_ids;     // slot order == id order (ties resolved without loads)
-    uint32_t* gbound;  // [nq] chip-wide admission bound per query (f32 keys, zeroed per launch)
+    uint32_t* gbound;  // [nq] chip-wide admission bound per query (f32 keys)
+    int tile_stride;   // 1 = every tile; >1 = sample pass over every tile_stride-th tile
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -589,11 +591,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     mbar_wait(empty + s, ph ^ 1);
                     mbar_arrive_expect_tx(full + s, kUmmaN * kUmmaKB);
                     uint8_t* dst = sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB + crank * kSliceRows * kUmmaKB;
+                    const int tt = t * p.tile_stride;
                     if constexpr (CS > 1)
-                        tma_load_2d_mc(dst, &rmap, full + s, kb * kb_elems, t * kUmmaN + crank * kSliceRows, kMask,
+                        tma_load_2d_mc(dst, &rmap, full + s, kb * kb_elems, tt * kUmmaN + crank * kSliceRows, kMask,
                                        pol_rows);
                     else
-                        tma_load_2d(dst, &rmap, full + s, kb * kb_elems, t * kUmmaN, pol_rows);
+                        tma_load_2d(dst, &rmap, full + s, kb * kb_elems, tt * kUmmaN, pol_rows);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -648,7 +651,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         int i = 0;
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
-            const int64_t slot = static_cast<int64_t>(t) * kUmmaN + tid;
+            const int64_t slot = static_cast<int64_t>(t) * p.tile_stride * kUmmaN + tid;
             const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
             const bool live = ((vw >> (slot & 31)) & 1u) != 0;
             // refresh the admission thresholds with the chip-wide bound: the
@@ -743,6 +746,38 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
+}
+
+// Seed of the chip-wide admission bound from a sample pass: per query, the
+// kp-th best key over the sampled per-CTA lists (0 if fewer than kp).
+__global__ void __launch_bounds__(256) sample_bound_kernel(const uint32_t* in_key, const int32_t* in_n, int ncta,
+                                                           int nq, int kp, uint32_t* gbound) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t scratch[16];
+    const int qi = blockIdx.x;
+    const int nflat = ncta * kp;
+    uint32_t before, equal;
+    uint32_t tot = 0;
+    for (int c = threadIdx.x; c < ncta; c += 256) tot += in_n[c * nq + qi];
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = tot;
+    __syncthreads();
+    uint32_t total = 0;
+    for (int w = 0; w < 8; ++w) total += scratch[w];
+    __syncthreads();
+    if (total < static_cast<uint32_t>(kp)) {
+        if (threadIdx.x == 0) gbound[qi] = 0;
+        return;
+    }
+    const uint32_t kstar = block_select<uint32_t>(
+        [&](int f, uint32_t& key) {
+            const int c = f / kp, e = f - c * kp;
+            if (e >= in_n[c * nq + qi]) return false;
+            key = in_key[(static_cast<size_t>(c) * nq + qi) * kp + e];
+            return true;
+        },
+        nflat, static_cast<uint32_t>(kp), true, 32, hist, scratch, &before, &equal);
+    if (threadIdx.x == 0) gbound[qi] = kstar;
 }
 
 // q64 [nq][dim] -> zero-padded [Nq][stride] bf16 or fp32 (TMA source).
