@@ -685,7 +685,7 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         // bound with the kp-th best sampled key -- a valid lower bound on the
         // global kp-th best -- so the main pass admits almost nothing extra.
         const int sample_tiles = std::min(max_clusters, ntiles / 16);
-        if (thr0 < 0.5f && sample_tiles >= 16) {
+        if (thr0 < 0.5f && sample_tiles >= 16 && nq >= 8) {
             ResParams sp = p;
             sp.ntiles = sample_tiles;
             sp.tile_stride = ntiles / sample_tiles;
@@ -778,11 +778,22 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         h->gbound.ensure(512);
         CK(cudaMemsetAsync(h->gbound.p, 0, kUmmaM * sizeof(uint32_t), st));
         p.gbound = h->gbound.p;
+        p.tile_stride = 1;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
+        const int sample_tiles = std::min(grid, ntiles / 16);
+        if (thr0 < 0.5f && sample_tiles >= 16 && nq >= 8) {  // seed the admission bound (see umma_res_query)
+            UmmaParams sp = p;
+            sp.ntiles = sample_tiles;
+            sp.tile_stride = ntiles / sample_tiles;
+            umma_scan_kernel<<<sample_tiles, kUmmaThreads, L.total, st>>>(qmap, rmap, sp);
+            sample_bound_kernel<<<nq, 256, 0, st>>>(h->lkey.p, h->ln.p, sample_tiles, nq, kp, h->gbound.p);
+            h->launches += 2;
+            CK(cudaGetLastError());
+        }
         const size_t tk = tbegin(h, 2, st);
         umma_scan_kernel<<<grid, kUmmaThreads, L.total, st>>>(qmap, rmap, p);
         tend(h, tk, st);

@@ -43,6 +43,7 @@ struct UmmaParams {
     int stages;
     int tf32;                // 1: kind::tf32 over fp32 rows, 0: kind::f16 over bf16 rows
     uint32_t* gbound;        // [nq] chip-wide admission bound (f32 keys, zeroed per launch)
+    int tile_stride;         // 1 = every tile; >1 = sample pass
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;       // [grid][nq][kp]
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     tma_load_2d(sa + static_cast<size_t>(s) * kUmmaM * kUmmaKB, &qmap, full + s, kb * kb_elems, 0,
                                 pol_q);
                     tma_load_2d(sb + static_cast<size_t>(s) * kUmmaN * kUmmaKB, &rmap, full + s, kb * kb_elems,
-                                t * kUmmaN, pol_rows);
+                                t * p.tile_stride * kUmmaN, pol_rows);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         int i = 0;
         for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
             const int acc = i & 1;
-            const int64_t row0 = static_cast<int64_t>(t) * kUmmaN;
+            const int64_t row0 = static_cast<int64_t>(t) * p.tile_stride * kUmmaN;
             // validity words of this tile (4 x 32 rows), fetched before the wait
             uint32_t vw[4];
 #pragma unroll
@@ -439,6 +440,7 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     off = (off + 15) / 16 * 16;
     off += static_cast<size_t>(Nq) * kResQPer * 8;
     off += static_cast<size_t>(4) * (kMaxKp + kResQPer) * 8;  // per-warp merge scratch
+    off += static_cast<size_t>(4) * Nq * 4;                    // per-warp ballots
     L.total = off + 1024;
     return L;
 }
@@ -531,6 +533,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     uint32_t* pcnt = reinterpret_cast<uint32_t*>(smem + L.pend_off);
     uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
     uint2* merge_scratch = pend + NQ * kResQPer;
+    uint32_t* wball = reinterpret_cast<uint32_t*>(merge_scratch + 4 * (kMaxKp + kResQPer));  // [4][NQ]
     constexpr uint32_t kTmemCols = NQ <= 16 ? 32 : (2 * NQ <= 64 ? 64 : 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -684,16 +687,31 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     if (j < nq_local && sc[j] >= thr[j]) mask |= 1ull << j;
             }
             while (bar_red_or(1, 128, mask != 0)) {
-                // queue what fits, then insert warp-per-query
-                uint64_t m = mask;
-                while (m) {
-                    const int j = __ffsll(m) - 1;
-                    m &= m - 1;
-                    const uint32_t pos = atomicAdd(pcnt + j, 1u);
-                    if (pos < kResQPer) {
-                        pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
-                        mask &= ~(1ull << j);
+                // queue what fits (row order), positions from ballots -- no
+                // atomics: in a warm-up tile every row passes for every query
+                for (int j = 0; j < NQ; ++j) {
+                    const uint32_t b = __ballot_sync(0xffffffffu, (mask >> j) & 1ull);
+                    if (lane == 0) wball[warp * NQ + j] = b;
+                }
+                named_bar_sync(2, 128);
+                if (mask) {
+                    const uint32_t lt = (1u << lane) - 1u;
+                    uint64_t m = mask;
+                    while (m) {
+                        const int j = __ffsll(m) - 1;
+                        m &= m - 1;
+                        uint32_t pos = __popc(wball[warp * NQ + j] & lt);
+                        for (int w = 0; w < warp; ++w) pos += __popc(wball[w * NQ + j]);
+                        if (pos < kResQPer) {
+                            pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
+                            mask &= ~(1ull << j);
+                        }
                     }
+                }
+                if (tid < NQ) {
+                    uint32_t c = 0;
+                    for (int w = 0; w < 4; ++w) c += __popc(wball[w * NQ + tid]);
+                    pcnt[tid] = c;
                 }
                 named_bar_sync(2, 128);
                 for (int j = warp; j < nq_local; j += 4) {
