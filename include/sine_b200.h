@@ -59,6 +59,7 @@ extern "C" {
 #define SINE_SCAN_UMMA_V1  0x400u /* force the query-streaming tcgen05 kernel */
 #define SINE_SCAN_CLUSTER  0x1000u /* tcgen05: share row tiles across up to 8 CTAs
                                       (TMA multicast), one HBM pass per 8 query groups */
+#define SINE_SCAN_PAIR     0x2000u /* tcgen05 cta_group::2: prefer the CTA-pair kernel */
 #define SINE_CERTIFY       0x800u /* sine_query_device: check the per-query exactness
                                      certificate and re-run failures on the fp32
                                      CUDA-core scan (synchronises the stream);

@@ -20,8 +20,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 SINE_OK, SINE_EINVAL, SINE_ECUDA, SINE_ENCCL, SINE_ENOMEM, SINE_ENOTFOUND, SINE_EDUP, SINE_ENORM = range(8)
 
 STORE_F32, STORE_BF16, STORE_META = 0x1, 0x2, 0x4
-SCAN_F32, SCAN_BF16, RERANK_F64, NO_NORM_CHECK, SCAN_CUDA_CORE, SCAN_UMMA_V1, CERTIFY, SCAN_CLUSTER = \
-    0x0, 0x1, 0x10, 0x100, 0x200, 0x400, 0x800, 0x1000
+SCAN_F32, SCAN_BF16, RERANK_F64, NO_NORM_CHECK, SCAN_CUDA_CORE, SCAN_UMMA_V1, CERTIFY, SCAN_CLUSTER, SCAN_PAIR = \
+    0x0, 0x1, 0x10, 0x100, 0x200, 0x400, 0x800, 0x1000, 0x2000
 POLICIES = {"lcfu": 0, "lru": 1, "lfu": 2}
 
 _i64p = ctypes.POINTER(ctypes.c_int64)

@@ -705,6 +705,78 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
     }
 }
 
+// CTA-pair tensor-core scan (cta_group::2): groups of 2*NQH queries, each
+// CTA of a pair holding NQH of them; one HBM pass per group.
+void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                     bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                     cudaStream_t st) {
+    constexpr int NQH = 32, NQ = 2 * NQH;
+    const bool tf32 = !bf16;
+    const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
+    const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
+    const int kblocks = static_cast<int>(row_bytes / kUmmaKB);
+    const int ntiles = static_cast<int>((h->nslots + 2 * kUmmaN - 1) / (2 * kUmmaN));
+    const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp, NQH);
+    if (L0.total + 2 * kUmmaN * kUmmaKB > 227 * 1024) fail(SINE_EINVAL, "pair plan does not fit shared memory");
+    const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
+    const ResSmem L = res_smem_layout(S, NQ, kblocks, kp, NQH);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(umma_pair_kernel<NQH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    const int npairs = std::max(1, std::min(h->num_sms / 2, ntiles));
+    h->qbf.ensure(static_cast<size_t>(NQ) * row_elems * 2);
+    h->lkey.ensure(static_cast<size_t>(2 * npairs) * NQ * kp);
+    h->lslot.ensure(static_cast<size_t>(2 * npairs) * NQ * kp);
+    h->ln.ensure(static_cast<size_t>(2 * npairs) * NQ);
+    h->gbound.ensure(512);
+    const void* rows = tf32 ? static_cast<const void*>(h->rows32) : static_cast<const void*>(h->rows16);
+    const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots);
+    const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, NQ, NQH);
+    for (int64_t q0 = 0; q0 < B; q0 += NQ) {
+        const int nq = static_cast<int>(std::min<int64_t>(NQ, B - q0));
+        res_prep_queries<<<grid_for(static_cast<int64_t>(NQ) * row_elems, 256, h->num_sms), 256, 0, st>>>(
+            q_dev + q0 * h->dim, nq, NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
+        CK(cudaMemsetAsync(h->gbound.p, 0, NQ * sizeof(uint32_t), st));
+        ResParams p{};
+        p.nslots = h->nslots;
+        p.ntiles = ntiles;
+        p.kblocks = kblocks;
+        p.nq = nq;
+        p.Nq = NQ;
+        p.kp = kp;
+        p.thr0 = thr0;
+        p.stages = S;
+        p.tf32 = tf32 ? 1 : 0;
+        p.slot_ids = h->ids_ascending ? 1 : 0;
+        p.gbound = h->gbound.p;
+        p.tile_stride = 1;
+        p.valid = h->valid;
+        p.ids = h->ids;
+        p.out_key = h->lkey.p;
+        p.out_slot = h->lslot.p;
+        p.out_n = h->ln.p;
+        const int sample_pairs = std::min(npairs, ntiles / 16);
+        if (thr0 < 0.5f && sample_pairs >= 16 && nq >= 8) {  // seed the admission bound (see umma_res_query)
+            ResParams sp = p;
+            sp.ntiles = sample_pairs;
+            sp.tile_stride = ntiles / sample_pairs;
+            umma_pair_kernel<NQH><<<2 * sample_pairs, kUmmaThreads, L.total, st>>>(qmap, rmap, sp);
+            sample_bound_kernel<<<nq, 256, 0, st>>>(h->lkey.p, h->ln.p, 2 * sample_pairs, nq, kp, h->gbound.p);
+            h->launches += 2;
+            CK(cudaGetLastError());
+        }
+        const size_t tk = tbegin(h, 2, st);
+        umma_pair_kernel<NQH><<<2 * npairs, kUmmaThreads, L.total, st>>>(qmap, rmap, p);
+        tend(h, tk, st);
+        h->launches += 2;
+        CK(cudaGetLastError());
+        merge_launch(h, 2 * npairs, nq, kp, q_dev + q0 * h->dim, k, min_sim, rerank, ids_dev + q0 * k,
+                     sims_dev + q0 * k, counts_dev + q0, st, q0);
+    }
+}
+
 void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, double min_sim, bool bf16, bool rerank,
                 int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, uint32_t mode) {
     const bool tf32 = !bf16;
@@ -735,6 +807,13 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         // cluster-multicast variant does not lower the per-query cost (the
         // L2->SM fan-out, not HBM, binds), so it is opt-in.
         const bool res = nq2 && (bf16 || B <= nq2);
+        // fp32 rows, 32 < B: a CTA pair keeps 64 queries per HBM pass
+        const bool pair_fits = 32 * row_bytes <= 96 * 1024;
+        const bool pair_auto = !bf16 && nq2 == 32 && B > nq2 && B <= 64;
+        if (!force_v1 && pair_fits && !(mode & SINE_SCAN_CLUSTER) && ((mode & SINE_SCAN_PAIR) || pair_auto)) {
+            umma_pair_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
+            return;
+        }
         if (!force_v1 && nq2 && (res || (mode & SINE_SCAN_CLUSTER))) {
             umma_res_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, nq2, ids_dev, sims_dev, counts_dev, st,
                            (mode & SINE_SCAN_CLUSTER) ? 8 : 1);

@@ -418,11 +418,13 @@ struct ResSmem {
     size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, total;
 };
 
-__host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, int kp) {
+// Nq_res: queries resident in this CTA's shared memory (== Nq except for the
+// CTA pair, where each CTA holds half of the Nq queries it scores).
+__host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, int kp, int Nq_res = -1) {
     ResSmem L;
     size_t off = 0;
     L.q_off = off;
-    off += static_cast<size_t>(kblocks) * Nq * kUmmaKB;
+    off += static_cast<size_t>(kblocks) * (Nq_res < 0 ? Nq : Nq_res) * kUmmaKB;
     L.a_off = off;
     off += static_cast<size_t>(S) * kUmmaN * kUmmaKB;
     L.bar_off = off;
@@ -810,6 +812,298 @@ __global__ void res_prep_queries(const double* q64, int nq, int Nq, int64_t dim,
             static_cast<float*>(out)[t] = static_cast<float>(v);
         else
             static_cast<__nv_bfloat16*>(out)[t] = __float2bfloat16_rn(static_cast<float>(v));
+    }
+}
+
+}  // namespace sine
+
+namespace sine {
+
+// ===========================================================================
+// CTA-pair variant (tcgen05 cta_group::2): one MMA covers M = 256 SE rows
+// (128 per CTA, each CTA TMA-loads its own rows) against N = 2*NQH queries,
+// of which each CTA keeps only its half resident in shared memory (the
+// B operand is split by N across the pair).  Each CTA's TMEM receives its
+// 128 rows x all N scores.  This keeps 64 fp32 (tf32) queries per HBM pass
+// with 96 KB of resident queries per SM.  The leader CTA (rank 0) owns the
+// stage / query barriers and issues the MMAs; completions are multicast to
+// both CTAs, and both epilogues release the accumulator on the leader.
+// ===========================================================================
+
+__device__ __forceinline__ uint32_t leader_addr(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
+
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_leader(const uint64_t* bar) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <int NQH>  // queries resident per CTA; the pair scores N = 2 * NQH
+__global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
+    umma_pair_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
+                     const ResParams p) {
+    constexpr int NQ = 2 * NQH;  // queries per launch (all of them reach every CTA's TMEM)
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages, nkb = p.kblocks, kp = p.kp;
+    const ResSmem L = res_smem_layout(S, NQ, nkb, kp, NQH);
+    uint8_t* sq = smem + L.q_off;
+    uint8_t* sa = smem + L.a_off;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* qfull = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qfull + 1);
+    uint32_t* lkey = reinterpret_cast<uint32_t*>(smem + L.list_key_off);
+    int32_t* lslot = reinterpret_cast<int32_t*>(smem + L.list_slot_off);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.qstate_off);
+    float* thr = reinterpret_cast<float*>(cnt + 2 * NQ);
+    uint32_t* pcnt = reinterpret_cast<uint32_t*>(smem + L.pend_off);
+    uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
+    uint2* merge_scratch = pend + NQ * kResQPer;
+    uint32_t* wball = reinterpret_cast<uint32_t*>(merge_scratch + 4 * (kMaxKp + kResQPer));
+    constexpr uint32_t kTmemCols = 2 * NQ <= 64 ? 64 : 128;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = static_cast<int>(cluster_ctarank());
+    const int pair = static_cast<int>(cluster_id_x());
+    const int npair = static_cast<int>(cluster_count_x());
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 8);  // 4 epilogue warps in each CTA (used on the leader)
+        }
+        mbar_init(qfull, 1);
+        fence_mbar_init();
+    }
+    for (int j = threadIdx.x; j < NQ; j += blockDim.x) {
+        cnt[j] = 0;
+        thr[j] = p.thr0;
+        pcnt[j] = 0;
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int kb_elems = p.tf32 ? kUmmaKB / 4 : kUmmaKB / 2;
+    const int ntiles = p.ntiles;  // 256-row pair tiles
+
+    if (warp == 4) {
+        // ---------------- TMA producers (both CTAs; the leader arms the barriers) ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
+            const uint64_t pol_rows = l2_evict_first_policy();
+            const uint64_t pol_q = l2_evict_last_policy();
+            if (rank == 0) mbar_arrive_expect_tx(qfull, 2u * nkb * NQH * kUmmaKB);
+            for (int kb = 0; kb < nkb; ++kb)
+                tma_load_2d_pair(sq + static_cast<size_t>(kb) * NQH * kUmmaKB, &qmap, leader_addr(qfull),
+                                 kb * kb_elems, rank * NQH, pol_q);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = pair; t < ntiles; t += npair) {
+                const int64_t row0 = (static_cast<int64_t>(t) * p.tile_stride * 2 + rank) * kUmmaN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(empty + s, ph ^ 1);
+                    if (rank == 0) mbar_arrive_expect_tx(full + s, 2u * kUmmaN * kUmmaKB);
+                    tma_load_2d_pair(sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB, &rmap, leader_addr(full + s),
+                                     kb * kb_elems, static_cast<int>(row0), pol_rows);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer (leader only): D[256 rows, N] += A . B^T ----------------
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = umma_idesc(p.tf32, 2 * kUmmaN, NQ);
+            mbar_wait(qfull, 0);
+            int s = 0;
+            uint32_t ph = 0;
+            int i = 0;
+            for (int t = pair; t < ntiles; t += npair, ++i) {
+                const int acc = i & 1;
+                mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * NQ;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full + s, ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB);
+                    const uint32_t b0 = smem_u32(sq + static_cast<size_t>(kb) * NQH * kUmmaKB);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ad = umma_smem_desc(a0 + kk * 32);
+                        const uint64_t bd = umma_smem_desc(b0 + kk * 32);
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        if (p.tf32)
+                            umma_tf32_pair(d, ad, bd, idesc, accum);
+                        else
+                            umma_f16_pair(d, ad, bd, idesc, accum);
+                    }
+                    umma_commit_pair(empty + s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit_pair(tfull + acc);
+            }
+        }
+    } else {
+        // ---------------- epilogue: thread = row of this CTA's half tile ----------------
+        const int tid = threadIdx.x;
+        const bool slot_ids = p.slot_ids != 0;
+        const int nq_local = min(NQ, p.nq);
+        int i = 0;
+        for (int t = pair; t < ntiles; t += npair, ++i) {
+            const int acc = i & 1;
+            const int64_t slot = (static_cast<int64_t>(t) * p.tile_stride * 2 + rank) * kUmmaN + tid;
+            const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
+            const bool live = ((vw >> (slot & 31)) & 1u) != 0;
+            if (tid < nq_local) {
+                const uint32_t g = *reinterpret_cast<volatile uint32_t*>(p.gbound + tid);
+                if (g) thr[tid] = fmaxf(thr[tid], key_f32(g));
+            }
+            named_bar_sync(2, 128);
+            mbar_wait(tfull + acc, (i >> 1) & 1);
+            tc_fence_after();
+            float sc[NQ];
+#pragma unroll
+            for (int c = 0; c < NQ / 16; ++c) {
+                uint32_t r[16];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * NQ + c * 16;
+                SINE_TMEM_LD16(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sc[c * 16 + j] = __uint_as_float(r[j]) + 0.0f;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0)
+                    mbar_arrive(tempty + acc);
+                else
+                    mbar_arrive_leader(tempty + acc);
+            }
+            uint64_t mask = 0;
+            if (live) {
+#pragma unroll
+                for (int j = 0; j < NQ; ++j)
+                    if (j < nq_local && sc[j] >= thr[j]) mask |= 1ull << j;
+            }
+            while (bar_red_or(1, 128, mask != 0)) {
+                for (int j = 0; j < NQ; ++j) {
+                    const uint32_t b = __ballot_sync(0xffffffffu, (mask >> j) & 1ull);
+                    if (lane == 0) wball[warp * NQ + j] = b;
+                }
+                named_bar_sync(2, 128);
+                if (mask) {
+                    const uint32_t lt = (1u << lane) - 1u;
+                    uint64_t m = mask;
+                    while (m) {
+                        const int j = __ffsll(m) - 1;
+                        m &= m - 1;
+                        uint32_t pos = __popc(wball[warp * NQ + j] & lt);
+                        for (int w = 0; w < warp; ++w) pos += __popc(wball[w * NQ + j]);
+                        if (pos < kResQPer) {
+                            pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
+                            mask &= ~(1ull << j);
+                        }
+                    }
+                }
+                if (tid < NQ) {
+                    uint32_t c = 0;
+                    for (int w = 0; w < 4; ++w) c += __popc(wball[w * NQ + tid]);
+                    pcnt[tid] = c;
+                }
+                named_bar_sync(2, 128);
+                for (int j = warp; j < nq_local; j += 4) {
+                    const int np = static_cast<int>(min(pcnt[j], static_cast<uint32_t>(kResQPer)));
+                    if (np > 0) {
+                        uint32_t* lk = lkey + j * kp;
+                        int32_t* ls = lslot + j * kp;
+                        const int n = warp_rank_merge(lk, ls, static_cast<int>(cnt[j]), kp, pend + j * kResQPer, np,
+                                                      merge_scratch + warp * (kMaxKp + kResQPer), p.ids, slot_ids,
+                                                      lane);
+                        if (lane == 0) {
+                            cnt[j] = n;
+                            if (n == kp) {
+                                const uint32_t wk = lk[kp - 1];
+                                thr[j] = fmaxf(thr[j], key_f32(wk));
+                                atomicMax(p.gbound + j, wk);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+                named_bar_sync(2, 128);
+                if (mask) {
+#pragma unroll
+                    for (int j = 0; j < NQ; ++j)
+                        if (((mask >> j) & 1ull) && !(sc[j] >= thr[j])) mask &= ~(1ull << j);
+                }
+            }
+        }
+        named_bar_sync(2, 128);
+        for (int j = 0; j < nq_local; ++j) {
+            const uint32_t n = cnt[j];
+            const size_t base = (static_cast<size_t>(blockIdx.x) * p.nq + j) * kp;
+            for (int e = tid; e < static_cast<int>(n); e += 128) {
+                p.out_key[base + e] = lkey[j * kp + e];
+                p.out_slot[base + e] = lslot[j * kp + e];
+            }
+            if (tid == 0) p.out_n[blockIdx.x * p.nq + j] = static_cast<int>(n);
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
 }
 

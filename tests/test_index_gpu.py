@@ -295,9 +295,9 @@ def test_tensor_core_and_cuda_core_paths_agree(pkg, index_golden, scan):
         for x, y, z in zip(a, b, c):
             np.testing.assert_array_equal(x, y)
             np.testing.assert_array_equal(x, z)
-        for B in (8, 16, 33, 64, 100, 129):  # resident group widths; cluster sizes 1, 2, 4
-            for cl in (False, True):
-                d = idx.query_batch(qs[:B], 5, ms, cluster=cl)
+        for B in (8, 16, 33, 64, 100, 129):  # resident group widths; cluster sizes 1, 2, 4; CTA pairs
+            for kw in ({}, {"cluster": True}, {"pair": True}):
+                d = idx.query_batch(qs[:B], 5, ms, **kw)
                 for x, y in zip(d, b):
                     np.testing.assert_array_equal(x, y[:B])
 
@@ -355,3 +355,27 @@ def test_certificate_falls_back_on_dense_clusters(pkg, scan):
             assert got_ids[j, :cnt[j]].tolist() == [c.id for c in want]
             np.testing.assert_allclose(got_sims[j, :cnt[j]], [c.similarity for c in want], atol=1e-12)
         assert idx.uncertified() >= 1
+
+
+def test_cta_pair_kernel_fp32_d768(pkg):
+    """fp32 rows at d=768 with 32 < B <= 64 take the tcgen05 cta_group::2
+    kernel; answers equal the fp32 CUDA-core scan and the oracle."""
+    rng = np.random.default_rng(77)
+    n, d = 30000, 768
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((64, d))
+    q[::2] = rows[rng.integers(0, n, 32)] + 0.3 * rng.standard_normal((32, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    idx = pkg.GpuCosineIndex(d)
+    idx.insert_batch(np.arange(n), rows)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    for B, ms in ((64, -1.0), (48, 0.3), (40, 0.9)):
+        a = idx.query_batch(q[:B], 10, ms)
+        b = idx.query_batch(q[:B], 10, ms, cuda_core=True)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+        for j in range(0, B, 7):
+            want = ora.query(q[j], 10, ms)
+            assert a[0][j, :a[2][j]].tolist() == [c.id for c in want]
