@@ -364,6 +364,7 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                 cases.append((scan, b, reps, tau, "auto"))
         cases.append((scan, 64, 5, TAU, "umma_v1"))
         cases.append((scan, 64, 3, TAU, "cuda_core"))
+        cases.append((scan, 4096, 1, TAU, "pair"))
     for scan, b, reps, tau, path in cases:
             if True:
                 qs = make_queries(rows, b, seed=100 + b)
@@ -374,7 +375,7 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                 cnt = torch.empty((b,), dtype=torch.int32, device="cuda")
                 run = lambda: idx.query_device(b, q.data_ptr(), K, tau, ids.data_ptr(), sims.data_ptr(),  # noqa
                                                cnt.data_ptr(), stream, scan=scan, cuda_core=path == "cuda_core",
-                                               umma_v1=path == "umma_v1")
+                                               umma_v1=path == "umma_v1", pair=path == "pair")
                 run()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
