@@ -117,6 +117,15 @@ int sine_query_device(sine_index_t *h, int64_t B, const double *q_dev, int k,
                       double min_sim, uint32_t mode, int64_t *ids_dev,
                       double *sims_dev, int32_t *counts_dev, void *stream);
 
+/* Asynchronous sine_query: enqueue the batch (host buffers, ideally pinned,
+ * which must stay valid until the wait) and return a ticket; up to 16
+ * batches in flight.  sine_query_wait blocks until the batch's results are
+ * in the output buffers, after the exactness certificate check. */
+int sine_query_submit(sine_index_t *h, int64_t B, const double *q, int k, double min_sim,
+                      uint32_t mode, int64_t *out_ids, double *out_sims,
+                      int32_t *out_counts, int64_t *ticket);
+int sine_query_wait(sine_index_t *h, int64_t ticket);
+
 int sine_update_meta(sine_index_t *h, int64_t n, const int64_t *ids,
                      const double *log_freq, const int64_t *frequency,
                      const double *last_access);

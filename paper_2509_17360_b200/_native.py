@@ -56,6 +56,10 @@ _SIGS = {
     "sine_query_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                                          ctypes.c_double, ctypes.c_uint32, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "sine_query_submit": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                         ctypes.c_double, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, _i64p]),
+    "sine_query_wait": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     "sine_update_meta": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _i64p, _f64p, _i64p, _f64p]),
     "sine_expired": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, _i64p,
                                     ctypes.c_int64, _i64p]),

@@ -181,6 +181,21 @@ struct sine_index {
     HostBuf<SelectState> st_h;
     HostBuf<unsigned long long> n_h;
     HostBuf<int32_t> cnt_h;
+    HostBuf<uint8_t> cert_h;
+    struct Ticket {
+        cudaEvent_t done = nullptr;
+        HostBuf<uint8_t> cert;
+        bool busy = false, certify = false;
+        int64_t B = 0;
+        int k = 0;
+        double min_sim = 0.0;
+        uint32_t mode = 0;
+        const double* q = nullptr;
+        int64_t* ids = nullptr;
+        double* sims = nullptr;
+        int32_t* counts = nullptr;
+    };
+    std::vector<Ticket> tickets;
 };
 
 namespace {
@@ -236,6 +251,16 @@ __global__ void gather_rows_kernel(const T* __restrict__ src, T* __restrict__ ds
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t r = t / width, c = t - r * width;
         dst[r * width + c] = src[from[r] * width + c];
+    }
+}
+
+__global__ void gather_rows64_kernel(const double* rows64, const int64_t* slots, int64_t n, int64_t dim,
+                                     double* out) {
+    const int64_t total = n * dim;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = t / dim, c = t - r * dim;
+        out[t] = rows64[slots[r] * dim + c];
     }
 }
 
@@ -1034,12 +1059,17 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
 // similarity) are re-run through the fp32 CUDA-core scan, whose 2e-6 error
 // bound is inside the north star's 1e-5 tie window.  Synchronises `st`.
 int64_t certify_and_fix(sine_index* h, int64_t B, const double* q_dev, int k, double min_sim, uint32_t mode,
-                        int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st) {
+                        int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st,
+                        const uint8_t* cert_host = nullptr) {
     if (!(mode & SINE_RERANK_F64) || !(h->flags & SINE_STORE_F32) || h->nlive == 0) return 0;
     const bool bf16 = (mode & 0xF) == SINE_SCAN_BF16;
     std::vector<uint8_t> cert(B);
-    CK(cudaMemcpyAsync(cert.data(), h->cert.p, B, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (cert_host) {
+        std::copy(cert_host, cert_host + B, cert.begin());
+    } else {
+        CK(cudaMemcpyAsync(cert.data(), h->cert.p, B, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
     const bool exact_path_used = !bf16 && (mode & SINE_SCAN_CUDA_CORE);
     if (exact_path_used) return 0;
     int64_t fixed = 0;
@@ -1300,7 +1330,11 @@ int sine_destroy(sine_index_t* h) {
         h->vids.release(), h->cub_tmp.release(), h->hist.release(), h->st.release(), h->qbf.release();
         h->vpack.release(), h->vpack_out.release(), h->vkey_out.release(), h->vslots_out.release();
         h->exp_off.release(), h->sel_h.release(), h->gbound.release();
-        h->st_h.release(), h->n_h.release(), h->cnt_h.release();
+        h->st_h.release(), h->n_h.release(), h->cnt_h.release(), h->cert_h.release();
+        for (auto& t : h->tickets) {
+            if (t.done) cudaEventDestroy(t.done);
+            t.cert.release();
+        }
         for (auto& e : h->ev) cudaEventDestroy(e);
         cudaStreamDestroy(h->stream);
         delete h;
@@ -1382,15 +1416,32 @@ int sine_ids(sine_index_t* h, int64_t* out, int64_t cap, int64_t* n) {
 
 int sine_get_rows(sine_index_t* h, int64_t n, const int64_t* ids, double* out) {
     return guarded([&] {
+        if (n <= 0) return;
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        std::vector<int64_t> slots(n);
         for (int64_t i = 0; i < n; ++i) {
-            const int64_t sl = find_slot(h, ids[i]);
-            if (sl < 0) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
-            CK(cudaMemcpyAsync(out + i * h->dim, h->rows64 + sl * h->dim, h->dim * sizeof(double),
-                               cudaMemcpyDeviceToHost, h->stream));
+            slots[i] = find_slot(h, ids[i]);
+            if (slots[i] < 0) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
         }
-        CK(cudaStreamSynchronize(h->stream));
+        // one gather on the device, one copy back (snapshots of 1M rows)
+        const int64_t chunk = std::max<int64_t>(1, (256ll << 20) / (h->dim * 8));
+        DevBuf<int64_t> dslots;
+        DevBuf<double> drows;
+        dslots.ensure(std::min(n, chunk));
+        drows.ensure(std::min(n, chunk) * h->dim);
+        for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+            const int64_t m = std::min(chunk, n - i0);
+            CK(cudaMemcpyAsync(dslots.p, slots.data() + i0, m * 8, cudaMemcpyHostToDevice, h->stream));
+            gather_rows64_kernel<<<grid_for(m * h->dim, 256, h->num_sms), 256, 0, h->stream>>>(h->rows64, dslots.p, m,
+                                                                                              h->dim, drows.p);
+            ++h->launches;
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(out + i0 * h->dim, drows.p, m * h->dim * 8, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        dslots.release();
+        drows.release();
     });
 }
 
@@ -1408,16 +1459,109 @@ int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_si
         h->o_cnt.ensure(B);
         CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
-        h->uncertified = certify_and_fix(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p,
-                                         h->stream);
+        // results and certificates come back together: one host sync in the
+        // common (all certified) case
+        const bool certify = (mode & SINE_RERANK_F64) && (h->flags & SINE_STORE_F32) && h->nlive > 0;
+        if (certify) {
+            h->cert_h.ensure(B);
+            CK(cudaMemcpyAsync(h->cert_h.p, h->cert.p, B, cudaMemcpyDeviceToHost, h->stream));
+        }
         CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        h->uncertified = 0;
+        if (certify) {
+            h->uncertified = certify_and_fix(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p,
+                                             h->stream, h->cert_h.p);
+            if (h->uncertified) {
+                CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost,
+                                   h->stream));
+                CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+            }
+        }
         if (h->timing) {
             CK(cudaEventElapsedTime(&h->t_scan, h->ev[0], h->ev[1]));
             CK(cudaEventElapsedTime(&h->t_merge, h->ev[1], h->ev[2]));
         }
+    });
+}
+
+int sine_query_submit(sine_index_t* h, int64_t B, const double* q, int k, double min_sim, uint32_t mode,
+                      int64_t* out_ids, double* out_sims, int32_t* out_counts, int64_t* ticket) {
+    return guarded([&] {
+        if (B <= 0) fail(SINE_EINVAL, "empty batch");
+        if (k < 1) fail(SINE_EINVAL, "k must be >= 1");
+        if (!(mode & SINE_NO_NORM_CHECK)) check_queries_host(h, B, q);
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        size_t slot = 0;
+        while (slot < h->tickets.size() && h->tickets[slot].busy) ++slot;
+        if (slot == h->tickets.size()) {
+            if (slot >= 16) fail(SINE_EINVAL, "too many queries in flight (max 16)");
+            h->tickets.emplace_back();
+            CK(cudaEventCreateWithFlags(&h->tickets[slot].done, cudaEventDisableTiming));
+        }
+        auto& t = h->tickets[slot];
+        h->q64.ensure(B * h->dim);
+        h->o_ids.ensure(B * k);
+        h->o_sims.ensure(B * k);
+        h->o_cnt.ensure(B);
+        CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
+        t.certify = (mode & SINE_RERANK_F64) && (h->flags & SINE_STORE_F32) && h->nlive > 0;
+        if (t.certify) {
+            t.cert.ensure(B);
+            CK(cudaMemcpyAsync(t.cert.p, h->cert.p, B, cudaMemcpyDeviceToHost, h->stream));
+        }
+        CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaEventRecord(t.done, h->stream));
+        t.busy = true;
+        t.B = B, t.k = k, t.min_sim = min_sim, t.mode = mode;
+        t.q = q, t.ids = out_ids, t.sims = out_sims, t.counts = out_counts;
+        *ticket = static_cast<int64_t>(slot);
+    });
+}
+
+int sine_query_wait(sine_index_t* h, int64_t ticket) {
+    return guarded([&] {
+        cudaEvent_t ev;
+        {
+            std::lock_guard<std::mutex> g(h->mu);
+            if (ticket < 0 || ticket >= static_cast<int64_t>(h->tickets.size()) || !h->tickets[ticket].busy)
+                fail(SINE_EINVAL, "unknown query ticket");
+            ev = h->tickets[ticket].done;
+        }
+        CK(cudaEventSynchronize(ev));  // without the handle lock: other calls proceed
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        auto& t = h->tickets[ticket];
+        t.busy = false;
+        h->uncertified = 0;
+        if (!t.certify) return;
+        // re-run uncertified queries on the fp32 scan from the caller's host
+        // copy (the device workspace may already hold a later batch)
+        DevBuf<double> q1;
+        DevBuf<int64_t> i1;
+        DevBuf<double> s1;
+        DevBuf<int32_t> c1;
+        for (int64_t b = 0; b < t.B; ++b) {
+            if (t.cert.p[b]) continue;
+            if (!q1.p) q1.ensure(h->dim), i1.ensure(t.k), s1.ensure(t.k), c1.ensure(1);
+            CK(cudaMemcpyAsync(q1.p, t.q + b * h->dim, h->dim * 8, cudaMemcpyHostToDevice, h->stream));
+            query_device_impl(h, 1, q1.p, t.k, t.min_sim, SINE_SCAN_F32 | SINE_RERANK_F64 | SINE_SCAN_CUDA_CORE, i1.p,
+                              s1.p, c1.p, h->stream);
+            CK(cudaMemcpyAsync(t.ids + b * t.k, i1.p, t.k * 8, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(t.sims + b * t.k, s1.p, t.k * 8, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(t.counts + b, c1.p, 4, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            ++h->uncertified;
+        }
+        q1.release(), i1.release(), s1.release(), c1.release();
     });
 }
 

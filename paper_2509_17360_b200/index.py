@@ -233,6 +233,16 @@ class GpuCosineIndex:
                                             ctypes.c_void_p(counts_ptr),
                                             ctypes.c_void_p(stream) if stream else None))
 
+    def query_batch_async(self, queries, k: int, min_similarity: float = -1.0, *, check: bool = True,
+                          scan: str | None = None, rerank: bool | None = None) -> "PendingQuery":
+        """Start a batched stage-1 on the device and return immediately; the
+        host can work (e.g. run the stage-2 judge on the previous batch)
+        until `.wait()` returns (ids, sims, counts)."""
+        q = check_matrix(queries, self.dimension) if check else N.f64(queries)
+        if k < 1:
+            raise ValidationError("k must be >= 1")
+        return PendingQuery(self, q, k, min_similarity, self._mode(scan, rerank))
+
     # --------------------------------------------------------- timing hooks
     def set_timing(self, on: bool = True) -> None:
         N.check(self._lib.sine_set_timing(self._h, 1 if on else 0))
@@ -334,3 +344,29 @@ def _meta_struct(meta: dict, n: int):
         keep[name] = a
         setattr(cols, name, N.ptr(a, ctypes.c_double if kind == "f" else ctypes.c_int64))
     return cols, keep
+
+
+class PendingQuery:
+    """An in-flight `query_batch_async` batch (pinned host buffers)."""
+
+    def __init__(self, index: GpuCosineIndex, q: np.ndarray, k: int, min_similarity: float, mode: int):
+        B = q.shape[0]
+        self._index = index
+        self._q = N.PinnedArray(q.shape, np.float64)
+        self._q.array[:] = q
+        self._ids = N.PinnedArray((B, k), np.int64)
+        self._sims = N.PinnedArray((B, k), np.float64)
+        self._counts = N.PinnedArray((B,), np.int32)
+        t = ctypes.c_int64()
+        N.check(index._lib.sine_query_submit(index.handle, B, self._q.array.ctypes.data, int(k),
+                                             float(min_similarity), mode, self._ids.array.ctypes.data,
+                                             self._sims.array.ctypes.data, self._counts.array.ctypes.data,
+                                             ctypes.byref(t)))
+        self._ticket = t.value
+        self._result = None
+
+    def wait(self):
+        if self._result is None:
+            N.check(self._index._lib.sine_query_wait(self._index.handle, self._ticket))
+            self._result = (self._ids.array.copy(), self._sims.array.copy(), self._counts.array.copy())
+        return self._result

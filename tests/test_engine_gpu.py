@@ -243,3 +243,55 @@ def test_large_purge_and_select_match_oracle(pkg, shuffled):
                                  meta["created"], meta["expiration"], now, cap)
     assert np.array_equal(np.concatenate([expired, victims]), want)
     assert len(idx) == n - expired.shape[0]
+
+
+def test_lookup_batch_pipelined_micro_batches(pkg):
+    """Micro-batched, overlapped stage-1 gives the same outcomes as one
+    batch and as sequential lookups when nothing is purged."""
+    emb = G.StubEmbedder(32, 1)
+    judge = G.StubJudge()
+    engines = [pkg.CacheEngine(pkg.CacheConfig(capacity_tokens=10_000), emb, judge) for _ in range(3)]
+    texts = [f"topic{t:02d} w{t % 3} {x}" for t in range(20) for x in ("alpha", "beta")]
+    for i, text in enumerate(texts):
+        e = emb.embed(text)
+        for eng in engines:
+            eng.admit(pkg.make_element(pkg.SemanticKey(text, "search"), f"v{i}", pkg.EmbeddingVector(e.components),
+                                       5, 400.0, 0.005, 0.0, 3600.0), now=0.0)
+    keys = [pkg.SemanticKey(f"topic{t:02d} w{(t + 1) % 3} {x}", "search") for t in range(20) for x in
+            ("alpha", "gamma", "beta")]
+    seq = [engines[0].lookup(k, 1.0) for k in keys]
+    one = engines[1].lookup_batch(keys, 1.0, micro_batch=1000)
+    pip = engines[2].lookup_batch(keys, 1.0, micro_batch=7)
+    for a, b, c in zip(seq, one, pip):
+        assert (a.kind, a.element_id, a.similarity, a.candidates_considered, a.judged) == \
+               (b.kind, b.element_id, b.similarity, b.candidates_considered, b.judged) == \
+               (c.kind, c.element_id, c.similarity, c.candidates_considered, c.judged)
+    assert engines[0].stats() == engines[1].stats() == engines[2].stats()
+
+
+def test_async_queries_in_flight_and_ttl_daemon(pkg):
+    import time as _t
+    rng = np.random.default_rng(4)
+    d, n = 64, 5000
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    idx = pkg.GpuCosineIndex(d)
+    idx.insert_batch(np.arange(n), rows)
+    qs = [rows[rng.integers(0, n, 9)] for _ in range(5)]
+    pend = [idx.query_batch_async(q, 6, 0.2) for q in qs]      # five batches in flight
+    for q, p in zip(qs, reversed(pend[::-1])):
+        want = idx.query_batch(q, 6, 0.2)
+        got = p.wait()
+        for x, y in zip(got, want):
+            np.testing.assert_array_equal(x, y)
+    # background TTL purge
+    eng = pkg.CacheEngine(pkg.CacheConfig(capacity_tokens=10_000), _DimEmbedder(), None)
+    for j in range(20):
+        spec = dict(size=3, staticity=5, freq=1, lat=50.0, cost=0.005, created=0.0, ttl=5.0 if j % 2 else 1e9)
+        eng.admit(_mk(pkg, spec, j), now=0.0)
+    stop = eng.start_ttl_maintenance(0.01, clock=lambda: 100.0)
+    deadline = _t.time() + 10
+    while len(eng) > 10 and _t.time() < deadline:
+        _t.sleep(0.02)
+    stop.set()
+    assert len(eng) == 10 and eng.stats()["expirations"] == 10
