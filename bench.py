@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-regimes", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-evict", action="store_true")
+    ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--evict-rows", type=int, default=10_000_000)
     return ap.parse_args()
 
@@ -317,6 +318,9 @@ def run_ours(args):
     regimes = []
     if world == 1 and not args.no_regimes:
         regimes = measure_regimes(idx, rows, torch, hbm_peak)
+    trace = None
+    if world == 1 and not args.no_trace:
+        trace = measure_trace(rows)
     eviction = None
     if world == 1 and not args.no_evict:
         del idx
@@ -344,7 +348,7 @@ def run_ours(args):
                            "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
                            "l2": "no flush: the index (>= 1.5 GB) exceeds the 126 MB L2"},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": int(launches), "regimes": regimes, "eviction": eviction}
+                "gpu_launches": int(launches), "regimes": regimes, "eviction": eviction, "trace": trace}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -494,6 +498,154 @@ def measure_eviction(n, hbm_peak, cpu_sample=300_000):
                          "frac": (n * bytes_per_se / (dev_ms / 1e3) / 1e9 / hbm_peak) if dev_ms else None},
             "cpu_baseline": {"value": m / cpu_s, "unit": "SEs/s", "cores": 1, "kind": "port",
                              "sample": f"{m} SEs: oracle evict_until_fits (Python cal_score + tuple sort)"}}
+
+
+# ------------------------------------------------- config E: mixed trace
+
+class _DictEmbedder:
+    def __init__(self, d):
+        self.dimension = d
+        self.seed = 1
+        self.table = {}
+
+    def embed(self, text):
+        return self.table[text]
+
+
+class _TextJudge:
+    """Constant-time stage-2 stub: same canonical key text -> 1.0."""
+
+    def score(self, query_text, key_text, value):
+        return 1.0 if query_text.split("#")[0] == key_text else 0.5
+
+    def staticity(self, key_text, value):
+        return 5
+
+
+def trace_ops(n, d, n_ops, rng, rows):
+    """80% lookups (70% Zipf(0.99) reuse of stored rows + noise, 30% fresh),
+    15% admissions at capacity, 5% evict_until_fits after a small capacity
+    cut."""
+    p = np.arange(1, n + 1, dtype=np.float64) ** -0.99
+    p /= p.sum()
+    picks = rng.choice(n, size=n_ops, p=p)
+    ops = []
+    for j in range(n_ops):
+        r = rng.random()
+        if r < 0.80:
+            if rng.random() < 0.7:
+                i = int(picks[j])
+                g = rng.standard_normal(d)
+                g -= (g @ rows[i]) * rows[i]
+                g /= np.linalg.norm(g)
+                v = 0.95 * rows[i] + math.sqrt(1 - 0.95 ** 2) * g
+                ops.append(("lookup", f"e{i}#{j}", v / np.linalg.norm(v)))
+            else:
+                v = rng.standard_normal(d)
+                ops.append(("lookup", f"fresh{j}", v / np.linalg.norm(v)))
+        elif r < 0.95:
+            v = rng.standard_normal(d)
+            ops.append(("admit", f"new{j}", v / np.linalg.norm(v), int(rng.integers(1, 30))))
+        else:
+            ops.append(("evict", int(rng.integers(50, 500))))
+    return ops
+
+
+def _make_elements(model, n, meta, shared_emb):
+    return [model.SemanticElement(model.SemanticKey(f"e{i}", "search"), "t",
+                                  shared_emb, int(meta["staticity"][i]), int(meta["freq"][i]),
+                                  float(meta["lat"][i]), float(meta["cost"][i]), int(meta["size"][i]),
+                                  float(meta["created"][i]), float(meta["expiration"][i])) for i in range(n)]
+
+
+def run_trace(engine, ops, embedder, model, now0, batched):
+    """Replays the trace; lookups between two writes go through one
+    lookup_batch call when `batched`."""
+    now = now0
+    i = 0
+    done = 0
+    while i < len(ops):
+        op = ops[i]
+        now += 0.01
+        if op[0] == "lookup":
+            j = i
+            while j < len(ops) and ops[j][0] == "lookup" and (batched or j == i):
+                embedder.table[ops[j][1]] = model.EmbeddingVector(tuple(ops[j][2]))
+                j += 1
+            keys = [model.SemanticKey(ops[m][1], "search") for m in range(i, j)]
+            if batched:
+                engine.lookup_batch(keys, now)
+            else:
+                engine.lookup(keys[0], now)
+            done += j - i
+            i = j
+            continue
+        if op[0] == "admit":
+            el = model.SemanticElement(model.SemanticKey(op[1], "search"), " ".join(["t"] * op[3]),
+                                       model.EmbeddingVector(tuple(op[2])), 5, 0, 400.0, 0.005, op[3], now,
+                                       now + 2.0e4)
+            engine.admit(el, now)
+        else:
+            engine.config.capacity_tokens -= op[1]
+            engine.evict_until_fits(now)
+        done += 1
+        i += 1
+    return done
+
+
+def measure_trace(rows, n_ops=2000, cpu_ops=24):
+    """Config E: end-to-end cache ops/s of the GPU engine on 1M SEs (d=768)
+    vs the reference engine loop (oracle restatement) on the host."""
+    import paper_2509_17360_b200 as P
+    from paper_2509_17360_b200 import model as M
+
+    n, d = rows.shape
+    rng = np.random.default_rng(21)
+    meta = evict_metadata(n, seed=6)
+    meta["created"] = np.zeros(n)
+    meta["expiration"] = np.full(n, 1.0e5)
+    shared = M.EmbeddingVector((1.0,))
+    out = {"workload": f"config E: {n} SEs x d={d}, 80% lookup (70% Zipf reuse) / 15% admit at capacity / "
+                       f"5% evict_until_fits, constant-time judge stub"}
+    for batched in (False, True):
+        ops = trace_ops(n, d, n_ops, rng, rows)
+        emb = _DictEmbedder(d)
+        els = _make_elements(M, n, meta, shared)
+        usage = int(meta["size"].sum())
+        eng = P.CacheEngine(P.CacheConfig(capacity_tokens=usage), emb, _TextJudge())
+        eng.bulk_admit(els, rows, now=0.0)
+        run_trace(eng, ops[:50], emb, M, 1.0, batched)  # warm-up
+        t0 = time.perf_counter()
+        done = run_trace(eng, ops[50:], emb, M, 2.0, batched)
+        dt = time.perf_counter() - t0
+        out["batched_ops_per_s" if batched else "ops_per_s"] = done / dt
+        st = eng.stats()
+        out["hit_rate" if not batched else "hit_rate_batched"] = st["hits"] / max(1, st["lookups"])
+        del eng, els
+    # CPU: the reference engine loop on the same population (bounded sample)
+    from oracle import sine_oracle as O
+    ops = trace_ops(n, d, cpu_ops, rng, rows)
+    table = {}
+    oe = O.OracleEngine(d, int(meta["size"].sum()), lambda t: table[t], _TextJudge().score, capacity_rows=n + 64)
+    oe.bulk_load(_make_elements(M, n, meta, shared), rows)
+    now = 2.0
+    t0 = time.perf_counter()
+    for op in ops:
+        now += 0.01
+        if op[0] == "lookup":
+            table[op[1]] = op[2]
+            oe.lookup(M.SemanticKey(op[1], "search"), now)
+        elif op[0] == "admit":
+            oe.admit(M.SemanticElement(M.SemanticKey(op[1], "search"), " ".join(["t"] * op[3]),
+                                       M.EmbeddingVector(tuple(op[2])), 5, 0, 400.0, 0.005, op[3], now,
+                                       now + 2.0e4), now)
+        else:
+            oe.capacity -= op[1]
+            oe.evict_until_fits(now)
+    out["cpu_baseline"] = {"value": len(ops) / (time.perf_counter() - t0), "unit": "ops/s", "cores": os.cpu_count(),
+                           "kind": "port", "sample": f"{len(ops)} trace ops on the oracle engine loop "
+                                                     "(numpy float64 GEMV + Python LCFU sort), same 1M SEs"}
+    return out
 
 
 def main():

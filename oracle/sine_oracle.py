@@ -19,7 +19,7 @@ Every function cites the reference file:line it restates
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
@@ -278,3 +278,94 @@ def evict_until_fits_np(ids, freq, cost, lat, stat, size, created, expiration,
     cum = np.cumsum(size[live][order])
     m = int(np.searchsorted(cum, usage - capacity, side="left")) + 1
     return np.concatenate([exp_ids, lid[order[:m]]])
+
+
+# ------------------------------------------------- engine loop (config E)
+
+class OracleEngine:
+    """Restatement of the reference CacheEngine hot loop (src/engine.py:
+    lookup :160-223, admit :300-336, evict_until_fits :342-360) over
+    OracleExactIndex and the oracle eviction order -- the CPU baseline of
+    the mixed agent trace.  Elements are any objects with the
+    SemanticElement fields; `embed` maps text -> unit vector."""
+
+    def __init__(self, dimension, capacity_tokens, embed, judge_score, tau_sim=0.9, tau_lsm=0.9,
+                 candidate_k=5, policy="lcfu", capacity_rows=16):
+        self.index = OracleExactIndex(dimension, capacity=capacity_rows)
+        self.capacity = capacity_tokens
+        self.embed = embed
+        self.judge_score = judge_score
+        self.tau_sim, self.tau_lsm, self.k, self.policy = tau_sim, tau_lsm, candidate_k, policy
+        self.elements, self.by_key, self.last_access = {}, {}, {}
+        self.usage = 0
+        self.next_id = 1
+
+    def bulk_load(self, elements, rows):
+        ids = list(range(self.next_id, self.next_id + len(elements)))
+        self.index.bulk_load(ids, rows)
+        for eid, el in zip(ids, elements):
+            self.elements[eid] = el
+            self.by_key[(el.key.text, el.key.tool)] = eid
+            self.last_access[eid] = el.created_at
+            self.usage += el.size_tokens
+        self.next_id += len(elements)
+
+    def _remove(self, eid):
+        el = self.elements.pop(eid)
+        self.by_key.pop((el.key.text, el.key.tool), None)
+        self.last_access.pop(eid, None)
+        self.usage -= el.size_tokens
+        self.index.remove(eid)
+
+    def lookup(self, key, now):
+        cands = self.index.query(self.embed(key.text), self.k, self.tau_sim)   # engine.py:177-178
+        for c in cands:                                                        # engine.py:185-204
+            el = self.elements.get(c.id)
+            if el is None or el.key.tool != key.tool:
+                continue
+            if el.is_expired(now):
+                self._remove(c.id)
+                continue
+            if self.judge_score(key.text, el.key.text, el.value) >= self.tau_lsm:
+                # hit bookkeeping (engine.py:209-217)
+                self.elements[c.id] = replace(el, frequency=el.frequency + 1)
+                self.last_access[c.id] = now
+                return c.id
+        return None
+
+    def _purge(self, now):                                                      # engine.py:362-367
+        for eid in sorted(e for e, el in self.elements.items() if el.is_expired(now)):
+            self._remove(eid)
+
+    def admit(self, el, now):                                                   # engine.py:300-336
+        old = self.by_key.get((el.key.text, el.key.tool))
+        if old is not None:
+            self._remove(old)
+        self._purge(now)
+        evicted = []
+        if self.usage + el.size_tokens > self.capacity:
+            for v in victim_order(self.elements, now, self.policy, self.last_access):
+                self._remove(v)
+                evicted.append(v)
+                if self.usage + el.size_tokens <= self.capacity:
+                    break
+        eid = self.next_id
+        self.next_id += 1
+        self.index.insert(eid, el.embedding)
+        self.elements[eid] = el
+        self.by_key[(el.key.text, el.key.tool)] = eid
+        self.last_access[eid] = now
+        self.usage += el.size_tokens
+        return eid, evicted
+
+    def evict_until_fits(self, now):                                            # engine.py:342-360
+        removed = sorted(e for e, el in self.elements.items() if el.is_expired(now))
+        for eid in removed:
+            self._remove(eid)
+        if self.usage > self.capacity:
+            for v in victim_order(self.elements, now, self.policy, self.last_access):
+                self._remove(v)
+                removed.append(v)
+                if self.usage <= self.capacity:
+                    break
+        return removed
