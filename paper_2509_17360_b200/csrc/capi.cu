@@ -732,10 +732,11 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
 
 // CTA-pair tensor-core scan (cta_group::2): groups of 2*NQH queries, each
 // CTA of a pair holding NQH of them; one HBM pass per group.
-void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
-                     bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
-                     cudaStream_t st) {
-    constexpr int NQH = 32, NQ = 2 * NQH;
+template <int NQH>
+void umma_pair_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                       bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                       cudaStream_t st) {
+    constexpr int NQ = 2 * NQH;
     const bool tf32 = !bf16;
     const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
     const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
@@ -802,6 +803,18 @@ void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
     }
 }
 
+// The pair keeps NQH queries per CTA: 64 when they fit 96 KB (bf16 at
+// d <= 768), else 32.
+void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                     bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                     cudaStream_t st) {
+    const int64_t row_bytes = bf16 ? h->stride16 * 2 : h->stride32 * 4;
+    if (64 * row_bytes <= 96 * 1024 && B > 32)
+        umma_pair_query_t<64>(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
+    else
+        umma_pair_query_t<32>(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
+}
+
 void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, double min_sim, bool bf16, bool rerank,
                 int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, uint32_t mode) {
     const bool tf32 = !bf16;
@@ -834,7 +847,8 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         const bool res = nq2 && (bf16 || B <= nq2);
         // fp32 rows, 32 < B: a CTA pair keeps 64 queries per HBM pass
         const bool pair_fits = 32 * row_bytes <= 96 * 1024;
-        const bool pair_auto = !bf16 && nq2 == 32 && B > nq2 && B <= 64;
+        const bool pair_auto = (!bf16 && nq2 == 32 && B > nq2 && B <= 64) ||
+                               (bf16 && nq2 == 64 && B > 64 && 64 * row_bytes <= 96 * 1024);
         if (!force_v1 && pair_fits && !(mode & SINE_SCAN_CLUSTER) && ((mode & SINE_SCAN_PAIR) || pair_auto)) {
             umma_pair_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
             return;

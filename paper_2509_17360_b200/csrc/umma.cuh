@@ -894,7 +894,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
     uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
     uint2* merge_scratch = pend + NQ * kResQPer;
     uint32_t* wball = reinterpret_cast<uint32_t*>(merge_scratch + 4 * (kMaxKp + kResQPer));
-    constexpr uint32_t kTmemCols = 2 * NQ <= 64 ? 64 : 128;
+    constexpr uint32_t kTmemCols = 2 * NQ <= 64 ? 64 : (2 * NQ <= 128 ? 128 : 256);
+    constexpr int MW = (NQ + 63) / 64;  // 64-bit words of the per-row query mask
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = static_cast<int>(cluster_ctarank());
@@ -1029,29 +1030,42 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
                 else
                     mbar_arrive_leader(tempty + acc);
             }
-            uint64_t mask = 0;
+            uint64_t mask[MW];
+#pragma unroll
+            for (int w = 0; w < MW; ++w) mask[w] = 0;
             if (live) {
 #pragma unroll
                 for (int j = 0; j < NQ; ++j)
-                    if (j < nq_local && sc[j] >= thr[j]) mask |= 1ull << j;
+                    if (j < nq_local && sc[j] >= thr[j]) mask[j >> 6] |= 1ull << (j & 63);
             }
-            while (bar_red_or(1, 128, mask != 0)) {
+            auto any_mask = [&]() {
+                uint64_t o = 0;
+#pragma unroll
+                for (int w = 0; w < MW; ++w) o |= mask[w];
+                return o != 0;
+            };
+            while (bar_red_or(1, 128, any_mask())) {
+#pragma unroll
                 for (int j = 0; j < NQ; ++j) {
-                    const uint32_t b = __ballot_sync(0xffffffffu, (mask >> j) & 1ull);
+                    const uint32_t b = __ballot_sync(0xffffffffu, (mask[j >> 6] >> (j & 63)) & 1ull);
                     if (lane == 0) wball[warp * NQ + j] = b;
                 }
                 named_bar_sync(2, 128);
-                if (mask) {
+                if (any_mask()) {
                     const uint32_t lt = (1u << lane) - 1u;
-                    uint64_t m = mask;
-                    while (m) {
-                        const int j = __ffsll(m) - 1;
-                        m &= m - 1;
-                        uint32_t pos = __popc(wball[warp * NQ + j] & lt);
-                        for (int w = 0; w < warp; ++w) pos += __popc(wball[w * NQ + j]);
-                        if (pos < kResQPer) {
-                            pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
-                            mask &= ~(1ull << j);
+#pragma unroll
+                    for (int w = 0; w < MW; ++w) {
+                        uint64_t m = mask[w];
+                        while (m) {
+                            const int jj = __ffsll(m) - 1;
+                            m &= m - 1;
+                            const int j = w * 64 + jj;
+                            uint32_t pos = __popc(wball[warp * NQ + j] & lt);
+                            for (int x = 0; x < warp; ++x) pos += __popc(wball[x * NQ + j]);
+                            if (pos < kResQPer) {
+                                pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
+                                mask[w] &= ~(1ull << jj);
+                            }
                         }
                     }
                 }
@@ -1081,10 +1095,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
                     __syncwarp();
                 }
                 named_bar_sync(2, 128);
-                if (mask) {
+                if (any_mask()) {
 #pragma unroll
                     for (int j = 0; j < NQ; ++j)
-                        if (((mask >> j) & 1ull) && !(sc[j] >= thr[j])) mask &= ~(1ull << j);
+                        if (((mask[j >> 6] >> (j & 63)) & 1ull) && !(sc[j] >= thr[j]))
+                            mask[j >> 6] &= ~(1ull << (j & 63));
                 }
             }
         }
