@@ -145,6 +145,10 @@ int sine_stream(sine_index_t *h, void **stream);
 int sine_set_timing(sine_index_t *h, int on);
 int sine_last_timing(sine_index_t *h, float *scan_ms, float *merge_ms, float *evict_ms);
 int sine_kernel_launches(sine_index_t *h, int64_t *n);
+/* Enqueue a device copy of the last query's per-query exactness
+ * certificates (B bytes, 1 = exact) -- lets a pipelined caller check them
+ * later instead of synchronising after every batch. */
+int sine_copy_certificates(sine_index_t *h, int64_t B, void *dst_dev, void *stream);
 /* Queries the last certified call had to re-run on the fp32 scan. */
 int sine_uncertified(sine_index_t *h, int64_t *n);
 /* Sum of device time (ms) and count of the launches of one kernel kind

@@ -71,6 +71,7 @@ _SIGS = {
                                         ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "sine_kernel_launches": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
     "sine_uncertified": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
+    "sine_copy_certificates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "sine_timing_totals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _f64p, _i64p, ctypes.c_int]),
     "sine_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "sine_host_free": (ctypes.c_int, [ctypes.c_void_p]),

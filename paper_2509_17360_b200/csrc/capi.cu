@@ -1728,6 +1728,15 @@ int sine_timing_totals(sine_index_t* h, int kind, double* total_ms, int64_t* lau
     });
 }
 
+int sine_copy_certificates(sine_index_t* h, int64_t B, void* dst_dev, void* stream) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        if (!h->cert.p || static_cast<int64_t>(h->cert.n) < B) fail(SINE_EINVAL, "no certificates for that batch");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        CK(cudaMemcpyAsync(dst_dev, h->cert.p, B, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
 int sine_uncertified(sine_index_t* h, int64_t* n) {
     return guarded([&] { *n = h->uncertified; });
 }

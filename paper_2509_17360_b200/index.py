@@ -265,6 +265,11 @@ class GpuCosineIndex:
         N.check(self._lib.sine_timing_totals(self._h, kind, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
         return ms.value, n.value
 
+    def copy_certificates(self, B: int, dst_ptr: int, stream: int | None = None) -> None:
+        """Enqueue a device copy of the last batch's exactness certificates."""
+        N.check(self._lib.sine_copy_certificates(self._h, int(B), ctypes.c_void_p(dst_ptr),
+                                                 ctypes.c_void_p(stream) if stream else None))
+
     def uncertified(self) -> int:
         """Queries the last (certified) call re-ran on the fp32 scan."""
         n = ctypes.c_int64()
