@@ -60,6 +60,11 @@ extern "C" {
 #define SINE_SCAN_CLUSTER  0x1000u /* tcgen05: share row tiles across up to 8 CTAs
                                       (TMA multicast), one HBM pass per 8 query groups */
 #define SINE_SCAN_PAIR     0x2000u /* tcgen05 cta_group::2: prefer the CTA-pair kernel */
+#define SINE_SCAN_GEMM     0x4000u /* tcgen05 cta_group::2 tiled GEMM (256 rows x 256
+                                      queries per pair tile, all query tiles of the batch
+                                      in one launch); chosen automatically for large
+                                      batches at high thresholds */
+#define SINE_SCAN_NO_GEMM  0x8000u /* never use the tiled GEMM path                */
 #define SINE_CERTIFY       0x800u /* sine_query_device: check the per-query exactness
                                      certificate and re-run failures on the fp32
                                      CUDA-core scan (synchronises the stream);
@@ -145,6 +150,10 @@ int sine_stream(sine_index_t *h, void **stream);
 int sine_set_timing(sine_index_t *h, int on);
 int sine_last_timing(sine_index_t *h, float *scan_ms, float *merge_ms, float *evict_ms);
 int sine_kernel_launches(sine_index_t *h, int64_t *n);
+/* Tiled-GEMM stage-1 launches (SINE_SCAN_GEMM) whose per-query candidate
+ * buffers overflowed and were re-run on the list-keeping kernels.  Not in
+ * the reference (diagnostic for the batched path, like sine_uncertified). */
+int sine_gemm_overflows(sine_index_t *h, int64_t *n);
 /* Enqueue a device copy of the last query's per-query exactness
  * certificates (B bytes, 1 = exact) -- lets a pipelined caller check them
  * later instead of synchronising after every batch. */

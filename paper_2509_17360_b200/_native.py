@@ -22,6 +22,7 @@ SINE_OK, SINE_EINVAL, SINE_ECUDA, SINE_ENCCL, SINE_ENOMEM, SINE_ENOTFOUND, SINE_
 STORE_F32, STORE_BF16, STORE_META = 0x1, 0x2, 0x4
 SCAN_F32, SCAN_BF16, RERANK_F64, NO_NORM_CHECK, SCAN_CUDA_CORE, SCAN_UMMA_V1, CERTIFY, SCAN_CLUSTER, SCAN_PAIR = \
     0x0, 0x1, 0x10, 0x100, 0x200, 0x400, 0x800, 0x1000, 0x2000
+SCAN_GEMM, SCAN_NO_GEMM = 0x4000, 0x8000
 POLICIES = {"lcfu": 0, "lru": 1, "lfu": 2}
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -70,6 +71,7 @@ _SIGS = {
     "sine_last_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
                                         ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "sine_kernel_launches": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
+    "sine_gemm_overflows": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
     "sine_uncertified": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
     "sine_copy_certificates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "sine_timing_totals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _f64p, _i64p, ctypes.c_int]),

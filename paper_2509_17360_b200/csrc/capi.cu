@@ -175,6 +175,8 @@ struct sine_index {
     DevBuf<int32_t> vslots_out;
     DevBuf<int64_t> exp_off;
     DevBuf<uint32_t> gbound;        // chip-wide admission bounds of the running launch
+    DevBuf<uint32_t> gcnt;          // tiled GEMM: candidates per query + overflow counter
+    int64_t gemm_overflows = 0;     // GEMM launches re-run on the list-keeping kernels
     HostBuf<unsigned long long> sel_h;  // counter + kand + kor
     DevBuf<SelectState> st;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
@@ -815,6 +817,79 @@ void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
         umma_pair_query_t<32>(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
 }
 
+// Tiled tensor-core GEMM over the whole batch (umma_gemm_kernel): one launch,
+// every query tile.  Returns false (nothing written to the outputs) when a
+// query's candidates overflowed the chunk capacity; the caller then runs the
+// list-keeping kernels.
+constexpr int kGemmChunks = 32;
+constexpr int64_t kGemmMinBatch = 256;
+
+bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                     bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                     cudaStream_t st) {
+    const bool tf32 = !bf16;
+    const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
+    const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
+    const int kblocks = static_cast<int>(row_bytes / kUmmaKB);
+    const int nrt = static_cast<int>((h->nslots + kGemmRows - 1) / kGemmRows);
+    const int nqt = static_cast<int>((B + kGemmNQ - 1) / kGemmNQ);
+    if (static_cast<int64_t>(nrt) * nqt >= (1ll << 31)) return false;
+    const int64_t Bpad = static_cast<int64_t>(nqt) * kGemmNQ;
+    const int S = static_cast<int>(std::min<size_t>(7, (227 * 1024 - gemm_smem_bytes(0)) / (2 * 128 * kUmmaKB)));
+    const size_t smem = gemm_smem_bytes(S);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    const int nitems = nrt * nqt;
+    const int npairs = std::max(1, std::min(h->num_sms / 2, nitems));
+    h->qbf.ensure(static_cast<size_t>(Bpad) * row_elems * 2);
+    h->lkey.ensure(static_cast<size_t>(kGemmChunks) * B * kp);
+    h->lslot.ensure(static_cast<size_t>(kGemmChunks) * B * kp);
+    h->ln.ensure(static_cast<size_t>(kGemmChunks) * B);
+    h->gcnt.ensure(static_cast<size_t>(B) + 1);
+    h->gbound.ensure(static_cast<size_t>(B));
+    h->n_h.ensure(1);
+    const void* rows = tf32 ? static_cast<const void*>(h->rows32) : static_cast<const void*>(h->rows16);
+    const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots, 128);
+    const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, Bpad, 128);
+    res_prep_queries<<<grid_for(Bpad * row_elems, 256, h->num_sms), 256, 0, st>>>(
+        q_dev, static_cast<int>(B), static_cast<int>(Bpad), h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
+    CK(cudaMemsetAsync(h->gcnt.p, 0, (static_cast<size_t>(B) + 1) * sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(h->gbound.p, 0, static_cast<size_t>(B) * sizeof(uint32_t), st));
+    GemmParams p{};
+    p.nslots = h->nslots;
+    p.nrt = nrt;
+    p.nqt = nqt;
+    p.kblocks = kblocks;
+    p.nq = static_cast<int>(B);
+    p.kp = kp;
+    p.chunks = kGemmChunks;
+    p.thr0 = thr0;
+    p.stages = S;
+    p.tf32 = tf32 ? 1 : 0;
+    p.valid = h->valid;
+    p.cnt = h->gcnt.p;
+    p.out_key = h->lkey.p;
+    p.out_slot = h->lslot.p;
+    const size_t tk = tbegin(h, 2, st);
+    umma_gemm_kernel<<<2 * npairs, kGemmThreads, smem, st>>>(qmap, rmap, p);
+    tend(h, tk, st);
+    CK(cudaGetLastError());
+    gemm_finish_kernel<<<static_cast<int>((B + 255) / 256), 256, 0, st>>>(h->gcnt.p, static_cast<int>(B), kp,
+                                                                          kGemmChunks, h->ln.p, h->gcnt.p + B);
+    h->launches += 3;
+    CK(cudaGetLastError());
+    uint32_t* ovf = reinterpret_cast<uint32_t*>(h->n_h.p);
+    CK(cudaMemcpyAsync(ovf, h->gcnt.p + B, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*ovf) return false;
+    merge_launch(h, kGemmChunks, static_cast<int>(B), kp, q_dev, k, min_sim, rerank, ids_dev, sims_dev, counts_dev,
+                 st, 0);
+    return true;
+}
+
 void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, double min_sim, bool bf16, bool rerank,
                 int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, uint32_t mode) {
     const bool tf32 = !bf16;
@@ -840,6 +915,15 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         const int64_t passes2 = nq2 ? (B + nq2 - 1) / nq2 : INT64_MAX;
         const int64_t passes1 = (B + kUmmaM - 1) / kUmmaM;
         const bool force_v1 = (mode & 0x400u) != 0;
+        // large batches at a high admission floor: one tiled GEMM launch
+        // (256 x 256 pair tiles, N = 256 per MMA) instead of B/128 HBM passes
+        const bool gemm_auto = !(mode & SINE_SCAN_NO_GEMM) && !force_v1 && B >= kGemmMinBatch && thr0 >= 0.25f &&
+                               !(mode & (SINE_SCAN_PAIR | SINE_SCAN_CLUSTER));
+        if ((mode & SINE_SCAN_GEMM) || gemm_auto) {
+            if (umma_gemm_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st))
+                return;
+            ++h->gemm_overflows;  // candidates overflowed: fall through to the list-keeping kernels
+        }
         // measured per-query cost on B200 (1M x 768): resident bf16 ~4.8 us,
         // resident tf32 ~17 us (32-query groups), streaming v1 ~6 us; the
         // cluster-multicast variant does not lower the per-query cost (the
@@ -1739,6 +1823,10 @@ int sine_copy_certificates(sine_index_t* h, int64_t B, void* dst_dev, void* stre
 
 int sine_uncertified(sine_index_t* h, int64_t* n) {
     return guarded([&] { *n = h->uncertified; });
+}
+
+int sine_gemm_overflows(sine_index_t* h, int64_t* n) {
+    return guarded([&] { *n = h->gemm_overflows; });
 }
 
 int sine_kernel_launches(sine_index_t* h, int64_t* n) {

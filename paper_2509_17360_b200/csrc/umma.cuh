@@ -1123,3 +1123,245 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
 }
 
 }  // namespace sine
+
+namespace sine {
+
+// ===========================================================================
+// Large batches (the tensor-bound regime, B in the thousands): a tiled
+// GEMM over (256-row tile) x (256-query tile) work items, all query tiles of
+// the batch in ONE launch.  A CTA pair (tcgen05 cta_group::2) owns an item:
+// each CTA TMA-loads 128 rows and 128 queries per 128-byte K block, the
+// leader issues M=256 x N=256 MMAs, and each CTA's TMEM receives its 128 rows
+// x 256 query scores (double-buffered: 2 x 256 columns = all 512).  Items are
+// ordered row-tile-major, so the pairs in flight at any moment work on a few
+// row tiles x every query tile: each row tile is read from HBM once and
+// re-served from L2 to the other query tiles; the queries (B x d) stay L2
+// resident.
+//
+// Epilogue (warps 0-3, thread = row): every score is compared with the
+// uniform admission floor thr0; passing (query, row) pairs are appended to
+// per-query candidate chunks in global memory ([C][nq][kp], the layout the
+// merge kernel reads as C lists).  There are no per-query lists to maintain,
+// so the epilogue is a TMEM drain plus a max-reduction per 32 scores.  All
+// rows >= thr0 are kept; a query whose count exceeds C*kp overflows and the
+// host re-runs the batch on the list-keeping kernels (used only at high
+// thresholds, where candidates are rare: the engine's tau_sim).
+// Reference: `self._vecs @ arr` + the `>= min_similarity` mask of `_rank`
+// (pkg/src/semcache/index.py:101, :43), for B queries at once.
+// ===========================================================================
+
+constexpr int kGemmNQ = 256;      // queries per item (MMA N)
+constexpr int kGemmRows = 256;    // rows per item (MMA M, 128 per CTA)
+constexpr int kGemmThreads = 192;
+
+struct GemmParams {
+    int64_t nslots;
+    int nrt, nqt;        // row tiles (256), query tiles (256)
+    int kblocks;
+    int nq;              // live queries
+    int kp, chunks;      // candidate capacity per query = chunks * kp
+    float thr0;
+    int stages;
+    int tf32;
+    const uint32_t* valid;
+    uint32_t* cnt;       // [nq] pairs >= thr0 seen per query (may exceed capacity)
+    uint32_t* out_key;   // [chunks][nq][kp]
+    int32_t* out_slot;
+};
+
+__host__ __device__ inline size_t gemm_smem_bytes(int S) {
+    return static_cast<size_t>(S) * 2 * 128 * kUmmaKB + (2 * S + 4) * sizeof(uint64_t) + 16 + 1024;
+}
+
+__device__ __forceinline__ void gemm_append(const GemmParams& p, int q, uint32_t key, int32_t slot) {
+    const uint32_t at = atomicAdd(p.cnt + q, 1u);
+    const uint32_t cap = static_cast<uint32_t>(p.chunks * p.kp);
+    if (at < cap) {
+        const uint32_t c = at / p.kp, e = at - c * p.kp;
+        const size_t o = (static_cast<size_t>(c) * p.nq + q) * p.kp + e;
+        p.out_key[o] = key;
+        p.out_slot[o] = slot;
+    }
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
+                     const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages, nkb = p.kblocks;
+    constexpr size_t kStage = 128 * kUmmaKB;  // 16 KB: 128 rows (or queries) x 128 B of K
+    uint8_t* sa = smem;
+    uint8_t* sb = smem + S * kStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * S * kStage);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = static_cast<int>(cluster_ctarank());
+    const int pair = static_cast<int>(cluster_id_x());
+    const int npair = static_cast<int>(cluster_count_x());
+    const int nitems = p.nrt * p.nqt;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 8);  // 4 epilogue warps in each CTA (used on the leader)
+        }
+        fence_mbar_init();
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int kb_elems = p.tf32 ? kUmmaKB / 4 : kUmmaKB / 2;
+
+    if (warp == 4) {
+        // ---------------- TMA producers (both CTAs; the leader arms the barriers) ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
+            const uint64_t pol_q = l2_evict_last_policy();
+            uint64_t pol_rows;  // re-read by the other query tiles of the same row tile
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_rows));
+            int s = 0;
+            uint32_t ph = 0;
+            for (int w = pair; w < nitems; w += npair) {
+                const int t = w / p.nqt, g = w - (w / p.nqt) * p.nqt;
+                const int r0 = t * kGemmRows + rank * 128;
+                const int q0 = g * kGemmNQ + rank * 128;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(empty + s, ph ^ 1);
+                    if (rank == 0) mbar_arrive_expect_tx(full + s, 4u * static_cast<uint32_t>(kStage));
+                    tma_load_2d_pair(sa + s * kStage, &rmap, leader_addr(full + s), kb * kb_elems, r0, pol_rows);
+                    tma_load_2d_pair(sb + s * kStage, &qmap, leader_addr(full + s), kb * kb_elems, q0, pol_q);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer (leader only): D[256 rows, 256 queries] ----------------
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = umma_idesc(p.tf32, kGemmRows, kGemmNQ);
+            int s = 0;
+            uint32_t ph = 0;
+            int i = 0;
+            for (int w = pair; w < nitems; w += npair, ++i) {
+                const int acc = i & 1;
+                mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * kGemmNQ;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full + s, ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + s * kStage);
+                    const uint32_t b0 = smem_u32(sb + s * kStage);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ad = umma_smem_desc(a0 + kk * 32);
+                        const uint64_t bd = umma_smem_desc(b0 + kk * 32);
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        if (p.tf32)
+                            umma_tf32_pair(d, ad, bd, idesc, accum);
+                        else
+                            umma_f16_pair(d, ad, bd, idesc, accum);
+                    }
+                    umma_commit_pair(empty + s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit_pair(tfull + acc);
+            }
+        }
+    } else {
+        // ---------------- epilogue: thread = row of this CTA's half tile ----------------
+        const int tid = threadIdx.x;
+        const float thr0 = p.thr0;
+        int i = 0;
+        for (int w = pair; w < nitems; w += npair, ++i) {
+            const int acc = i & 1;
+            const int t = w / p.nqt, g = w - (w / p.nqt) * p.nqt;
+            const int64_t slot = static_cast<int64_t>(t) * kGemmRows + rank * 128 + tid;
+            const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
+            const bool live = ((vw >> (slot & 31)) & 1u) != 0;
+            const int qbase = g * kGemmNQ;
+            mbar_wait(tfull + acc, (i >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kGemmNQ / 32; c += 2) {
+                uint32_t r0[32], r1[32];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * kGemmNQ + c * 32;
+                SINE_TMEM_LD32(taddr, r0);
+                SINE_TMEM_LD32(taddr + 32, r1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    m0 = fmaxf(m0, __uint_as_float(r0[j]));
+                    m1 = fmaxf(m1, __uint_as_float(r1[j]));
+                }
+                if (live && m0 >= thr0) {  // rare: fully unrolled so the scores stay in registers
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float sc = __uint_as_float(r0[j]) + 0.0f;
+                        const int q = qbase + c * 32 + j;
+                        if (sc >= thr0 && q < p.nq) gemm_append(p, q, f32_key(sc), static_cast<int32_t>(slot));
+                    }
+                }
+                if (live && m1 >= thr0) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float sc = __uint_as_float(r1[j]) + 0.0f;
+                        const int q = qbase + c * 32 + 32 + j;
+                        if (sc >= thr0 && q < p.nq) gemm_append(p, q, f32_key(sc), static_cast<int32_t>(slot));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0)
+                    mbar_arrive(tempty + acc);
+                else
+                    mbar_arrive_leader(tempty + acc);
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// Per-query candidate counts -> the merge kernel's per-list counts, and the
+// number of queries whose candidates overflowed the chunk capacity.
+__global__ void gemm_finish_kernel(const uint32_t* cnt, int nq, int kp, int chunks, int32_t* out_n,
+                                   uint32_t* overflow) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint32_t n = cnt[q];
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t r = static_cast<int64_t>(n) - static_cast<int64_t>(c) * kp;
+        out_n[c * nq + q] = static_cast<int32_t>(r < 0 ? 0 : (r > kp ? kp : r));
+    }
+    if (n > static_cast<uint32_t>(chunks * kp)) atomicAdd(overflow, 1u);
+}
+
+}  // namespace sine

@@ -116,7 +116,7 @@ class GpuCosineIndex:
         return self._h
 
     def _mode(self, scan: str | None = None, rerank: bool | None = None, cuda_core: bool = False,
-              umma_v1: bool = False, cluster: bool = False, pair: bool = False) -> int:
+              umma_v1: bool = False, cluster: bool = False, pair: bool = False, gemm: bool | None = None) -> int:
         scan = scan or self.scan
         rerank = self.rerank if rerank is None else rerank
         m = N.SCAN_BF16 if scan == "bf16" else N.SCAN_F32
@@ -130,6 +130,8 @@ class GpuCosineIndex:
             m |= N.SCAN_CLUSTER
         if pair:
             m |= N.SCAN_PAIR
+        if gemm is not None:  # None: the library decides (large batches at high thresholds)
+            m |= N.SCAN_GEMM if gemm else N.SCAN_NO_GEMM
         return m | N.NO_NORM_CHECK
 
     # ------------------------------------------------------------ queries
@@ -195,7 +197,7 @@ class GpuCosineIndex:
 
     def query_batch(self, queries, k: int, min_similarity: float = -1.0, *, scan: str | None = None,
                     rerank: bool | None = None, check: bool = True, cuda_core: bool = False,
-                    umma_v1: bool = False, cluster: bool = False, pair: bool = False):
+                    umma_v1: bool = False, cluster: bool = False, pair: bool = False, gemm: bool | None = None):
         """B independent queries in one pass over the index.
 
         Returns (ids int64[B, k] padded with -1, sims float64[B, k],
@@ -203,7 +205,7 @@ class GpuCosineIndex:
         q = check_matrix(queries, self.dimension) if check else N.f64(queries)
         if k < 1:
             raise ValidationError("k must be >= 1")
-        return self._query(q, k, min_similarity, self._mode(scan, rerank, cuda_core, umma_v1, cluster, pair))
+        return self._query(q, k, min_similarity, self._mode(scan, rerank, cuda_core, umma_v1, cluster, pair, gemm))
 
     def _query(self, q: np.ndarray, k: int, min_similarity: float, mode: int):
         B = q.shape[0]
@@ -226,13 +228,13 @@ class GpuCosineIndex:
     def query_device(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                      counts_ptr: int, stream: int | None = None, *, scan: str | None = None,
                      rerank: bool | None = None, cuda_core: bool = False, umma_v1: bool = False,
-                     certify: bool = True, pair: bool = False) -> None:
+                     certify: bool = True, pair: bool = False, gemm: bool | None = None) -> None:
         """Device-pointer variant (torch tensors); enqueued on `stream`.
 
         With `certify` (default) the per-query exactness certificate is
         checked and failing queries are re-run on the fp32 scan; this
         synchronises the stream once per call."""
-        mode = self._mode(scan, rerank, cuda_core, umma_v1, pair=pair) | (N.CERTIFY if certify else 0)
+        mode = self._mode(scan, rerank, cuda_core, umma_v1, pair=pair, gemm=gemm) | (N.CERTIFY if certify else 0)
         N.check(self._lib.sine_query_device(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
                                             float(min_similarity), mode,
                                             ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
@@ -274,6 +276,13 @@ class GpuCosineIndex:
         """Queries the last (certified) call re-ran on the fp32 scan."""
         n = ctypes.c_int64()
         N.check(self._lib.sine_uncertified(self._h, ctypes.byref(n)))
+        return n.value
+
+    def gemm_overflows(self) -> int:
+        """Tiled-GEMM launches whose candidates overflowed (re-run on the
+        list-keeping kernels)."""
+        n = ctypes.c_int64()
+        N.check(self._lib.sine_gemm_overflows(self._h, ctypes.byref(n)))
         return n.value
 
     def kernel_launches(self) -> int:

@@ -379,3 +379,63 @@ def test_cta_pair_kernel_fp32_d768(pkg):
         for j in range(0, B, 7):
             want = ora.query(q[j], 10, ms)
             assert a[0][j, :a[2][j]].tolist() == [c.id for c in want]
+
+
+@pytest.mark.parametrize("d", [64, 384, 768])
+def test_tiled_gemm_matches_oracle(pkg, d):
+    """The large-batch tiled GEMM (256 x 256 CTA-pair tiles, all query tiles
+    in one launch) on ragged row and query tiles, with tombstones: ids
+    bit-exact and fp64 similarities (1e-12) vs the oracle, both scan modes."""
+    rng = np.random.default_rng(100 + d)
+    n, B = 20011, 700
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((B, d))
+    pick = rng.integers(0, n, B // 2)
+    q[: B // 2] = rows[pick] + (0.01 + 0.02 * rng.random((B // 2, 1))) * rng.standard_normal((B // 2, d))
+    q[B // 2: B // 2 + 20] = rows[pick[:20]]  # exact duplicates: ties with the stored row
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ids = np.arange(n) * 3 + 7
+    dead = rng.choice(n, 500, replace=False)
+    ora = O.OracleExactIndex(d)
+    keep = np.setdiff1d(np.arange(n), dead)
+    ora.bulk_load(ids[keep], rows[keep])
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(ids, rows)
+        idx.remove_batch(ids[dead[:100]])  # tombstones only (below the compaction trigger)
+        idx.remove_batch(ids[dead[100:]])
+        for bq, ms in ((B, 0.9), (300, 0.5)):
+            got = idx.query_batch(q[:bq], 10, ms, gemm=True)
+            assert idx.gemm_overflows() == 0
+            for j in range(bq):
+                want = ora.query(q[j], 10, ms)
+                assert got[0][j, :got[2][j]].tolist() == [c.id for c in want], (scan, bq, ms, j)
+                np.testing.assert_allclose(got[1][j, :got[2][j]], [c.similarity for c in want], atol=1e-12, rtol=0)
+
+
+def test_tiled_gemm_bf16_raw_and_overflow_fallback(pkg):
+    """bf16 without re-rank through the GEMM path stays within the 2e-2
+    bf16 tolerance; a low threshold overflows the per-query candidate
+    buffers and the batch is re-run on the list-keeping kernels (exact)."""
+    rng = np.random.default_rng(5)
+    n, d, B = 9000, 256, 520
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rows[rng.integers(0, n, B)] + 0.02 * rng.standard_normal((B, d))  # cos ~0.95
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    idx = pkg.GpuCosineIndex(d, scan="bf16")
+    idx.insert_batch(np.arange(n), rows)
+    ids, sims, counts = idx.query_batch(q, 5, 0.9, rerank=False, gemm=True)
+    for j in range(B):
+        want = ora.query(q[j], 5, 0.9)
+        assert counts[j] >= 1
+        assert abs(sims[j, 0] - want[0].similarity) < 2e-2
+    before = idx.gemm_overflows()
+    got = idx.query_batch(q, 5, -1.0, gemm=True)
+    assert idx.gemm_overflows() == before + 1
+    for j in range(0, B, 13):
+        want = ora.query(q[j], 5, -1.0)
+        assert got[0][j, :got[2][j]].tolist() == [c.id for c in want]
