@@ -201,7 +201,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    hbm_peak, _, peak_kind = peaks()
+    hbm_peak, tensor_peak, peak_kind = peaks()
 
     rows = make_rows(args.rows, DIM)
     lo, hi = rank * args.rows // world, (rank + 1) * args.rows // world
@@ -328,7 +328,7 @@ def run_ours(args):
 
     regimes = []
     if world == 1 and not args.no_regimes:
-        regimes = measure_regimes(idx, rows, torch, hbm_peak)
+        regimes = measure_regimes(idx, rows, torch, hbm_peak, tensor_peak)
     trace = None
     if world == 1 and not args.no_trace:
         trace = measure_trace(rows)
@@ -366,21 +366,21 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def measure_regimes(idx, rows, torch, hbm_peak):
+def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
     """Config B's three batch regimes x both scan modes (device timing)."""
     out = []
     stream = torch.cuda.current_stream().cuda_stream
     assert stream, "regimes must run on a non-default stream"
     cases = []
     for scan in ("fp32", "bf16"):
-        for b, reps in ((1, 20), (8, 10), (64, 5), (4096, 1)):
+        for b, reps in ((1, 20), (8, 10), (64, 5), (256, 5), (1024, 3), (4096, 3)):
             for tau in (TAU, -1.0):
-                if b == 4096 and tau == -1.0:
+                if b >= 256 and tau == -1.0:
                     continue
                 cases.append((scan, b, reps, tau, "auto"))
         cases.append((scan, 64, 5, TAU, "umma_v1"))
         cases.append((scan, 64, 3, TAU, "cuda_core"))
-        cases.append((scan, 4096, 1, TAU, "pair"))
+        cases.append((scan, 4096, 1, TAU, "pair"))  # the per-group HBM passes the GEMM replaces
     for scan, b, reps, tau, path in cases:
             if True:
                 qs = make_queries(rows, b, seed=100 + b)
@@ -391,7 +391,8 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                 cnt = torch.empty((b,), dtype=torch.int32, device="cuda")
                 run = lambda: idx.query_device(b, q.data_ptr(), K, tau, ids.data_ptr(), sims.data_ptr(),  # noqa
                                                cnt.data_ptr(), stream, scan=scan, cuda_core=path == "cuda_core",
-                                               umma_v1=path == "umma_v1", pair=path == "pair")
+                                               umma_v1=path == "umma_v1", pair=path == "pair",
+                                               gemm=False if path == "pair" else None)
                 run()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -404,10 +405,14 @@ def measure_regimes(idx, rows, torch, hbm_peak):
                 n = rows.shape[0]
                 byt = algorithmic_bytes(n, DIM, b, K, scan)
                 flops = 2.0 * n * DIM * b
+                # tensor peak: measured bf16 dense (MEASURED_PEAKS.json); kind::tf32
+                # issues half the bf16 K per instruction, so its peak is half
+                tpeak = tensor_peak * (1.0 if scan == "bf16" else 0.5)
                 out.append({"batch": b, "scan": scan, "min_similarity": tau, "path": path, "ms_per_batch": ms,
                             "lookups_per_s": b / (ms / 1e3),
                             "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
-                            "tflops": flops / (ms / 1e3) / 1e12})
+                            "tflops": flops / (ms / 1e3) / 1e12,
+                            "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak})
     return out
 
 
@@ -464,11 +469,19 @@ def measure_eviction(n, hbm_peak, cpu_sample=300_000):
     cnt = ctypes.c_int64()
     lib = idx._lib
     idx.set_timing(True)
-    # 1) TTL purge: expired ids ascending, tombstoned on the device
+    # 1) TTL purge: expired ids ascending (read-only passes warm the path and
+    # time the scan + ordered compaction), then the removing pass that also
+    # tombstones them on the device
+    optr = out.array.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    scan_t = []
+    for _ in range(4):
+        t0 = time.perf_counter()
+        Nat.check(lib.sine_expired(idx.handle, now, 0, optr, n, ctypes.byref(cnt)))
+        scan_t.append(time.perf_counter() - t0)
     t0 = time.perf_counter()
-    Nat.check(lib.sine_expired(idx.handle, now, 1, out.array.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n,
-                               ctypes.byref(cnt)))
+    Nat.check(lib.sine_expired(idx.handle, now, 1, optr, n, ctypes.byref(cnt)))
     exp_s = time.perf_counter() - t0
+    exp_scan_s = min(scan_t[1:])
     n_expired = cnt.value
     expired_ids = out.array[:n_expired].copy()
     # 2) the LCFU victim prefix over the live SEs (read-only: repeated for timing)
@@ -503,6 +516,7 @@ def measure_eviction(n, hbm_peak, cpu_sample=300_000):
                         f"now={now}",
             "expired": n_expired, "victims": n_victims, "parity_vs_oracle": parity,
             "select_ms_e2e": sel_s * 1e3, "select_ms_device": dev_ms, "expire_ms_e2e": exp_s * 1e3,
+            "expire_list_ms_e2e": exp_scan_s * 1e3,
             "evict_until_fits_ms": total_s * 1e3, "ses_per_s": n / total_s,
             "roofline": {"bound": "hbm", "bytes_per_se": bytes_per_se,
                          "achieved": n * bytes_per_se / (dev_ms / 1e3) / 1e9 if dev_ms else None,
