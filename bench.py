@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-evict", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--evict-rows", type=int, default=10_000_000)
+    ap.add_argument("--no-config-c", action="store_true")
+    ap.add_argument("--config-c-rows", type=int, default=10_000_000)
     return ap.parse_args()
 
 
@@ -277,9 +279,10 @@ def run_ours(args):
             idx.query_batch(qs[args.warmup + s_][j_:j_ + 1], K, TAU, cuda_core=True)
     scan_ms, scan_n = idx.timing_totals(0, reset=False)
     kernel_name = "scan_kernel"
+    gemm = b > (128 if args.scan == "bf16" else 64) and TAU >= 0.25  # the library's tiled-GEMM gate
     if scan_n == 0:  # the batch went through the tensor-core stage-1
         scan_ms, scan_n = idx.timing_totals(2, reset=False)
-        kernel_name = "umma_res_kernel"
+        kernel_name = "umma_gemm_kernel" if gemm else ("umma_pair_kernel" if b > 32 else "umma_res_kernel")
     merge_ms, merge_n = idx.timing_totals(1, reset=True)
     idx.set_timing(False)
     launches = idx.kernel_launches() - launches0
@@ -306,6 +309,13 @@ def run_ours(args):
                 "kernel": kernel_name, "kernel_ms": scan_avg_ms,
                 "scan_share_of_step": scan_ms / max(elapsed_ms, 1e-9),
                 "bytes_per_launch": bytes_per_launch, "frac_of_nominal_8tbs": achieved / 8000.0}
+    if gemm:  # tensor-bound regime: algorithmic flops per launch over the kernel time
+        tpeak = tensor_peak * (1.0 if args.scan == "bf16" else 0.5)  # kind::tf32 runs at half the bf16 rate
+        tf = 2.0 * shard_rows * DIM * q_per_launch / (scan_avg_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": tf, "peak": tpeak, "unit": "TFLOP/s", "frac": tf / tpeak,
+                    "traffic": None, "peak_kind": peak_kind, "kernel": kernel_name, "kernel_ms": scan_avg_ms,
+                    "scan_share_of_step": scan_ms / max(elapsed_ms, 1e-9),
+                    "flops_per_launch": 2.0 * shard_rows * DIM * q_per_launch}
 
     # e2e through the public API with pinned host buffers (H2D + D2H inside)
     e2e = None
@@ -337,6 +347,12 @@ def run_ours(args):
         del idx
         torch.cuda.empty_cache()
         eviction = measure_eviction(args.evict_rows, hbm_peak)
+    config_c = None
+    if world == 1 and not args.no_config_c:
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        config_c = measure_config_c(torch, hbm_peak, tensor_peak, args.config_c_rows)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -360,7 +376,7 @@ def run_ours(args):
                            "l2": "no flush: the index (>= 1.5 GB) exceeds the 126 MB L2"},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
                 "gpu_launches": int(launches), "uncertified_steps": uncertified,
-                "regimes": regimes, "eviction": eviction, "trace": trace}
+                "regimes": regimes, "eviction": eviction, "trace": trace, "config_c": config_c}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -413,6 +429,82 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                             "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
                             "tflops": flops / (ms / 1e3) / 1e12,
                             "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak})
+    return out
+
+
+# ------------------------------------------------ config C: 10M x 1024, k=20
+
+def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
+    """Config C's shard at P=1: all 10M SEs x d=1024 resident on ONE B200
+    (fp64 master 82 GB + fp32 41 GB + bf16 20.5 GB), generated on the device
+    (standard-normal rows normalised in float64, seed 7).  Stage-1 at B = 1,
+    64, 4096, tau = 0.9, device-timed; P = 2/4/8 shards are 1/P of these rows
+    (this pool has one GPU per box).  Spot check: every planted query's
+    source row is its top candidate."""
+    from paper_2509_17360_b200 import GpuCosineIndex
+
+    free, _ = torch.cuda.mem_get_info()
+    need = n * d * (8 + 4 + 2) + n * 64
+    store_f32 = free > need * 1.05
+    if free < n * d * (8 + 2) * 1.05:
+        return {"skipped": f"needs {n * d * 10 / 1e9:.0f} GB free, have {free / 1e9:.0f} GB"}
+    idx = GpuCosineIndex(d, scan="bf16", store_f32=store_f32, store_bf16=True, capacity=n)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    chunk = 250_000
+    t0 = time.perf_counter()
+    for i0 in range(0, n, chunk):
+        m = min(chunk, n - i0)
+        x = torch.randn((m, d), dtype=torch.float64, device="cuda", generator=g)
+        x /= x.norm(dim=1, keepdim=True)
+        idx.insert_device(np.arange(i0, i0 + m, dtype=np.int64) + 1, x.data_ptr())
+        del x
+    torch.cuda.synchronize()
+    load_s = time.perf_counter() - t0
+    rng = np.random.default_rng(9)
+    src = rng.choice(n, 2048, replace=False) + 1
+    base = idx.rows(src)
+    qs = rng.standard_normal((4096, d))
+    qs /= np.linalg.norm(qs, axis=1, keepdims=True)
+    for j in range(2048):  # even queries: planted near-duplicates, cos in [0.88, 0.99]
+        x = base[j]
+        gq = qs[2 * j] - (qs[2 * j] @ x) * x
+        gq /= np.linalg.norm(gq)
+        c = rng.uniform(0.88, 0.99)
+        qs[2 * j] = c * x + math.sqrt(1 - c * c) * gq
+        qs[2 * j] /= np.linalg.norm(qs[2 * j])
+    q = torch.from_numpy(qs).cuda()
+    ids = torch.empty((4096, k), dtype=torch.int64, device="cuda")
+    sims = torch.empty((4096, k), dtype=torch.float64, device="cuda")
+    cnt = torch.empty((4096,), dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    out = {"workload": f"config C at P=1: {n} SEs x d={d}, k={k}, tau={TAU}, rows generated on the device",
+           "rows": n, "dim": d, "k": k, "store_f32": store_f32, "load_s": load_s, "regimes": []}
+    cases = [("bf16", 1, 10), ("bf16", 64, 5), ("bf16", 4096, 2)]
+    if store_f32:
+        cases += [("fp32", 1, 10), ("fp32", 64, 5), ("fp32", 4096, 1)]
+    for scan, b, reps in cases:
+        run = lambda: idx.query_device(b, q.data_ptr(), k, TAU, ids.data_ptr(), sims.data_ptr(),  # noqa: E731
+                                       cnt.data_ptr(), stream, scan=scan, certify=False)
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        got = ids[:b, 0].cpu().numpy()
+        planted = np.arange(0, b, 2)
+        hit = float(np.mean(got[planted] == src[planted // 2])) if planted.size else None
+        flops = 2.0 * n * d * b
+        tpeak = tensor_peak * (1.0 if scan == "bf16" else 0.5)
+        out["regimes"].append({"batch": b, "scan": scan, "ms_per_batch": ms, "lookups_per_s": b / (ms / 1e3),
+                               "hbm_frac": algorithmic_bytes(n, d, b, k, scan) / (ms / 1e3) / 1e9 / hbm_peak,
+                               "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak,
+                               "planted_top1": hit})
+    del idx
+    torch.cuda.empty_cache()
     return out
 
 

@@ -101,7 +101,8 @@ int sine_reserve(sine_index_t *h, int64_t rows);
  * index was created with SINE_STORE_META. */
 int sine_insert(sine_index_t *h, int64_t n, const int64_t *ids, const double *rows,
                 const sine_meta_cols_t *meta, uint32_t flags);
-/* Same, rows already in device memory (bulk load). */
+/* Same, rows already in device memory (bulk load).  Waits for all prior
+ * work on the device first, so rows written on any stream are complete. */
 int sine_insert_device(sine_index_t *h, int64_t n, const int64_t *ids,
                        const double *rows_dev, const sine_meta_cols_t *meta,
                        uint32_t flags);

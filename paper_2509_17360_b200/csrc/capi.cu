@@ -1470,6 +1470,9 @@ int sine_insert_device(sine_index_t* h, int64_t n, const int64_t* ids, const dou
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
         check_new_ids(h, n, ids);
+        // the rows may come from any stream (e.g. a torch kernel that just
+        // wrote them): order the copy after all prior device work
+        CK(cudaDeviceSynchronize());
         append(h, n, ids, rows_dev, true, meta);
     });
 }

@@ -439,3 +439,26 @@ def test_tiled_gemm_bf16_raw_and_overflow_fallback(pkg):
     for j in range(0, B, 13):
         want = ora.query(q[j], 5, -1.0)
         assert got[0][j, :got[2][j]].tolist() == [c.id for c in want]
+
+
+def test_insert_device_orders_after_producer_stream(pkg):
+    """Rows produced by a torch kernel on another stream and handed to
+    insert_device right away are read only after that kernel finished."""
+    torch = pytest.importorskip("torch")
+    d, n = 512, 200_000
+    idx = pkg.GpuCosineIndex(d, scan="bf16", store_f32=True, store_bf16=True, capacity=2 * n)
+    side = torch.cuda.Stream()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    kept = []
+    with torch.cuda.stream(side):
+        for c in range(2):
+            x = torch.randn((n, d), dtype=torch.float64, device="cuda", generator=g)
+            for _ in range(20):  # keep the producer stream busy
+                x = x * 1.0000001
+            x /= x.norm(dim=1, keepdim=True)
+            idx.insert_device(np.arange(c * n, (c + 1) * n), x.data_ptr())
+            kept.append(x)
+    torch.cuda.synchronize()
+    X = torch.cat(kept).cpu().numpy()
+    pick = np.random.default_rng(0).choice(2 * n, 500, replace=False)
+    np.testing.assert_array_equal(idx.rows(pick), X[pick])
