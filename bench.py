@@ -440,7 +440,7 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
     (standard-normal rows normalised in float64, seed 7).  Stage-1 at B = 1,
     64, 4096, tau = 0.9, device-timed; P = 2/4/8 shards are 1/P of these rows
     (this pool has one GPU per box).  Spot check: every planted query's
-    source row is its top candidate."""
+    source row is its top candidate exactly when cos >= tau."""
     from paper_2509_17360_b200 import GpuCosineIndex
 
     free, _ = torch.cuda.mem_get_info()
@@ -465,6 +465,7 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
     base = idx.rows(src)
     qs = rng.standard_normal((4096, d))
     qs /= np.linalg.norm(qs, axis=1, keepdims=True)
+    cos = np.zeros(2048)
     for j in range(2048):  # even queries: planted near-duplicates, cos in [0.88, 0.99]
         x = base[j]
         gq = qs[2 * j] - (qs[2 * j] @ x) * x
@@ -472,6 +473,7 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
         c = rng.uniform(0.88, 0.99)
         qs[2 * j] = c * x + math.sqrt(1 - c * c) * gq
         qs[2 * j] /= np.linalg.norm(qs[2 * j])
+        cos[j] = float(qs[2 * j] @ x)
     q = torch.from_numpy(qs).cuda()
     ids = torch.empty((4096, k), dtype=torch.int64, device="cuda")
     sims = torch.empty((4096, k), dtype=torch.float64, device="cuda")
@@ -496,13 +498,16 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
         ms = e0.elapsed_time(e1) / reps
         got = ids[:b, 0].cpu().numpy()
         planted = np.arange(0, b, 2)
-        hit = float(np.mean(got[planted] == src[planted // 2])) if planted.size else None
+        # a planted query must return its source row iff cos >= tau (random
+        # rows sit near cos 0 at d=1024); outside the 1e-5 window of tau
+        sure = np.abs(cos[planted // 2] - TAU) > 1e-5
+        hit = float(np.mean((got[planted] == src[planted // 2])[sure] == (cos[planted // 2] >= TAU)[sure]))
         flops = 2.0 * n * d * b
         tpeak = tensor_peak * (1.0 if scan == "bf16" else 0.5)
         out["regimes"].append({"batch": b, "scan": scan, "ms_per_batch": ms, "lookups_per_s": b / (ms / 1e3),
                                "hbm_frac": algorithmic_bytes(n, d, b, k, scan) / (ms / 1e3) / 1e9 / hbm_peak,
                                "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak,
-                               "planted_top1": hit})
+                               "planted_hit_exact": hit})
     del idx
     torch.cuda.empty_cache()
     return out

@@ -914,11 +914,15 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         const int64_t passes2 = nq2 ? (B + nq2 - 1) / nq2 : INT64_MAX;
         const int64_t passes1 = (B + kUmmaM - 1) / kUmmaM;
         const bool force_v1 = (mode & 0x400u) != 0;
-        // large batches at a high admission floor: one tiled GEMM launch
-        // (256 x 256 pair tiles, N = 256 per MMA) instead of B/128 HBM passes
-        // (measured, 1M x 768, tau 0.9: bf16 B=256 0.40 ms vs 0.84 ms in two
-        // 128-query pair passes; fp32 B=256 0.70 vs 1.65 ms)
-        const int64_t per_pass = bf16 ? 128 : 64;  // queries per pair-kernel HBM pass
+        // queries per HBM pass of the list-keeping kernels: the resident
+        // group (nq2 per CTA) or the CTA pair (2 x pair_nqh, half per CTA)
+        const int pair_nqh = 64 * row_bytes <= 96 * 1024 ? 64 : (32 * row_bytes <= 96 * 1024 ? 32 : 0);
+        const int64_t per_pass = std::max<int64_t>(nq2, 2 * pair_nqh);
+        // larger batches at a high admission floor: one tiled GEMM launch
+        // (256 x 256 pair tiles, N = 256 per MMA) instead of B / per_pass
+        // HBM passes; up to 256 queries it costs about one HBM pass (measured,
+        // 1M x 768, tau 0.9: bf16 B=256 0.39 ms vs 0.84 ms in two 128-query
+        // pair passes; fp32 B=256 0.71 vs 1.65 ms)
         const bool gemm_auto = !(mode & SINE_SCAN_NO_GEMM) && !force_v1 && B > per_pass && thr0 >= 0.25f &&
                                !(mode & (SINE_SCAN_PAIR | SINE_SCAN_CLUSTER));
         if ((mode & SINE_SCAN_GEMM) || gemm_auto) {
@@ -931,10 +935,9 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         // cluster-multicast variant does not lower the per-query cost (the
         // L2->SM fan-out, not HBM, binds), so it is opt-in.
         const bool res = nq2 && (bf16 || B <= nq2);
-        // fp32 rows, 32 < B: a CTA pair keeps 64 queries per HBM pass
-        const bool pair_fits = 32 * row_bytes <= 96 * 1024;
-        const bool pair_auto = (!bf16 && nq2 == 32 && B > nq2 && B <= 64) ||
-                               (bf16 && nq2 == 64 && B > 64 && 64 * row_bytes <= 96 * 1024);
+        // nq2 < B <= 2 x pair_nqh: one CTA-pair pass instead of two resident passes
+        const bool pair_fits = pair_nqh > 0;
+        const bool pair_auto = pair_fits && B > nq2 && B <= 2 * pair_nqh;
         if (!force_v1 && pair_fits && !(mode & SINE_SCAN_CLUSTER) && ((mode & SINE_SCAN_PAIR) || pair_auto)) {
             umma_pair_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st);
             return;
