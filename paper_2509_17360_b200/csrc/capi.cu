@@ -178,7 +178,10 @@ struct sine_index {
     DevBuf<uint32_t> gcnt;          // tiled GEMM: candidates per query + overflow counter
     int64_t gemm_overflows = 0;     // GEMM launches re-run on the list-keeping kernels
     HostBuf<unsigned long long> sel_h;  // counter + kand + kor
-    DevBuf<SelectState> st;
+    DevBuf<SelectState> st, st1;       // selection state; st1 = after pass 1 (the record prefix)
+    DevBuf<uint64_t> rkeys;            // eviction candidate records: keys [n][3]
+    DevBuf<int64_t> rsize, dcount;     // record sizes; device counters
+    DevBuf<int32_t> rslot;             // record -> slot
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
     HostBuf<SelectState> st_h;
     HostBuf<unsigned long long> n_h;
@@ -1225,28 +1228,10 @@ struct KeyDecomposer {
     }
 };
 
-// Ordered collection of the slots matching the selection state (mode 0:
-// key prefix <= T, mode 1: == T).  Returns the count (one host sync).
-int64_t collect_ordered(sine_index* h, const EvictCols& cols, int mode, uint64_t* out_k, int32_t* out_slot,
-                        unsigned long long* kand, unsigned long long* kor, int64_t cap) {
-    cudaStream_t st = h->stream;
-    const int nb = static_cast<int>((h->nslots + kColChunk - 1) / kColChunk);
-    h->scratch_i32.ensure(nb);
-    h->exp_off.ensure(nb + 1);
-    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st.p, mode, h->scratch_i32.p);
-    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
-    int64_t total = 0;
-    CK(cudaMemcpyAsync(&total, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (total > cap) fail(SINE_ECUDA, "collection exceeds its buffer");
-    collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st.p, mode, h->exp_off.p, out_k, out_slot, kand, kor);
-    h->launches += 3;
-    CK(cudaGetLastError());
-    return total;
-}
-
-void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, std::vector<int64_t>& out) {
-    out.clear();
+// Victims are written straight into the caller's buffer (pinned or pageable).
+void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, int64_t* out, int64_t cap,
+                         int64_t* nout) {
+    *nout = 0;
     if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata (SINE_STORE_META)");
     if (excess <= 0 || h->nlive == 0) return;
     cudaStream_t st = h->stream;
@@ -1273,50 +1258,85 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     CK(cudaMemcpyAsync(h->st.p, h->st_h.p, sizeof(SelectState), cudaMemcpyHostToDevice, st));
 
     const EvictCols cols = evict_cols(h);
-    // shrink the working set to the prefix-matching slots once they are at
-    // most ~60% of the live ones: later passes then gather only those
-    const int64_t cand_max = std::max<int64_t>(1 << 20, h->nlive * 6 / 10);
-    const int32_t* cand = nullptr;
-    int64_t ncand = 0;
-    bool first = true;
     const int grid_all = grid_for(h->nslots, 256, h->num_sms);
-    for (int pass = 0; pass < 25; ++pass) {
-        HistArgs a{};
-        a.c = cols;
-        a.policy = policy;
-        a.now = now;
-        a.cand = cand;
-        a.ncand = ncand;
-        a.k1 = h->k1.p;
-        a.first = first ? 1 : 0;
-        a.st = h->st.p;
-        a.hw = hw, a.hc = hc, a.hand = hand, a.hor = hor;
-        const int g = cand ? grid_for(ncand, 256, h->num_sms) : grid_all;
-        evict_hist_kernel<<<g, 256, 0, st>>>(a);
-        evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, first ? 1 : 0);
-        h->launches += 2;
+    const int nb = static_cast<int>((h->nslots + kColChunk - 1) / kColChunk);
+    h->scratch_i32.ensure(nb);
+    h->exp_off.ensure(nb + 1);
+    h->st1.ensure(1);
+    h->dcount.ensure(4);
+    h->n_h.ensure(2);
+    // pass 1 over every live slot: primary keys (cached) + the first digit
+    HistArgs a{};
+    a.c = cols;
+    a.policy = policy;
+    a.now = now;
+    a.k1 = h->k1.p;
+    a.first = 1;
+    a.st = h->st.p;
+    a.hw = hw, a.hc = hc, a.hand = hand, a.hor = hor;
+    evict_hist_kernel<<<grid_all, 256, 0, st>>>(a);
+    evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 1);
+    // the slots of the chosen prefix bucket -> dense records (slot order):
+    // later passes stream 32 B per candidate instead of gathering columns
+    CK(cudaMemcpyAsync(h->st1.p, h->st.p, sizeof(SelectState), cudaMemcpyDeviceToDevice, st));
+    h->rkeys.ensure(3 * std::max<int64_t>(h->nlive, 1));
+    h->rsize.ensure(std::max<int64_t>(h->nlive, 1));
+    h->rslot.ensure(std::max<int64_t>(h->nlive, 1));
+    int64_t* nrec = h->dcount.p;      // records
+    int64_t* nbelow = h->dcount.p + 1;  // victims below the record prefix
+    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->scratch_i32.p);
+    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
+    collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->exp_off.p, h->rkeys.p, h->rslot.p, nullptr,
+                                             nullptr, h->rsize.p);
+    CK(cudaMemcpyAsync(nrec, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    h->launches += 5;
+    CK(cudaGetLastError());
+    // refinement passes over the records, enqueued four at a time (a pass
+    // after `done` returns at once); one host check per group
+    HistArgs r = a;
+    r.first = 0;
+    r.rk = h->rkeys.p;
+    r.rsz = h->rsize.p;
+    r.rn = nrec;
+    const int grid_rec = grid_for(h->nlive, 256, h->num_sms);
+    for (int pass = 1; pass < 25; pass += 4) {
+        for (int j = 0; j < 4; ++j) {
+            evict_hist_kernel<<<grid_rec, 256, 0, st>>>(r);
+            evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 0);
+        }
+        h->launches += 8;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->st_h.p, h->st.p, sizeof(SelectState), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        first = false;
-        const SelectState s = *h->st_h.p;
-        if (s.done) break;
-        if (!cand && s.count <= cand_max) {
-            h->cand.ensure(s.count);
-            ncand = collect_ordered(h, cols, 1, nullptr, h->cand.p, nullptr, nullptr, s.count);
-            cand = h->cand.p;
-        }
+        if (h->st_h.p->done) break;
     }
-    // collect the victims (key prefix <= T) with the AND / OR of their keys
-    const int64_t vmax = h->nlive;
+    // victims = live slots below the record prefix (slot order), then the
+    // records with key <= T (slot order): equal (primary, created_at) keys
+    // fall in the same part, so the stable sort below keeps id order
     CK(cudaMemsetAsync(kand, 0xff, 3 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(kor, 0, 3 * sizeof(unsigned long long), st));
-    h->vkeys.ensure(3 * std::max<int64_t>(vmax, 1));
-    h->vslots.ensure(std::max<int64_t>(vmax, 1));
-    const int64_t V = collect_ordered(h, cols, 0, h->vkeys.p, h->vslots.p, kand, kor, vmax);
-    (void)counter;
+    h->vkeys.ensure(3 * std::max<int64_t>(h->nlive, 1));
+    h->vslots.ensure(std::max<int64_t>(h->nlive, 1));
+    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->scratch_i32.p);
+    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
+    collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
+                                             kor);
+    CK(cudaMemcpyAsync(nbelow, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    const int nbr = static_cast<int>((h->nlive + kColChunk - 1) / kColChunk);
+    h->scratch_i32.ensure(std::max(nb, nbr));
+    h->exp_off.ensure(std::max(nb, nbr) + 1);
+    collect_count_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->scratch_i32.p, h->rkeys.p, nrec);
+    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nbr, h->exp_off.p);
+    collect_write_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
+                                              kor, nullptr, h->rkeys.p, nrec, h->rslot.p, nbelow);
+    h->launches += 6;
+    CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->sel_h.p + 1, kand, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->n_h.p, nbelow, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->n_h.p + 1, h->exp_off.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    const int64_t V = static_cast<int64_t>(h->n_h.p[0]) + static_cast<int64_t>(h->n_h.p[1]);
+    (void)counter;
     // bytes of the composite key that vary over the victims; with slot order
     // == id order the id bytes are left to the (stable) sort's input order
     const bool skip_id = h->ids_ascending;
@@ -1359,10 +1379,11 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         h->launches += 3;
         CK(cudaGetLastError());
     }
-    out.resize(V);
-    CK(cudaMemcpyAsync(out.data(), h->vids.p, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     record(h, 4, st);
+    if (V > cap) fail(SINE_EINVAL, "output buffer too small for the victim list");
+    CK(cudaMemcpyAsync(out, h->vids.p, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    *nout = V;
     if (h->timing) CK(cudaEventElapsedTime(&h->t_evict, h->ev[3], h->ev[4]));
 }
 
@@ -1746,10 +1767,11 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
         ++h->launches;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out, h->vids.p, total * 8, cudaMemcpyDeviceToHost, h->stream));
-        std::vector<int32_t> slots;
+        int32_t* slots = nullptr;  // pinned staging: the host tables drop these slots
         if (remove) {
-            slots.resize(total);
-            CK(cudaMemcpyAsync(slots.data(), h->vslots.p, total * 4, cudaMemcpyDeviceToHost, h->stream));
+            h->cnt_h.ensure(total);
+            slots = h->cnt_h.p;
+            CK(cudaMemcpyAsync(slots, h->vslots.p, total * 4, cudaMemcpyDeviceToHost, h->stream));
         }
         CK(cudaStreamSynchronize(h->stream));
         if (!h->ids_ascending) std::sort(out, out + total);
@@ -1759,7 +1781,8 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
             ++h->launches;
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(h->stream));
-            for (int32_t sl : slots) {
+            for (int64_t i = 0; i < total; ++i) {
+                const int32_t sl = slots[i];
                 if (!h->ids_ascending) h->pos.erase(h->ids_h[sl]);
                 h->live_h[sl] = 0;
             }
@@ -1776,11 +1799,7 @@ int sine_select_victims(sine_index_t* h, int policy, double now, int64_t excess,
         if (policy < 0 || policy > 2) fail(SINE_EINVAL, "unknown eviction policy");
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
-        std::vector<int64_t> v;
-        select_victims_impl(h, policy, now, excess, v);
-        *n = static_cast<int64_t>(v.size());
-        if (*n > cap) fail(SINE_EINVAL, "output buffer too small for the victim list");
-        std::copy(v.begin(), v.end(), out);
+        select_victims_impl(h, policy, now, excess, out, cap, n);
     });
 }
 

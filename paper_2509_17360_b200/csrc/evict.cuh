@@ -81,21 +81,38 @@ struct HistArgs {
     uint64_t* k1;          // cached primary keys [nslots]
     int first;             // compute (and cache) primary keys
     const SelectState* st;
+    // record mode (rk != nullptr): the candidates were compacted into dense
+    // records -- keys [n][3] + sizes [n], n = *rn on the device -- so a pass
+    // streams 32 B per candidate instead of gathering four columns by slot
+    const uint64_t* rk;
+    const int64_t* rsz;
+    const int64_t* rn;
     unsigned long long* hw;   // [256] weights
     unsigned long long* hc;   // [256] counts
     unsigned long long* hand; // [3]
     unsigned long long* hor;  // [3]
 };
 
+// 64-bit weight sum in shared memory from native 32-bit atomics (a 64-bit
+// shared atomicAdd compiles to a CAS spin loop): low word + carries.
+__device__ __forceinline__ void smem_add64(uint32_t* lo, uint32_t* hi, uint64_t v) {
+    const uint32_t l = static_cast<uint32_t>(v);
+    const uint32_t old = atomicAdd(lo, l);
+    const uint32_t h = static_cast<uint32_t>(v >> 32) + (old + l < old ? 1u : 0u);
+    if (h) atomicAdd(hi, h);
+}
+
 __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
-    __shared__ unsigned long long sw[256], sc[256];
-    sw[threadIdx.x] = 0;
+    __shared__ uint32_t swl[256], swh[256], sc[256];
+    if (a.st->done) return;  // passes are enqueued ahead of the host's done check
+    swl[threadIdx.x] = 0;
+    swh[threadIdx.x] = 0;
     sc[threadIdx.x] = 0;
     __syncthreads();
     const int nd = a.st->ndigits;
     uint64_t pre[3] = {a.st->prefix[0], a.st->prefix[1], a.st->prefix[2]};
     uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
-    const int64_t n = a.cand ? a.ncand : a.c.nslots;
+    const int64_t n = a.rk ? *a.rn : (a.cand ? a.ncand : a.c.nslots);
     const int lane = threadIdx.x & 31;
     const int64_t stride = 256ll * gridDim.x;
     // warp-uniform trip count so the whole warp takes part in the aggregation
@@ -104,7 +121,19 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
         bool act = false;
         uint32_t dg = 0;
         uint64_t sz = 0;
-        if (i < n) {
+        if (i < n && a.rk) {
+            const uint64_t k[3] = {a.rk[3 * i], a.rk[3 * i + 1], a.rk[3 * i + 2]};
+            if (prefix_cmp(k, pre, nd) == 0) {
+                act = true;
+                dg = key_digit(k, nd);
+                sz = static_cast<uint64_t>(a.rsz[i]);
+#pragma unroll
+                for (int w = 0; w < 3; ++w) {
+                    vand[w] &= k[w];
+                    vor[w] |= k[w];
+                }
+            }
+        } else if (i < n) {
             const int64_t s = a.cand ? a.cand[i] : i;
             if (a.cand || valid_bit(a.c.valid, s)) {
                 uint64_t k[3];
@@ -114,16 +143,19 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
                 } else {
                     k[0] = a.k1[s];
                 }
-                k[1] = f64_key(a.c.created[s]);
-                k[2] = i64_key(a.c.ids[s]);
+                // digits inside the primary word need only k[0]; the other
+                // words are then reported as varying (a conservative AND/OR)
+                const bool rest = nd >= 8;
+                k[1] = rest ? f64_key(a.c.created[s]) : 0ull;
+                k[2] = rest ? i64_key(a.c.ids[s]) : 0ull;
                 if (prefix_cmp(k, pre, nd) == 0) {
                     act = true;
                     dg = key_digit(k, nd);
                     sz = static_cast<uint64_t>(a.c.size[s]);
 #pragma unroll
                     for (int w = 0; w < 3; ++w) {
-                        vand[w] &= k[w];
-                        vor[w] |= k[w];
+                        vand[w] &= rest || w == 0 ? k[w] : 0ull;
+                        vor[w] |= rest || w == 0 ? k[w] : ~0ull;
                     }
                 }
             }
@@ -136,8 +168,8 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
         const bool group_leader = act && (__ffs(peers) - 1) == lane;
         if (__popc(__ballot_sync(0xffffffffu, group_leader)) > 4) {
             if (act) {
-                atomicAdd(&sw[dg], static_cast<unsigned long long>(sz));
-                atomicAdd(&sc[dg], 1ull);
+                smem_add64(&swl[dg], &swh[dg], sz);
+                atomicAdd(&sc[dg], 1u);
             }
             rem = 0;
         }
@@ -150,8 +182,8 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == leader) {
-                atomicAdd(&sw[ldg], v);
-                atomicAdd(&sc[ldg], static_cast<unsigned long long>(__popc(grp)));
+                smem_add64(&swl[ldg], &swh[ldg], v);
+                atomicAdd(&sc[ldg], static_cast<uint32_t>(__popc(grp)));
             }
             rem &= ~grp;
         }
@@ -164,17 +196,28 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
             vor[w] |= __shfl_xor_sync(0xffffffffu, vor[w], o);
         }
     }
-    if ((threadIdx.x & 31) == 0) {
+    // block-level AND/OR first: one global atomic per word per block
+    __shared__ unsigned long long band[3], bor[3];
+    if (threadIdx.x < 3) {
+        band[threadIdx.x] = ~0ull;
+        bor[threadIdx.x] = 0ull;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && (vor[0] | vor[1] | vor[2] | ~vand[0] | ~vand[1] | ~vand[2])) {
 #pragma unroll
         for (int w = 0; w < 3; ++w) {
-            atomicAnd(a.hand + w, static_cast<unsigned long long>(vand[w]));
-            atomicOr(a.hor + w, static_cast<unsigned long long>(vor[w]));
+            atomicAnd(band + w, static_cast<unsigned long long>(vand[w]));
+            atomicOr(bor + w, static_cast<unsigned long long>(vor[w]));
         }
     }
     __syncthreads();
+    if (threadIdx.x < 3 && (bor[0] | bor[1] | bor[2] | ~band[0] | ~band[1] | ~band[2])) {
+        atomicAnd(a.hand + threadIdx.x, band[threadIdx.x]);
+        atomicOr(a.hor + threadIdx.x, bor[threadIdx.x]);
+    }
     if (sc[threadIdx.x]) {
-        atomicAdd(a.hw + threadIdx.x, sw[threadIdx.x]);
-        atomicAdd(a.hc + threadIdx.x, sc[threadIdx.x]);
+        atomicAdd(a.hw + threadIdx.x, (static_cast<unsigned long long>(swh[threadIdx.x]) << 32) | swl[threadIdx.x]);
+        atomicAdd(a.hc + threadIdx.x, static_cast<unsigned long long>(sc[threadIdx.x]));
     }
 }
 
@@ -187,6 +230,7 @@ __global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsign
     __shared__ int chosen;
     __shared__ unsigned long long before_w;
     const int t = threadIdx.x;
+    if (st->done) return;
     cw[t] = hw[t];
     if (t == 0) chosen = -1;
     __syncthreads();
@@ -243,110 +287,47 @@ __global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsign
     }
 }
 
-struct CollectArgs {
-    EvictCols c;
-    const uint64_t* k1;
-    const SelectState* st;
-    const int32_t* cand;  // nullptr: all slots
-    int64_t ncand;
-    int mode;             // 0: victims (prefix <=), 1: candidates (prefix ==)
-    uint64_t* out_k;      // [cap][3] (victims) or unused
-    int32_t* out_slot;    // [cap]
-    unsigned long long* out_n;
-    int64_t cap;
-    unsigned long long* kand;  // mode 0: AND / OR of the victims' keys (nullable)
-    unsigned long long* kor;
-};
-
-__global__ void __launch_bounds__(256) evict_collect_kernel(const CollectArgs a) {
-    const int nd = a.st->ndigits;
-    const bool all = a.st->done == 2;
-    const uint64_t pre[3] = {a.st->prefix[0], a.st->prefix[1], a.st->prefix[2]};
-    const int64_t n = a.cand ? a.ncand : a.c.nslots;
-    const int lane = threadIdx.x & 31;
-    uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
-    for (int64_t i0 = blockIdx.x * 256ll + (threadIdx.x & ~31); i0 < n; i0 += 256ll * gridDim.x) {
-        const int64_t i = i0 + lane;
-        bool take = false;
-        int64_t s = 0;
-        uint64_t k[3] = {0, 0, 0};
-        if (i < n) {
-            s = a.cand ? a.cand[i] : i;
-            if (a.cand || valid_bit(a.c.valid, s)) {
-                k[0] = a.k1[s];
-                k[1] = f64_key(a.c.created[s]);
-                k[2] = i64_key(a.c.ids[s]);
-                const int cmp = all ? -1 : prefix_cmp(k, pre, nd);
-                take = a.mode == 0 ? cmp <= 0 : cmp == 0;
-            }
-        }
-        // one global atomic per warp for the output position
-        const uint32_t m = __ballot_sync(0xffffffffu, take);
-        if (!m) continue;
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.out_n, static_cast<unsigned long long>(__popc(m)));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (!take) continue;
-        const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
-        if (static_cast<int64_t>(at) < a.cap) {
-            a.out_slot[at] = static_cast<int32_t>(s);
-            if (a.mode == 0) {
-                a.out_k[3 * at] = k[0];
-                a.out_k[3 * at + 1] = k[1];
-                a.out_k[3 * at + 2] = k[2];
-#pragma unroll
-                for (int w = 0; w < 3; ++w) {
-                    vand[w] &= k[w];
-                    vor[w] |= k[w];
-                }
-            }
-        }
-    }
-    if (a.mode == 0 && a.kand) {
-#pragma unroll
-        for (int w = 0; w < 3; ++w) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                vand[w] &= __shfl_xor_sync(0xffffffffu, vand[w], o);
-                vor[w] |= __shfl_xor_sync(0xffffffffu, vor[w], o);
-            }
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int w = 0; w < 3; ++w) {
-                atomicAnd(a.kand + w, static_cast<unsigned long long>(vand[w]));
-                atomicOr(a.kor + w, static_cast<unsigned long long>(vor[w]));
-            }
-        }
-    }
-}
-
-// ---- ordered (atomic-free) collection: count per 4096-slot chunk, scan,
-// write.  Same predicate as evict_collect_kernel; output in slot order.
+// ---- ordered (atomic-free) collection: count per 4096-entry chunk, scan,
+// write; output in source order (slots, or records that are in slot order).
 
 struct CollectPred {
     EvictCols c;
     const uint64_t* k1;
+    const uint64_t* rk;  // record source (index = record) instead of slots
     int nd;
     int all;
-    int mode;  // 0: prefix <= T (victims), 1: prefix == T (candidates)
+    int mode;  // 0: prefix <= T (victims), 1: prefix == T (candidates), 2: prefix < T
     uint64_t pre[3];
 
     __device__ __forceinline__ bool operator()(int64_t s, uint64_t* k) const {
-        if (!valid_bit(c.valid, s)) return false;
-        k[0] = k1[s];
-        k[1] = f64_key(c.created[s]);
-        k[2] = i64_key(c.ids[s]);
+        if (rk) {
+            k[0] = rk[3 * s], k[1] = rk[3 * s + 1], k[2] = rk[3 * s + 2];
+        } else {
+            if (!valid_bit(c.valid, s)) return false;
+            k[0] = k1[s];
+            if (nd <= 8 && !all) {  // the first word decides; the rest only when taken
+                const int cmp = prefix_cmp(k, pre, nd);
+                const bool take = mode == 0 ? cmp <= 0 : (mode == 1 ? cmp == 0 : cmp < 0);
+                if (take) {
+                    k[1] = f64_key(c.created[s]);
+                    k[2] = i64_key(c.ids[s]);
+                }
+                return take;
+            }
+            k[1] = f64_key(c.created[s]);
+            k[2] = i64_key(c.ids[s]);
+        }
         const int cmp = all ? -1 : prefix_cmp(k, pre, nd);
-        return mode == 0 ? cmp <= 0 : cmp == 0;
+        return mode == 0 ? cmp <= 0 : (mode == 1 ? cmp == 0 : cmp < 0);
     }
 };
 
 __device__ __forceinline__ CollectPred make_pred(const EvictCols& c, const uint64_t* k1, const SelectState* st,
-                                                 int mode) {
+                                                 int mode, const uint64_t* rk = nullptr) {
     CollectPred p;
     p.c = c;
     p.k1 = k1;
+    p.rk = rk;
     p.nd = st->ndigits;
     p.all = st->done == 2;
     p.mode = mode;
@@ -358,12 +339,15 @@ __device__ __forceinline__ CollectPred make_pred(const EvictCols& c, const uint6
 
 constexpr int kColChunk = 4096;  // slots per block; 16 per thread
 
+// Source: slots [0, nslots), or records [0, *rn) when rk != nullptr.
 __global__ void __launch_bounds__(256) collect_count_kernel(EvictCols c, const uint64_t* k1, const SelectState* st,
-                                                            int mode, int32_t* counts) {
+                                                            int mode, int32_t* counts, const uint64_t* rk = nullptr,
+                                                            const int64_t* rn = nullptr) {
     __shared__ int32_t wsum[8];
-    const CollectPred pred = make_pred(c, k1, st, mode);
+    const CollectPred pred = make_pred(c, k1, st, mode, rk);
+    const int64_t n = rk ? *rn : c.nslots;
     const int64_t b = static_cast<int64_t>(blockIdx.x) * kColChunk;
-    const int64_t e = min(b + kColChunk, c.nslots);
+    const int64_t e = min(b + kColChunk, n);
     int32_t cnt = 0;
     uint64_t k[3];
     for (int64_t i = b + threadIdx.x; i < e; i += 256) cnt += pred(i, k) ? 1 : 0;
@@ -377,52 +361,67 @@ __global__ void __launch_bounds__(256) collect_count_kernel(EvictCols c, const u
     }
 }
 
+// out_k / out_size nullable; with a record source, rslot maps record ->
+// slot; `base` (device, nullable) offsets the output (appending after an
+// earlier collection).
 __global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const uint64_t* k1, const SelectState* st,
                                                             int mode, const int64_t* offsets, uint64_t* out_k,
                                                             int32_t* out_slot, unsigned long long* kand,
-                                                            unsigned long long* kor) {
+                                                            unsigned long long* kor, int64_t* out_size = nullptr,
+                                                            const uint64_t* rk = nullptr, const int64_t* rn = nullptr,
+                                                            const int32_t* rslot = nullptr,
+                                                            const int64_t* base = nullptr) {
     __shared__ int32_t wtot[8];
-    const CollectPred pred = make_pred(c, k1, st, mode);
+    const CollectPred pred = make_pred(c, k1, st, mode, rk);
+    const int64_t n = rk ? *rn : c.nslots;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kColChunk + threadIdx.x * 16;
-    uint32_t bits = 0;
+    // warp w owns entries [block*4096 + 512w, +512): 16 coalesced rounds of
+    // 32 consecutive entries; output order = entry order
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * kColChunk + warp * 512;
+    uint32_t m[16];
+    int32_t cnt = 0;
     uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
     uint64_t k[3];
-#pragma unroll 4
+#pragma unroll
     for (int j = 0; j < 16; ++j) {
-        const int64_t i = s0 + j;
-        if (i < c.nslots && pred(i, k)) {
-            bits |= 1u << j;
+        const int64_t i = w0 + j * 32 + lane;
+        const bool take = i < n && pred(i, k);
+        if (take) {
 #pragma unroll
             for (int w = 0; w < 3; ++w) {
                 vand[w] &= k[w];
                 vor[w] |= k[w];
             }
         }
+        m[j] = __ballot_sync(0xffffffffu, take);
+        cnt += __popc(m[j]);
     }
-    const int32_t cnt = __popc(bits);
-    int32_t inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-    }
-    if (lane == 31) wtot[warp] = inc;
+    if (lane == 0) wtot[warp] = cnt;
     __syncthreads();
-    int64_t off = offsets[blockIdx.x];
+    int64_t off = offsets[blockIdx.x] + (base ? *base : 0);
     for (int w = 0; w < warp; ++w) off += wtot[w];
-    off += inc - cnt;
-    while (bits) {
-        const int j = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int64_t i = s0 + j;
-        out_slot[off] = static_cast<int32_t>(i);
-        if (out_k) {
-            out_k[3 * off] = k1[i];
-            out_k[3 * off + 1] = f64_key(c.created[i]);
-            out_k[3 * off + 2] = i64_key(c.ids[i]);
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if ((m[j] >> lane) & 1u) {
+            const int64_t i = w0 + j * 32 + lane;
+            const int64_t at = off + __popc(m[j] & lt);
+            const int64_t slot = rk ? rslot[i] : i;
+            out_slot[at] = static_cast<int32_t>(slot);
+            if (out_k) {
+                if (rk) {
+                    out_k[3 * at] = rk[3 * i];
+                    out_k[3 * at + 1] = rk[3 * i + 1];
+                    out_k[3 * at + 2] = rk[3 * i + 2];
+                } else {
+                    out_k[3 * at] = k1[i];
+                    out_k[3 * at + 1] = f64_key(c.created[i]);
+                    out_k[3 * at + 2] = i64_key(c.ids[i]);
+                }
+            }
+            if (out_size) out_size[at] = c.size[slot];
         }
-        ++off;
+        off += __popc(m[j]);
     }
     if (kand) {
 #pragma unroll
@@ -433,12 +432,23 @@ __global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const u
                 vor[w] |= __shfl_xor_sync(0xffffffffu, vor[w], o);
             }
         }
-        if (lane == 0 && vor[0] | vor[1] | vor[2]) {
+        __shared__ unsigned long long band[3], bor[3];
+        if (threadIdx.x < 3) {
+            band[threadIdx.x] = ~0ull;
+            bor[threadIdx.x] = 0ull;
+        }
+        __syncthreads();
+        if (lane == 0 && cnt) {
 #pragma unroll
             for (int w = 0; w < 3; ++w) {
-                atomicAnd(kand + w, static_cast<unsigned long long>(vand[w]));
-                atomicOr(kor + w, static_cast<unsigned long long>(vor[w]));
+                atomicAnd(band + w, static_cast<unsigned long long>(vand[w]));
+                atomicOr(bor + w, static_cast<unsigned long long>(vor[w]));
             }
+        }
+        __syncthreads();
+        if (threadIdx.x < 3 && (bor[0] | bor[1] | bor[2])) {
+            atomicAnd(kand + threadIdx.x, band[threadIdx.x]);
+            atomicOr(kor + threadIdx.x, bor[threadIdx.x]);
         }
     }
 }
