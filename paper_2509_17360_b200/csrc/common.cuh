@@ -123,6 +123,74 @@ __device__ __forceinline__ bool cand_better(uint2 a, uint2 b, const int64_t* ids
     return slot_ids ? a.x < b.x : __ldg(ids + a.x) < __ldg(ids + b.x);
 }
 
+// Warp bitonic sort, descending, of 32*R 64-bit values (element i = lane +
+// 32*r).  Pairs across lanes exchange by shuffles, pairs across registers in
+// place.
+template <int R>
+__device__ __forceinline__ void warp_bitonic_desc(uint64_t (&v)[R], int lane) {
+    constexpr int N = 32 * R;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int rp = r ^ (j >> 5);
+                    if (rp > r) {
+                        const bool desc = ((lane + 32 * r) & k) == 0;
+                        const uint64_t a = v[r], b = v[rp];
+                        if (desc ? a < b : a > b) {
+                            v[r] = b;
+                            v[rp] = a;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int i = lane + 32 * r;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool lower = (i & j) == 0, desc = (i & k) == 0;
+                    const uint64_t mx = v[r] > o ? v[r] : o, mn = v[r] > o ? o : v[r];
+                    v[r] = lower == desc ? mx : mn;
+                }
+            }
+        }
+    }
+}
+
+// Slots in id order: one 64-bit composite (key, ~slot) orders candidates
+// exactly as cand_better (key desc, id asc); list + pending are sorted
+// together by a warp bitonic network (R = 2 or 4 values per lane).
+template <int R>
+__device__ __forceinline__ int warp_bitonic_merge(uint32_t* lk, int32_t* ls, int n, int kp, const uint2* pend,
+                                                  int np, int lane) {
+    uint64_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        uint64_t c = 0;  // empty: sorts last
+        if (e < n)
+            c = (static_cast<uint64_t>(lk[e]) << 32) | (0xffffffffu - static_cast<uint32_t>(ls[e]));
+        else if (e < n + np)
+            c = (static_cast<uint64_t>(pend[e - n].y) << 32) | (0xffffffffu - pend[e - n].x);
+        v[r] = c;
+    }
+    __syncwarp();
+    warp_bitonic_desc<R>(v, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        if (e < kp && e < n + np) {
+            lk[e] = static_cast<uint32_t>(v[r] >> 32);
+            ls[e] = static_cast<int32_t>(0xffffffffu - static_cast<uint32_t>(v[r]));
+        }
+    }
+    __syncwarp();
+    return min(n + np, kp);
+}
+
 // Merge np pending (slot, key) candidates into one query's best-first list
 // (n entries, capacity kp) in a single warp step: every entry of list U
 // pending is ranked against all others and lands at its rank if < kp.
@@ -130,6 +198,8 @@ __device__ __forceinline__ bool cand_better(uint2 a, uint2 b, const int64_t* ids
 __device__ __forceinline__ int warp_rank_merge(uint32_t* lk, int32_t* ls, int n, int kp, const uint2* pend, int np,
                                                uint2* scratch, const int64_t* ids, bool slot_ids, int lane) {
     const int tot = n + np;
+    if (slot_ids && tot <= 64) return warp_bitonic_merge<2>(lk, ls, n, kp, pend, np, lane);
+    if (slot_ids && tot <= 128) return warp_bitonic_merge<4>(lk, ls, n, kp, pend, np, lane);
     for (int e = lane; e < tot; e += 32)
         scratch[e] = e < n ? make_uint2(static_cast<uint32_t>(ls[e]), lk[e]) : pend[e - n];
     __syncwarp();

@@ -447,6 +447,17 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     return L;
 }
 
+// sc[j] for a run-time j without demoting the array to local memory: an
+// unrolled select over the register array (only on the rare pending path).
+template <int N>
+__device__ __forceinline__ float pick_reg(const float (&sc)[N], int j) {
+    float r = 0.0f;
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+        if (q == j) r = sc[q];
+    return r;
+}
+
 __device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool v) {
     uint32_t r;
     asm volatile(
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                         uint32_t pos = __popc(wball[warp * NQ + j] & lt);
                         for (int w = 0; w < warp; ++w) pos += __popc(wball[w * NQ + j]);
                         if (pos < kResQPer) {
-                            pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
+                            pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(pick_reg<NQ>(sc, j)));
                             mask &= ~(1ull << j);
                         }
                     }
@@ -1063,7 +1074,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
                             uint32_t pos = __popc(wball[warp * NQ + j] & lt);
                             for (int x = 0; x < warp; ++x) pos += __popc(wball[x * NQ + j]);
                             if (pos < kResQPer) {
-                                pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(sc[j]));
+                                pend[j * kResQPer + pos] = make_uint2(static_cast<uint32_t>(slot), f32_key(pick_reg<NQ>(sc, j)));
                                 mask[w] &= ~(1ull << jj);
                             }
                         }
