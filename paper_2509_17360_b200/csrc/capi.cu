@@ -176,6 +176,7 @@ struct sine_index {
     DevBuf<int64_t> exp_off;
     DevBuf<uint32_t> gbound;        // chip-wide admission bounds of the running launch
     DevBuf<uint32_t> gcnt;          // tiled GEMM: candidates per query + overflow counter
+    DevBuf<uint32_t> tmax;          // sample pass: per (tile, query) max score keys
     int64_t gemm_overflows = 0;     // GEMM launches re-run on the list-keeping kernels
     HostBuf<unsigned long long> sel_h;  // counter + kand + kor
     DevBuf<SelectState> st, st1;       // selection state; st1 = after pass 1 (the record prefix)
@@ -714,13 +715,18 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         // a sample pass (one strided tile per cluster) seeds the chip-wide
         // bound with the kp-th best sampled key -- a valid lower bound on the
         // global kp-th best -- so the main pass admits almost nothing extra.
-        const int sample_tiles = std::min(max_clusters, ntiles / 16);
-        if (thr0 < 0.5f && sample_tiles >= 16 && nq >= 8) {
+        // The sample pass keeps no lists: per sampled tile and query it
+        // writes the max score; the kp-th largest tile maximum is a valid
+        // lower bound on the kp-th best score (kp distinct rows reach it).
+        const int sample_tiles = std::min(2 * max_clusters, ntiles / 8);
+        if (thr0 < 0.5f && sample_tiles >= 2 * kp && nq >= 8) {
+            h->tmax.ensure(static_cast<size_t>(sample_tiles) * CS * NQ);
             ResParams sp = p;
             sp.ntiles = sample_tiles;
             sp.tile_stride = ntiles / sample_tiles;
-            const int scl = launch(sp, sample_tiles);
-            sample_bound_kernel<<<nq, 256, 0, st>>>(h->lkey.p, h->ln.p, scl, nq, kp, h->gbound.p);
+            sp.out_max = h->tmax.p;
+            launch(sp, std::min(max_clusters, sample_tiles));
+            sample_max_bound_kernel<<<nq, 256, 0, st>>>(h->tmax.p, sample_tiles, nq, kp, h->gbound.p);
             h->launches += 2;
             CK(cudaGetLastError());
         }
@@ -788,13 +794,15 @@ void umma_pair_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int
         p.out_key = h->lkey.p;
         p.out_slot = h->lslot.p;
         p.out_n = h->ln.p;
-        const int sample_pairs = std::min(npairs, ntiles / 16);
-        if (thr0 < 0.5f && sample_pairs >= 16 && nq >= 8) {  // seed the admission bound (see umma_res_query)
+        const int sample_tiles = std::min(2 * npairs, ntiles / 8);  // pair tiles (see umma_res_query)
+        if (thr0 < 0.5f && sample_tiles >= kp && nq >= 8) {
+            h->tmax.ensure(static_cast<size_t>(2 * sample_tiles) * NQ);
             ResParams sp = p;
-            sp.ntiles = sample_pairs;
-            sp.tile_stride = ntiles / sample_pairs;
-            umma_pair_kernel<NQH><<<2 * sample_pairs, kUmmaThreads, L.total, st>>>(qmap, rmap, sp);
-            sample_bound_kernel<<<nq, 256, 0, st>>>(h->lkey.p, h->ln.p, 2 * sample_pairs, nq, kp, h->gbound.p);
+            sp.ntiles = sample_tiles;
+            sp.tile_stride = ntiles / sample_tiles;
+            sp.out_max = h->tmax.p;
+            umma_pair_kernel<NQH><<<2 * std::min(npairs, sample_tiles), kUmmaThreads, L.total, st>>>(qmap, rmap, sp);
+            sample_max_bound_kernel<<<nq, 256, 0, st>>>(h->tmax.p, 2 * sample_tiles, nq, kp, h->gbound.p);
             h->launches += 2;
             CK(cudaGetLastError());
         }

@@ -412,10 +412,16 @@ struct ResParams {
     uint32_t* out_key;
     int32_t* out_slot;
     int32_t* out_n;
+    // sample pass (non-null): no lists; per (sampled tile, query) the max
+    // score key over the tile's rows, [tile][nq] (pair: [2*tile + rank][nq])
+    uint32_t* out_max;
 };
 
+constexpr int kSparse = 128;     // (query, row) pairs per tile handed to the sparse inserter
+constexpr int kSparseRows = 32;  // tiles with more passing rows take the dense (bitonic) rounds
+
 struct ResSmem {
-    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, total;
+    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, sparse_off, total;
 };
 
 // Nq_res: queries resident in this CTA's shared memory (== Nq except for the
@@ -443,8 +449,98 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     off += static_cast<size_t>(Nq) * kResQPer * 8;
     off += static_cast<size_t>(4) * (kMaxKp + kResQPer) * 8;  // per-warp merge scratch
     off += static_cast<size_t>(4) * Nq * 4;                    // per-warp ballots
+    off = (off + 15) / 16 * 16;
+    L.sparse_off = off;  // counter + kSparse (query, slot, key) entries
+    off += 16 + static_cast<size_t>(kSparse) * 16;
     L.total = off + 1024;
     return L;
+}
+
+// Insert one candidate into a query's best-first list (warp-cooperative:
+// rank by a warp count, shift the tail down one, write).  Raises the
+// query's admission threshold and the chip-wide bound once the list is full.
+__device__ __noinline__ void warp_insert_one(uint32_t* lk, int32_t* ls, uint32_t* cnt_j, float* thr_j, uint32_t* gb_j,
+                                             int kp, uint32_t key, int32_t slot, const int64_t* ids, bool slot_ids,
+                                             int lane) {
+    const int n = static_cast<int>(*cnt_j);
+    const uint2 me = make_uint2(static_cast<uint32_t>(slot), key);
+    if (n == kp && !cand_better(me, make_uint2(static_cast<uint32_t>(ls[kp - 1]), lk[kp - 1]), ids, slot_ids)) return;
+    int r = 0;
+    for (int e = lane; e < n; e += 32)
+        r += cand_better(make_uint2(static_cast<uint32_t>(ls[e]), lk[e]), me, ids, slot_ids) ? 1 : 0;
+    r = __reduce_add_sync(0xffffffffu, r);
+    const int m = min(n, kp - 1);  // entries that survive the shift
+    uint32_t tk[kMaxKp / 32];
+    int32_t ts[kMaxKp / 32];
+#pragma unroll
+    for (int c = 0; c < kMaxKp / 32; ++c) {
+        const int e = r + lane + 32 * c;
+        if (e < m) {
+            tk[c] = lk[e];
+            ts[c] = ls[e];
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < kMaxKp / 32; ++c) {
+        const int e = r + lane + 32 * c;
+        if (e < m) {
+            lk[e + 1] = tk[c];
+            ls[e + 1] = ts[c];
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        lk[r] = key;
+        ls[r] = slot;
+        const int nn = min(n + 1, kp);
+        *cnt_j = static_cast<uint32_t>(nn);
+        if (nn == kp) {
+            const uint32_t wk = lk[kp - 1];
+            *thr_j = fmaxf(*thr_j, key_f32(wk));
+            atomicMax(gb_j, wk);
+        }
+    }
+    __syncwarp();
+}
+
+// Sample pass: per query, the max score of this CTA's 128 rows of the tile
+// (warp max, then across the 4 epilogue warps through `wmax` [4][NQ]).
+// The k'-th largest such tile maximum is a lower bound on the k'-th best
+// score over all rows (k' distinct rows reach it).
+template <int NQ>
+__device__ __forceinline__ void tile_max_out(const float (&sc)[NQ], bool live, int nq_local, uint32_t* wmax,
+                                             uint32_t* out, int warp, int lane, int tid) {
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+        float v = live ? sc[j] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) wmax[warp * NQ + j] = __float_as_uint(v);
+    }
+    named_bar_sync(2, 128);
+    if (tid < nq_local) {
+        float m = -INFINITY;
+        for (int w = 0; w < 4; ++w) m = fmaxf(m, __uint_as_float(wmax[w * NQ + tid]));
+        out[tid] = m > -INFINITY ? f32_key(m + 0.0f) : 0u;  // NaN never wins fmaxf
+    }
+    named_bar_sync(2, 128);
+}
+
+// Sparse phase of a tile: the ns (<= kSparse) appended pairs are inserted
+// by the four epilogue warps, warp w taking the queries j with j % 4 == w
+// (one writer per list).  Ends with the epilogue barrier.
+__device__ __forceinline__ void sparse_insert_phase(const uint4* sbuf, uint32_t ns, uint32_t* lkey, int32_t* lslot,
+                                                    uint32_t* cnt, float* thr, uint32_t* gb, int kp,
+                                                    const int64_t* ids, bool slot_ids, int warp, int lane) {
+    for (uint32_t i = 0; i < ns; ++i) {
+        const uint4 e = sbuf[i];
+        if (static_cast<int>(e.x & 3u) != warp) continue;
+        if (!(key_f32(e.z) >= thr[e.x])) continue;  // the threshold rose since the append
+        warp_insert_one(lkey + e.x * kp, lslot + e.x * kp, cnt + e.x, thr + e.x, gb + e.x, kp, e.z,
+                        static_cast<int32_t>(e.y), ids, slot_ids, lane);
+    }
+    named_bar_sync(2, 128);
 }
 
 // sc[j] for a run-time j without demoting the array to local memory: an
@@ -456,6 +552,17 @@ __device__ __forceinline__ float pick_reg(const float (&sc)[N], int j) {
     for (int q = 0; q < N; ++q)
         if (q == j) r = sc[q];
     return r;
+}
+
+__device__ __forceinline__ int bar_red_popc(int id, int nthreads, bool v) {
+    uint32_t r;
+    asm volatile(
+        "{\n.reg .pred pi;\nsetp.ne.u32 pi, %1, 0;\n"
+        "barrier.red.popc.u32 %0, %2, %3, pi;\n}\n"
+        : "=r"(r)
+        : "r"(v ? 1u : 0u), "r"(id), "r"(nthreads)
+        : "memory");
+    return static_cast<int>(r);
 }
 
 __device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool v) {
@@ -547,6 +654,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
     uint2* merge_scratch = pend + NQ * kResQPer;
     uint32_t* wball = reinterpret_cast<uint32_t*>(merge_scratch + 4 * (kMaxKp + kResQPer));  // [4][NQ]
+    uint32_t* scount = reinterpret_cast<uint32_t*>(smem + L.sparse_off);
+    uint4* sbuf = reinterpret_cast<uint4*>(smem + L.sparse_off + 16);
     constexpr uint32_t kTmemCols = NQ <= 16 ? 32 : (2 * NQ <= 64 ? 64 : 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -568,6 +677,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         thr[j] = p.thr0;
         pcnt[j] = 0;
     }
+    if (threadIdx.x == 0) *scount = 0;
     const int crank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
     const int cid = CS > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
     const int ncl = CS > 1 ? static_cast<int>(cluster_count_x()) : static_cast<int>(gridDim.x);
@@ -692,6 +802,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + acc);  // TMEM buffer free for tile i+2
+            if (p.out_max) {
+                tile_max_out<NQ>(sc, live, nq_local, wball, p.out_max + static_cast<size_t>(t) * p.nq + crank * NQ,
+                                 warp, lane, tid);
+                continue;
+            }
 
             uint64_t mask = 0;
             if (live) {
@@ -699,7 +814,35 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 for (int j = 0; j < NQ; ++j)
                     if (j < nq_local && sc[j] >= thr[j]) mask |= 1ull << j;
             }
-            while (bar_red_or(1, 128, mask != 0)) {
+            // sparse hand-off: once the thresholds are warm a tile admits a
+            // few pairs; they go to a tile buffer and are inserted one by
+            // one.  A warm-up tile (many rows pass) takes the dense rounds.
+            const int nrows = bar_red_popc(1, 128, mask != 0);
+            bool dense = nrows > kSparseRows;
+            uint32_t ns = 0;
+            if (nrows && !dense) {
+                while (mask) {
+                    const int j = __ffsll(mask) - 1;
+                    const uint32_t at = atomicAdd(scount, 1u);
+                    if (at >= kSparse) break;  // the rest takes the dense rounds below
+                    sbuf[at] = make_uint4(static_cast<uint32_t>(j), static_cast<uint32_t>(slot),
+                                          f32_key(pick_reg<NQ>(sc, j)), 0u);
+                    mask &= mask - 1;
+                }
+                dense = bar_red_or(1, 128, mask != 0);
+                ns = min(*reinterpret_cast<volatile uint32_t*>(scount), static_cast<uint32_t>(kSparse));
+            }
+            if (ns) {
+                sparse_insert_phase(sbuf, ns, lkey, lslot, cnt, thr, p.gbound + crank * NQ, kp, p.ids, slot_ids,
+                                    warp, lane);
+                if (tid == 0) *scount = 0;
+                if (mask) {
+#pragma unroll
+                    for (int j = 0; j < NQ; ++j)
+                        if (((mask >> j) & 1ull) && !(sc[j] >= thr[j])) mask &= ~(1ull << j);
+                }
+            }
+            while (dense && bar_red_or(1, 128, mask != 0)) {
                 // queue what fits (row order), positions from ballots -- no
                 // atomics: in a warm-up tile every row passes for every query
                 for (int j = 0; j < NQ; ++j) {
@@ -757,7 +900,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
         }
         named_bar_sync(2, 128);
-        for (int j = 0; j < nq_local; ++j) {
+        for (int j = 0; j < nq_local && !p.out_max; ++j) {
             const int qg = crank * NQ + j;  // query index within the launch
             const uint32_t n = cnt[j];
             const size_t base = (static_cast<size_t>(cid) * p.nq + qg) * kp;
@@ -808,6 +951,35 @@ __global__ void __launch_bounds__(256) sample_bound_kernel(const uint32_t* in_ke
             return true;
         },
         nflat, static_cast<uint32_t>(kp), true, 32, hist, scratch, &before, &equal);
+    if (threadIdx.x == 0) gbound[qi] = kstar;
+}
+
+// Seed of the chip-wide admission bound from a max-sample pass: per query,
+// the kp-th largest of the ntile sampled tile maxima (0 if fewer than kp).
+__global__ void __launch_bounds__(256) sample_max_bound_kernel(const uint32_t* tmax, int ntile, int nq, int kp,
+                                                               uint32_t* gbound) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t scratch[16];
+    const int qi = blockIdx.x;
+    uint32_t before, equal;
+    uint32_t c = 0;
+    for (int f = threadIdx.x; f < ntile; f += 256) c += tmax[static_cast<size_t>(f) * nq + qi] != 0u ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = c;
+    __syncthreads();
+    uint32_t total = 0;
+    for (int w = 0; w < 8; ++w) total += scratch[w];
+    __syncthreads();
+    if (total < static_cast<uint32_t>(kp)) {
+        if (threadIdx.x == 0) gbound[qi] = 0;
+        return;
+    }
+    const uint32_t kstar = block_select<uint32_t>(
+        [&](int f, uint32_t& key) {
+            key = tmax[static_cast<size_t>(f) * nq + qi];
+            return key != 0u;
+        },
+        ntile, static_cast<uint32_t>(kp), true, 32, hist, scratch, &before, &equal);
     if (threadIdx.x == 0) gbound[qi] = kstar;
 }
 
@@ -905,6 +1077,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
     uint2* pend = reinterpret_cast<uint2*>(smem + L.pend_off + ((NQ * 4 + 16 + 15) / 16 * 16));
     uint2* merge_scratch = pend + NQ * kResQPer;
     uint32_t* wball = reinterpret_cast<uint32_t*>(merge_scratch + 4 * (kMaxKp + kResQPer));
+    uint32_t* scount = reinterpret_cast<uint32_t*>(smem + L.sparse_off);
+    uint4* sbuf = reinterpret_cast<uint4*>(smem + L.sparse_off + 16);
     constexpr uint32_t kTmemCols = 2 * NQ <= 64 ? 64 : (2 * NQ <= 128 ? 128 : 256);
     constexpr int MW = (NQ + 63) / 64;  // 64-bit words of the per-row query mask
 
@@ -929,6 +1103,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
         thr[j] = p.thr0;
         pcnt[j] = 0;
     }
+    if (threadIdx.x == 0) *scount = 0;
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
@@ -1041,6 +1216,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
                 else
                     mbar_arrive_leader(tempty + acc);
             }
+            if (p.out_max) {
+                tile_max_out<NQ>(sc, live, nq_local, wball, p.out_max + static_cast<size_t>(2 * t + rank) * p.nq,
+                                 warp, lane, tid);
+                continue;
+            }
             uint64_t mask[MW];
 #pragma unroll
             for (int w = 0; w < MW; ++w) mask[w] = 0;
@@ -1055,7 +1235,40 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
                 for (int w = 0; w < MW; ++w) o |= mask[w];
                 return o != 0;
             };
-            while (bar_red_or(1, 128, any_mask())) {
+            // sparse hand-off (see umma_res_kernel)
+            const int nrows = bar_red_popc(1, 128, any_mask());
+            bool dense = nrows > kSparseRows;
+            uint32_t ns = 0;
+            if (nrows && !dense) {
+                bool full = false;
+#pragma unroll
+                for (int w = 0; w < MW; ++w) {
+                    while (mask[w] && !full) {
+                        const int jj = __ffsll(mask[w]) - 1;
+                        const uint32_t at = atomicAdd(scount, 1u);
+                        if (at >= kSparse) {
+                            full = true;
+                            break;
+                        }
+                        sbuf[at] = make_uint4(static_cast<uint32_t>(w * 64 + jj), static_cast<uint32_t>(slot),
+                                              f32_key(pick_reg<NQ>(sc, w * 64 + jj)), 0u);
+                        mask[w] &= mask[w] - 1;
+                    }
+                }
+                dense = bar_red_or(1, 128, any_mask());
+                ns = min(*reinterpret_cast<volatile uint32_t*>(scount), static_cast<uint32_t>(kSparse));
+            }
+            if (ns) {
+                sparse_insert_phase(sbuf, ns, lkey, lslot, cnt, thr, p.gbound, kp, p.ids, slot_ids, warp, lane);
+                if (tid == 0) *scount = 0;
+                if (any_mask()) {
+#pragma unroll
+                    for (int j = 0; j < NQ; ++j)
+                        if (((mask[j >> 6] >> (j & 63)) & 1ull) && !(sc[j] >= thr[j]))
+                            mask[j >> 6] &= ~(1ull << (j & 63));
+                }
+            }
+            while (dense && bar_red_or(1, 128, any_mask())) {
 #pragma unroll
                 for (int j = 0; j < NQ; ++j) {
                     const uint32_t b = __ballot_sync(0xffffffffu, (mask[j >> 6] >> (j & 63)) & 1ull);
@@ -1115,7 +1328,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) __cluster_dims__(2, 1, 1)
             }
         }
         named_bar_sync(2, 128);
-        for (int j = 0; j < nq_local; ++j) {
+        for (int j = 0; j < nq_local && !p.out_max; ++j) {
             const uint32_t n = cnt[j];
             const size_t base = (static_cast<size_t>(blockIdx.x) * p.nq + j) * kp;
             for (int e = tid; e < static_cast<int>(n); e += 128) {
