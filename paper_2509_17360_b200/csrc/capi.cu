@@ -384,10 +384,13 @@ void check_new_ids(const sine_index* h, int64_t n, const int64_t* ids) {
     }
 }
 
+// id -> slot over every slot in the host tables (including a batch being
+// appended, whose slots are not yet counted in nslots)
 void build_pos_map(sine_index* h) {
+    const int64_t n = static_cast<int64_t>(h->ids_h.size());
     h->pos.clear();
-    h->pos.reserve(h->nslots * 2);
-    for (int64_t s = 0; s < h->nslots; ++s)
+    h->pos.reserve(n * 2);
+    for (int64_t s = 0; s < n; ++s)
         if (h->live_h[s]) h->pos[h->ids_h[s]] = s;
 }
 
@@ -833,6 +836,8 @@ void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
 // query's candidates overflowed the chunk capacity; the caller then runs the
 // list-keeping kernels.
 constexpr int kGemmChunks = 32;
+constexpr float kGemmMinFloor = 0.25f;  // below it the GEMM seeds per-query floors from a sample pass
+constexpr int kGemmSeedMinTiles = 8 * 64;  // row tiles a seeded GEMM needs (the sample is 1/8 of them)
 
 bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
                      bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
@@ -883,6 +888,26 @@ bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
     p.cnt = h->gcnt.p;
     p.out_key = h->lkey.p;
     p.out_slot = h->lslot.p;
+    p.rt_stride = 1;
+    if (thr0 < kGemmMinFloor) {
+        // low floor: a sample pass over every 8th row tile writes per-query
+        // tile maxima; the kp-th largest is a lower bound on the kp-th best
+        // score and becomes the query's admission floor in the main pass
+        const int nrt_s = std::max(kp, nrt / 8);
+        if (nrt_s > nrt) return false;
+        h->tmax.ensure(static_cast<size_t>(2 * nrt_s) * B);
+        GemmParams sp = p;
+        sp.nrt = nrt_s;
+        sp.rt_stride = nrt / nrt_s;
+        sp.out_max = h->tmax.p;
+        const int sp_pairs = std::max(1, std::min(h->num_sms / 2, nrt_s * nqt));
+        umma_gemm_kernel<<<2 * sp_pairs, kGemmThreads, smem, st>>>(qmap, rmap, sp);
+        sample_max_bound_kernel<<<static_cast<int>(B), 256, 0, st>>>(h->tmax.p, 2 * nrt_s, static_cast<int>(B), kp,
+                                                                     h->gbound.p);
+        h->launches += 2;
+        CK(cudaGetLastError());
+        p.qthr = h->gbound.p;
+    }
     const size_t tk = tbegin(h, 2, st);
     umma_gemm_kernel<<<2 * npairs, kGemmThreads, smem, st>>>(qmap, rmap, p);
     tend(h, tk, st);
@@ -934,7 +959,9 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         // HBM passes; up to 256 queries it costs about one HBM pass (measured,
         // 1M x 768, tau 0.9: bf16 B=256 0.39 ms vs 0.84 ms in two 128-query
         // pair passes; fp32 B=256 0.71 vs 1.65 ms)
-        const bool gemm_auto = !(mode & SINE_SCAN_NO_GEMM) && !force_v1 && B > per_pass && thr0 >= 0.25f &&
+        const int64_t row_tiles = (h->nslots + kGemmRows - 1) / kGemmRows;
+        const bool gemm_floor_ok = thr0 >= kGemmMinFloor || row_tiles >= kGemmSeedMinTiles;
+        const bool gemm_auto = !(mode & SINE_SCAN_NO_GEMM) && !force_v1 && B > per_pass && gemm_floor_ok &&
                                !(mode & (SINE_SCAN_PAIR | SINE_SCAN_CLUSTER));
         if ((mode & SINE_SCAN_GEMM) || gemm_auto) {
             if (umma_gemm_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st))

@@ -1391,10 +1391,13 @@ struct GemmParams {
     uint32_t* cnt;       // [nq] pairs >= thr0 seen per query (may exceed capacity)
     uint32_t* out_key;   // [chunks][nq][kp]
     int32_t* out_slot;
+    const uint32_t* qthr;  // [nq] per-query admission keys (max with thr0), nullable = uniform thr0
+    int rt_stride;         // row tile t of the launch is physical tile t * rt_stride (sample pass)
+    uint32_t* out_max;     // sample pass: [2 * t + rank][nq] max score key of the CTA's 128 rows
 };
 
 __host__ __device__ inline size_t gemm_smem_bytes(int S) {
-    return static_cast<size_t>(S) * 2 * 128 * kUmmaKB + (2 * S + 4) * sizeof(uint64_t) + 16 + 1024;
+    return static_cast<size_t>(S) * 2 * 128 * kUmmaKB + (2 * S + 4) * sizeof(uint64_t) + 16 + 3 * 256 * 4 + 1024;
 }
 
 __device__ __forceinline__ void gemm_append(const GemmParams& p, int q, uint32_t key, int32_t slot) {
@@ -1408,9 +1411,77 @@ __device__ __forceinline__ void gemm_append(const GemmParams& p, int q, uint32_t
     }
 }
 
+// Epilogue of one item for the sample pass (out_max: per query, the max
+// score key over this CTA's 128 rows -> [2t + rank][nq]) or for per-query
+// admission floors (qthr, staged in shared memory per item).  A 32-score
+// chunk of a row is skipped when its max is below the chunk's smallest floor.
+__device__ __noinline__ void gemm_epilogue_general(const GemmParams& p, uint32_t tmem, int acc, int warp, int lane,
+                                                   int tid, bool live, int64_t slot, int qbase, size_t orow,
+                                                   uint32_t* colmax, float* fl, uint64_t* tfull, int i) {
+    if (!p.out_max) {
+        const uint32_t k0 = f32_key(p.thr0);
+        for (int j = tid; j < kGemmNQ; j += 128) {
+            const int q = qbase + j;
+            fl[j] = q < p.nq ? key_f32(max(k0, __ldg(p.qthr + q))) : INFINITY;
+        }
+        named_bar_sync(2, 128);  // (fl is double-buffered by accumulator: one barrier per item suffices)
+    }
+    mbar_wait(tfull + acc, (i >> 1) & 1);
+    tc_fence_after();
+    // chunks not unrolled and appends in a bit loop: keeps the code small
+    // (an unrolled 256-site append body thrashes the instruction cache)
+#pragma unroll 1
+    for (int c = 0; c < kGemmNQ / 32; ++c) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * kGemmNQ + c * 32;
+        SINE_TMEM_LD32(taddr, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (p.out_max) {
+            uint32_t mine = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float x = __uint_as_float(r[j]);
+                const uint32_t kx = (live && x == x) ? f32_key(x + 0.0f) : 0u;  // NaN never sets a bound
+                const uint32_t m = __reduce_max_sync(0xffffffffu, kx);
+                if (lane == j) mine = m;
+            }
+            atomicMax(colmax + c * 32 + lane, mine);
+            continue;
+        }
+        const float tmin = key_f32(__reduce_min_sync(0xffffffffu, f32_key(fl[c * 32 + lane])));
+        float m = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]));
+        if (live && m >= tmin) {
+            uint32_t pass = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (__uint_as_float(r[j]) + 0.0f >= fl[c * 32 + j] && qbase + c * 32 + j < p.nq) pass |= 1u << j;
+            while (pass) {
+                const int j = __ffs(pass) - 1;
+                pass &= pass - 1;
+                float sc = 0.0f;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj)
+                    if (jj == j) sc = __uint_as_float(r[jj]);
+                gemm_append(p, qbase + c * 32 + j, f32_key(sc + 0.0f), static_cast<int32_t>(slot));
+            }
+        }
+    }
+    if (p.out_max) {
+        named_bar_sync(2, 128);
+        for (int j = tid; j < kGemmNQ; j += 128) {
+            const int q = qbase + j;
+            if (q < p.nq) p.out_max[orow * p.nq + q] = colmax[j];
+            colmax[j] = 0u;
+        }
+        named_bar_sync(2, 128);
+    }
+}
+
 __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
-                     const GemmParams p) {
+                     const __grid_constant__ GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages, nkb = p.kblocks;
@@ -1422,12 +1493,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint32_t* colmax = tmem_slot + 4;  // [256] sample pass: per-query max keys of this item
+    float* floors = reinterpret_cast<float*>(colmax + kGemmNQ);  // [2][256] per-query floors (by accumulator)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = static_cast<int>(cluster_ctarank());
     const int pair = static_cast<int>(cluster_id_x());
     const int npair = static_cast<int>(cluster_count_x());
     const int nitems = p.nrt * p.nqt;
+    for (int j = threadIdx.x; j < kGemmNQ; j += blockDim.x) colmax[j] = 0u;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
@@ -1462,7 +1536,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
             uint32_t ph = 0;
             for (int w = pair; w < nitems; w += npair) {
                 const int t = w / p.nqt, g = w - (w / p.nqt) * p.nqt;
-                const int r0 = t * kGemmRows + rank * 128;
+                const int r0 = t * p.rt_stride * kGemmRows + rank * 128;
                 const int q0 = g * kGemmNQ + rank * 128;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(empty + s, ph ^ 1);
@@ -1520,10 +1594,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
         for (int w = pair; w < nitems; w += npair, ++i) {
             const int acc = i & 1;
             const int t = w / p.nqt, g = w - (w / p.nqt) * p.nqt;
-            const int64_t slot = static_cast<int64_t>(t) * kGemmRows + rank * 128 + tid;
+            const int64_t slot = static_cast<int64_t>(t) * p.rt_stride * kGemmRows + rank * 128 + tid;
             const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
             const bool live = ((vw >> (slot & 31)) & 1u) != 0;
             const int qbase = g * kGemmNQ;
+            if (p.out_max || p.qthr) {
+                // sample pass (per-query max over the rows) or per-query
+                // admission floors: the general, slower epilogue
+                gemm_epilogue_general(p, tmem, acc, warp, lane, tid, live, slot, qbase,
+                                      static_cast<size_t>(2 * t + rank), colmax, floors + acc * kGemmNQ, tfull, i);
+            } else {
             mbar_wait(tfull + acc, (i >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
@@ -1555,6 +1635,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
                         if (sc >= thr0 && q < p.nq) gemm_append(p, q, f32_key(sc), static_cast<int32_t>(slot));
                     }
                 }
+            }
             }
             tc_fence_before();
             __syncwarp();

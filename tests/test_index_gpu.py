@@ -433,11 +433,22 @@ def test_tiled_gemm_bf16_raw_and_overflow_fallback(pkg):
         want = ora.query(q[j], 5, 0.9)
         assert counts[j] >= 1
         assert abs(sims[j, 0] - want[0].similarity) < 2e-2
-    before = idx.gemm_overflows()
-    got = idx.query_batch(q, 5, -1.0, gemm=True)
-    assert idx.gemm_overflows() == before + 1
+    # a dense cluster (every row within cos ~0.98 of the query) overflows
+    # the per-query candidate buffers at a floor >= 0.25: exact fallback
+    base = rng.standard_normal(d)
+    crow = base + 0.1 * rng.standard_normal((n, d))
+    crow /= np.linalg.norm(crow, axis=1, keepdims=True)
+    cidx = pkg.GpuCosineIndex(d, scan="bf16", store_f32=True)  # exact: certificate fallback to fp32 rows
+    cidx.insert_batch(np.arange(n), crow)
+    cora = O.OracleExactIndex(d)
+    cora.bulk_load(np.arange(n), crow)
+    cq = base + 0.1 * rng.standard_normal((B, d))
+    cq /= np.linalg.norm(cq, axis=1, keepdims=True)
+    before = cidx.gemm_overflows()
+    got = cidx.query_batch(cq, 5, 0.5, gemm=True)
+    assert cidx.gemm_overflows() == before + 1
     for j in range(0, B, 13):
-        want = ora.query(q[j], 5, -1.0)
+        want = cora.query(cq[j], 5, 0.5)
         assert got[0][j, :got[2][j]].tolist() == [c.id for c in want]
 
 
@@ -462,3 +473,58 @@ def test_insert_device_orders_after_producer_stream(pkg):
     X = torch.cat(kept).cpu().numpy()
     pick = np.random.default_rng(0).choice(2 * n, 500, replace=False)
     np.testing.assert_array_equal(idx.rows(pick), X[pick])
+
+
+def test_tiled_gemm_seeded_low_threshold(pkg):
+    """Low min_similarity through the tiled GEMM: a sample pass seeds
+    per-query floors (the k'-th largest tile maximum), the main pass keeps
+    every pair above them; exact vs the oracle, no overflow."""
+    rng = np.random.default_rng(21)
+    n, d, B = 40000, 256, 300
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((B, d))
+    q[:100] = rows[rng.integers(0, n, 100)] + 0.05 * rng.standard_normal((100, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(np.arange(n), rows)
+        for k, ms in ((10, -1.0), (20, 0.1)):
+            got = idx.query_batch(q, k, ms, gemm=True)
+            assert idx.gemm_overflows() == 0
+            for j in range(B):
+                want = ora.query(q[j], k, ms)
+                assert got[0][j, :got[2][j]].tolist() == [c.id for c in want], (scan, k, ms, j)
+                np.testing.assert_allclose(got[1][j, :got[2][j]], [c.similarity for c in want], atol=1e-12, rtol=0)
+
+
+def test_unordered_id_batches_remove_and_requery(pkg):
+    """Ids arriving out of order (first batch unordered, then ascending,
+    then unordered again) stay addressable: remove / duplicate checks /
+    rows() see every id (reference index.py:71-92 semantics)."""
+    rng = np.random.default_rng(31)
+    d = 32
+    rows = rng.standard_normal((900, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    ids = rng.permutation(100000)[:900]
+    idx = pkg.GpuCosineIndex(d)
+    idx.insert_batch(ids[:300], rows[:300])
+    idx.insert_batch(np.sort(ids[300:600]) + 200000, rows[300:600])
+    idx.insert_batch(ids[600:], rows[600:])
+    all_ids = np.concatenate([ids[:300], np.sort(ids[300:600]) + 200000, ids[600:]])
+    with pytest.raises(pkg.ValidationError):
+        idx.insert(int(ids[5]), rows[0])
+    np.testing.assert_array_equal(idx.rows(all_ids[::37]), rows[::37])
+    gone = all_ids[::5]
+    idx.remove_batch(gone)
+    ora = O.OracleExactIndex(d)
+    keep = np.setdiff1d(np.arange(900), np.arange(900)[::5])
+    ora.bulk_load(all_ids[keep], rows[keep])
+    assert len(idx) == len(keep)
+    q = rows[:20] + 0.1 * rng.standard_normal((20, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    got = idx.query_batch(q, 7, -1.0)
+    for j in range(20):
+        assert got[0][j, :got[2][j]].tolist() == [c.id for c in ora.query(q[j], 7, -1.0)]

@@ -1,0 +1,69 @@
+"""Row-sharded stage-1 with real GPU shards: two ranks (gloo for the
+candidate all-gather, since this pool's boxes have one GPU) each own a
+GpuCosineIndex on cuda:0; the merged answer must equal the oracle on the
+unsharded rows, ids bit-exact and fp64 similarities to 1e-12."""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from test_sharded_gloo import _free_port
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from oracle import sine_oracle as O
+    from paper_2509_17360_b200 import GpuCosineIndex
+    from paper_2509_17360_b200.sharded import ShardedCosineIndex
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    rng = np.random.default_rng(1)
+    n, d, B = 30000, 384, 96
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    rows[1000:1010] = rows[7]  # exact ties spread over both shards
+    ids = rng.permutation(10 * n)[:n]
+    sh = ShardedCosineIndex(GpuCosineIndex(d, device=0))
+    sh.insert_batch(ids[:20000], rows[:20000])
+    sh.insert_batch(ids[20000:], rows[20000:])
+    sh.remove_batch(ids[:300:7])
+    keep = np.setdiff1d(np.arange(n), np.arange(300)[::7])
+    full = O.OracleExactIndex(d)
+    full.bulk_load(ids[keep], rows[keep])
+    q = rng.standard_normal((B, d))
+    q[:40] = rows[rng.integers(0, n, 40)] + 0.02 * rng.standard_normal((40, d))
+    q[40] = rows[7]
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ok = True
+    for k, ms in ((10, 0.9), (20, -1.0)):
+        gi, gs, gc = sh.query_batch(q, k, ms)
+        for j in range(B):
+            want = full.query(q[j], k, ms)
+            ok &= gi[j, :gc[j]].tolist() == [c.id for c in want]
+            ok &= bool(np.allclose(gs[j, :gc[j]], [c.similarity for c in want], atol=1e-12, rtol=0))
+    out[rank] = bool(ok)
+    dist.destroy_process_group()
+
+
+def test_sharded_gpu_shards_equal_oracle():
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m:
+        out = m.dict()
+        procs = [ctx.Process(target=_worker, args=(r, 2, port, out)) for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(300)
+        assert all(p.exitcode == 0 for p in procs)
+        assert dict(out) == {0: True, 1: True}
