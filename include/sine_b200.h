@@ -155,6 +155,19 @@ int sine_kernel_launches(sine_index_t *h, int64_t *n);
  * buffers overflowed and were re-run on the list-keeping kernels.  Not in
  * the reference (diagnostic for the batched path, like sine_uncertified). */
 int sine_gemm_overflows(sine_index_t *h, int64_t *n);
+/* Float-hex text of row blocks, byte-identical to the reference's
+ * snapshot / record writers (" ".join(float(c).hex() ...), index.py:343-346,
+ * model.py:237) and read back bit-exactly like float.fromhex (index.py:370,
+ * model.py:263).  Host-only, multi-threaded, no device needed.
+ *   sine_hex_format: n lines "[<id> ]<hex> ... <hex>\n" (ids may be NULL);
+ *     out must hold sine_hex_bound(n, d, ids != NULL) bytes; *len = bytes.
+ *   sine_hex_parse: n such lines (ids NULL: no id field) -> ids, rows [n][d];
+ *     a malformed line -> SINE_EINVAL naming it. */
+int64_t sine_hex_bound(int64_t n, int64_t d, int with_ids);
+int sine_hex_format(const int64_t *ids, const double *rows, int64_t n, int64_t d,
+                    char *out, int64_t cap, int64_t *len);
+int sine_hex_parse(const char *text, int64_t len, int64_t n, int64_t d, int64_t *ids,
+                   double *rows);
 /* Enqueue a device copy of the last query's per-query exactness
  * certificates (B bytes, 1 = exact) -- lets a pipelined caller check them
  * later instead of synchronising after every batch. */

@@ -72,6 +72,11 @@ _SIGS = {
                                         ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "sine_kernel_launches": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
     "sine_gemm_overflows": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
+    "sine_hex_bound": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
+    "sine_hex_format": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_int64, _i64p]),
+    "sine_hex_parse": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_void_p, ctypes.c_void_p]),
     "sine_uncertified": (ctypes.c_int, [ctypes.c_void_p, _i64p]),
     "sine_copy_certificates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "sine_timing_totals": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _f64p, _i64p, ctypes.c_int]),
@@ -151,3 +156,30 @@ class PinnedArray:
         if p is not None and p.value and _lib is not None:
             _lib.sine_host_free(p)
             self._p = None
+
+
+def hex_format(rows: np.ndarray, ids=None) -> memoryview:
+    """Float-hex text of a row block ("[<id> ]<hex> ...\\n" per row), byte-
+    identical to the reference's float.hex writers (native, multi-threaded)."""
+    lib = load_library()
+    rows = f64(rows)
+    n, d = rows.shape
+    ids_a = i64(ids) if ids is not None else None
+    cap = lib.sine_hex_bound(n, d, 1 if ids_a is not None else 0)
+    out = np.empty(max(cap, 1), dtype=np.uint8)
+    ln = ctypes.c_int64()
+    check(lib.sine_hex_format(ids_a.ctypes.data if ids_a is not None else None, rows.ctypes.data, n, d,
+                              out.ctypes.data, cap, ctypes.byref(ln)))
+    return memoryview(out)[:ln.value]  # no copy: file writes and bytes() take it as is
+
+
+def hex_parse(text: bytes, n: int, d: int, with_ids: bool, offset: int = 0):
+    """Inverse of hex_format over text[offset:]: (ids int64[n] or None,
+    rows float64[n, d]).  `text` is read in place (no copy)."""
+    lib = load_library()
+    rows = np.empty((n, d), dtype=np.float64)
+    ids = np.empty(n, dtype=np.int64) if with_ids else None
+    base = ctypes.cast(ctypes.c_char_p(text), ctypes.c_void_p).value
+    check(lib.sine_hex_parse(base + offset, len(text) - offset, n, d,
+                             ids.ctypes.data if ids is not None else None, rows.ctypes.data))
+    return ids, rows

@@ -33,6 +33,7 @@
 #include "../../include/sine_b200.h"
 #include "common.cuh"
 #include "evict.cuh"
+#include "hexio.cuh"
 #include "merge.cuh"
 #include "scan.cuh"
 #include "umma.cuh"
@@ -1893,6 +1894,27 @@ int sine_gemm_overflows(sine_index_t* h, int64_t* n) {
 
 int sine_kernel_launches(sine_index_t* h, int64_t* n) {
     return guarded([&] { *n = h->launches; });
+}
+
+int64_t sine_hex_bound(int64_t n, int64_t d, int with_ids) {
+    return n * ((with_ids ? hexio::kMaxId : 0) + d * (hexio::kMaxTok + 1) + 1);
+}
+
+int sine_hex_format(const int64_t* ids, const double* rows, int64_t n, int64_t d, char* out, int64_t cap,
+                    int64_t* len) {
+    return guarded([&] {
+        if (n < 0 || d < 1) fail(SINE_EINVAL, "bad row block shape");
+        if (cap < sine_hex_bound(n, d, ids != nullptr)) fail(SINE_EINVAL, "output buffer below sine_hex_bound");
+        *len = n ? hexio::format_rows(ids, rows, n, d, out) : 0;
+    });
+}
+
+int sine_hex_parse(const char* text, int64_t len, int64_t n, int64_t d, int64_t* ids, double* rows) {
+    return guarded([&] {
+        if (n < 0 || d < 1) fail(SINE_EINVAL, "bad row block shape");
+        const std::string err = hexio::parse_rows(text, len, n, d, ids, rows);
+        if (!err.empty()) fail(SINE_EINVAL, "snapshot " + err);
+    });
 }
 
 int sine_host_alloc(size_t bytes, void** p) {

@@ -307,26 +307,42 @@ class GpuCosineIndex:
     def snapshot_lines(self) -> list[str]:
         """Reference snapshot format (index.py:340-354): header + one line of
         float-hex components per id, in slot order."""
+        return self.snapshot_bytes().decode().split("\n")[:-1]
+
+    def snapshot_bytes(self) -> bytes:
+        """The reference snapshot file (index.py:340-354, _write_snapshot
+        :376-379) as bytes: the rows are gathered on the device and the
+        float-hex body is formatted natively (byte-identical text)."""
+        head, body = self._snapshot_parts()
+        return head + bytes(body)
+
+    def _snapshot_parts(self):
         ids = self.ids()
-        rows = self.rows(ids)
-        lines = [self.SNAPSHOT_MAGIC, f"dimension: {self.dimension}", f"seed: {self.seed}",
-                 f"count: {len(ids)}"]
-        for i, r in zip(ids, rows):
-            lines.append(f"{i} " + " ".join(float(c).hex() for c in r))
-        return lines
+        head = "\n".join([self.SNAPSHOT_MAGIC, f"dimension: {self.dimension}", f"seed: {self.seed}",
+                          f"count: {len(ids)}"]) + "\n"
+        body = N.hex_format(self.rows(ids), ids) if ids else memoryview(b"")
+        return head.encode(), body
 
     def save(self, path: str) -> None:
-        with open(path, "w", encoding="utf-8") as fh:
-            fh.write("\n".join(self.snapshot_lines()) + "\n")
+        head, body = self._snapshot_parts()
+        with open(path, "wb") as fh:
+            fh.write(head)
+            fh.write(body)
+
+    def write_snapshot(self, fh) -> None:
+        """Append the snapshot to an open binary file (engine state files)."""
+        head, body = self._snapshot_parts()
+        fh.write(head)
+        fh.write(body)
 
     @classmethod
     def load(cls, path: str, **kwargs) -> "GpuCosineIndex":
-        with open(path, "r", encoding="utf-8") as fh:
-            lines = fh.read().splitlines()
-        dimension, seed, entries = parse_snapshot_lines(lines, cls.SNAPSHOT_MAGIC)
+        with open(path, "rb") as fh:
+            data = fh.read()
+        dimension, seed, ids, rows = parse_snapshot_bytes(data, cls.SNAPSHOT_MAGIC)
         idx = cls(dimension, seed=seed, **kwargs)
-        if entries:
-            idx.insert_batch([e[0] for e in entries], np.stack([e[1] for e in entries]))
+        if len(ids):
+            idx.insert_batch(ids, rows)
         return idx
 
 
@@ -349,6 +365,30 @@ def parse_snapshot_lines(lines: list[str], magic: str):
         vec = np.array([float.fromhex(p) for p in rest.split(" ")]) if rest else np.zeros(0)
         entries.append((int(head), vec))
     return dimension, seed, entries
+
+
+def parse_snapshot_bytes(data: bytes, magic: str):
+    """Native reader for the reference snapshot format (index.py:357-373):
+    header lines parsed here, the float-hex body by the library.  Returns
+    (dimension, seed, ids int64[count], rows float64[count, dimension])."""
+    head, off = [], 0
+    for _ in range(4):  # header lines only; the body is parsed in place
+        nl = data.find(b"\n", off)
+        head.append(data[off:] if nl < 0 else data[off:nl])
+        off = len(data) if nl < 0 else nl + 1
+    if head[0].decode(errors="replace") != magic:
+        raise ValidationError(f"snapshot is not a {magic} file")
+    try:
+        dimension = int(head[1].split(b":", 1)[1])
+        seed = int(head[2].split(b":", 1)[1])
+        count = int(head[3].split(b":", 1)[1])
+    except (IndexError, ValueError) as exc:
+        raise ValidationError(f"malformed snapshot header: {exc}") from exc
+    if count and dimension >= 1:
+        ids, rows = N.hex_parse(data, count, dimension, True, offset=off)
+    else:
+        ids, rows = np.empty(0, dtype=np.int64), np.empty((0, max(dimension, 0)))
+    return dimension, seed, ids, rows
 
 
 def _meta_struct(meta: dict, n: int):

@@ -115,3 +115,68 @@ def test_merge_topk_orders_like_reference():
     assert i.tolist() == [[3, 8, 4, 2]] and c.tolist() == [4]
     i, s, c = merge_topk(sims[:, :, :1] * 0 - 1, ids[:, :, :1] * 0 - 1, 2)
     assert i.tolist() == [[-1, -1]] and c.tolist() == [0]
+
+
+def _special_values():
+    import math
+    import struct
+    vals = [0.0, -0.0, 1.0, -1.0, 0.5, 5e-324, -5e-324, 2.2250738585072014e-308, 2.225073858507201e-308,
+            1.7976931348623157e308, -1.7976931348623157e308, math.inf, -math.inf, math.nan, 1e-300, 123456.789,
+            0.1, 1 / 3, 2.0 ** 1023, 2.0 ** -1022, 2.0 ** -1074]
+    vals.append(struct.unpack("<d", struct.pack("<Q", 0x7ff8000000000001 | (1 << 63)))[0])  # -nan
+    return vals
+
+
+def test_native_hex_matches_python_float_hex():
+    """sine_hex_format is byte-identical to " ".join(float(c).hex() ...)
+    (reference index.py:343-346, model.py:237), including zeros, signed
+    zero, subnormals, extremes, inf and nan; ids print like str(int)."""
+    from paper_2509_17360_b200 import _native as N
+    rng = np.random.default_rng(0)
+    rows = np.concatenate([rng.standard_normal((50, 7)) * 10.0 ** rng.integers(-300, 300, (50, 7)),
+                           np.array(_special_values()[:21]).reshape(3, 7)])
+    ids = rng.integers(-2 ** 62, 2 ** 62, rows.shape[0])
+    ids[0], ids[1] = 0, -1
+    want = "".join(f"{i} " + " ".join(float(c).hex() for c in r) + "\n" for i, r in zip(ids.tolist(), rows))
+    assert bytes(N.hex_format(rows, ids)).decode() == want
+    want_noid = "".join(" ".join(float(c).hex() for c in r) + "\n" for r in rows)
+    assert bytes(N.hex_format(rows)).decode() == want_noid
+    assert bytes(N.hex_format(np.array([[_special_values()[-1]]]))).decode() == "nan\n"
+
+
+def test_native_hex_parse_round_trip_and_errors():
+    from paper_2509_17360_b200 import _native as N
+    from paper_2509_17360_b200.errors import ValidationError
+    rng = np.random.default_rng(1)
+    rows = rng.standard_normal((600, 33))
+    rows[0, :5] = [0.0, -0.0, 5e-324, np.inf, -np.inf]
+    ids = rng.permutation(10 ** 6)[:600]
+    gi, gr = N.hex_parse(bytes(N.hex_format(rows, ids)), 600, 33, True)
+    assert gi.tolist() == ids.tolist()
+    assert gr.tobytes() == rows.tobytes()  # bit-exact, signed zero included
+    # non-canonical spellings float.fromhex accepts
+    _, r = N.hex_parse(b"0x1p-3 0X1.8P+1 -0x0.0p+0 inf\n", 1, 4, False)
+    assert r[0].tolist() == [float.fromhex("0x1p-3"), 3.0, -0.0, np.inf]
+    assert np.signbit(r[0, 2])
+    for bad in (b"1 0x1.0p+0 zz\n", b"1 0x1.0p+0\n", b"1 0x1.0p+0 0x1.0p+0 0x1.0p+0\n", b"x 0x1.0p+0 0x1.0p+0\n",
+                b"1 0x1.0p+0  0x1.0p+0\n"):
+        with pytest.raises(ValidationError):
+            N.hex_parse(bad, 1, 2, True)
+    with pytest.raises(ValidationError):  # fewer lines than the count
+        N.hex_parse(b"1 0x1.0p+0 0x1.0p+0\n", 2, 2, True)
+
+
+def test_snapshot_bytes_parse_matches_reference_reader():
+    """parse_snapshot_bytes reads the reference's own snapshot text (built
+    here with the reference format's float.hex lines) bit-exactly."""
+    from paper_2509_17360_b200.index import parse_snapshot_bytes, parse_snapshot_lines
+    rng = np.random.default_rng(2)
+    rows = rng.standard_normal((40, 6))
+    lines = ["exact-cosine-index", "dimension: 6", "seed: 3", "count: 40"]
+    lines += [f"{i * 7} " + " ".join(float(c).hex() for c in r) for i, r in enumerate(rows)]
+    text = "\n".join(lines) + "\n"
+    d, s, ids, got = parse_snapshot_bytes(text.encode(), "exact-cosine-index")
+    d2, s2, entries = parse_snapshot_lines(text.splitlines(), "exact-cosine-index")
+    assert (d, s) == (d2, s2) == (6, 3)
+    assert ids.tolist() == [e[0] for e in entries]
+    assert got.tobytes() == np.stack([e[1] for e in entries]).tobytes()
