@@ -466,10 +466,11 @@ def measure_persistence(rows, n=200_000):
     d = rows.shape[1]
     idx = GpuCosineIndex(d, scan="fp32", capacity=n)
     idx.insert_batch(np.arange(n) + 1, rows[:n], _checked=True)
-    idx.snapshot_bytes()  # warm
+    idx._snapshot_parts()  # warm
     t0 = time.perf_counter()
-    data = idx.snapshot_bytes()
+    head, body = idx._snapshot_parts()  # exactly what save() hands to the file
     save_s = time.perf_counter() - t0
+    data = head + bytes(body)
     t0 = time.perf_counter()
     dim, seed, ids, got = parse_snapshot_bytes(data, GpuCosineIndex.SNAPSHOT_MAGIC)
     back = GpuCosineIndex(dim, seed=seed, scan="fp32", capacity=n)
