@@ -198,11 +198,19 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # SINE_BENCH_GLOO_1GPU=1: a functional check of the N > 1 flow on a
+    # one-GPU box (every rank on cuda:0, gloo collectives); not a bench number
+    one_gpu = os.environ.get("SINE_BENCH_GLOO_1GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm_peak, tensor_peak, peak_kind = peaks()
 
     rows = make_rows(args.rows, DIM)
@@ -224,19 +232,19 @@ def run_ours(args):
     # launches onto it, and the CUDA events below time exactly that stream
     work = torch.cuda.Stream()
     torch.cuda.set_stream(work)
+    # exactness certificates are logged on the device per step and all
+    # checked after the timed loop (no per-step host sync); a failing one
+    # would be re-run and reported
+    cert_log = torch.zeros((nsteps, b), dtype=torch.uint8, device=q_dev.device)
     if world > 1:
         from paper_2509_17360_b200.sharded import ShardedCosineIndex
         sh = ShardedCosineIndex(idx)
         sh._rows = [(r + 1) * args.rows // world - r * args.rows // world for r in range(world)]
 
-        def step(s):
-            sh.query_device(q_dev[s], K, TAU)
+        def step(s):  # local scan -> one NCCL all-gather -> device shard merge
+            sh.query_device(q_dev[s], K, TAU, certify=False, cert_out=cert_log[s])
     else:
         stream = work.cuda_stream
-        # exactness certificates are logged on the device per step and all
-        # checked after the timed loop (no per-step host sync); a failing
-        # one would be re-run and reported
-        cert_log = torch.zeros((nsteps, b), dtype=torch.uint8, device=q_dev.device)
 
         def step(s):
             idx.query_device(b, q_dev[s].data_ptr(), K, TAU, ids_d.data_ptr(), sims_d.data_ptr(),
@@ -257,10 +265,20 @@ def run_ours(args):
     idx.timing_totals(0, reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        t_spin = time.perf_counter()
-        while time.perf_counter() - t_spin < 1.0:  # sampler start-up; GPU kept busy, untimed
-            step(s % max(args.warmup, 1))
+        # sampler start-up: GPU kept busy ~1 s, untimed.  With N > 1 every
+        # step is a collective, so all ranks run the same (rank-0-timed) count
+        t_spin, n_spin = time.perf_counter(), 0
+        while True:
+            step(n_spin % max(args.warmup, 1))
             torch.cuda.synchronize()
+            n_spin += 1
+            more = time.perf_counter() - t_spin < 1.0
+            if world > 1:
+                go = torch.tensor([1 if more else 0], device=q_dev.device)
+                dist.broadcast(go, 0)
+                more = bool(go.item())
+            if not more:
+                break
         idx.timing_totals(0, reset=True)
         idx.timing_totals(1, reset=True)
         launches0 = idx.kernel_launches()
@@ -271,10 +289,9 @@ def run_ours(args):
         ev1.record()
         barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    uncertified = 0
+    bad = (cert_log[args.warmup:] == 0).nonzero()
+    uncertified = int(bad.shape[0])
     if world == 1:
-        bad = (cert_log[args.warmup:] == 0).nonzero()
-        uncertified = int(bad.shape[0])
         for s_, j_ in bad.tolist():  # outside the timed region: the exact fp32 re-run
             idx.query_batch(qs[args.warmup + s_][j_:j_ + 1], K, TAU, cuda_core=True)
     scan_ms, scan_n = idx.timing_totals(0, reset=False)
@@ -302,7 +319,7 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):  # dram bytes per launch from the committed ncu --set full capture
         t = json.load(open(tpath)).get(kernel_name)
-        if t and args.scan == "fp32" and b == 1 and args.rows == N_ROWS:
+        if t and args.scan == "fp32" and b == 1 and shard_rows == N_ROWS:
             traffic = t["dram_bytes_per_launch"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -155,6 +155,16 @@ int sine_kernel_launches(sine_index_t *h, int64_t *n);
  * buffers overflowed and were re-run on the list-keeping kernels.  Not in
  * the reference (diagnostic for the batched path, like sine_uncertified). */
 int sine_gemm_overflows(sine_index_t *h, int64_t *n);
+/* Row-sharded stage-1 (one process per GPU): merge the P per-rank exact
+ * top-k lists of B queries -- the all-gather output on the device, rank r's
+ * [B][k] ids / sims at r * rank_stride elements (0 = B * k), id -1 =
+ * padding -- into the global top-k by (similarity desc, id asc), the
+ * order of index.py:45.  Device pointers, enqueued on `stream`.  Because
+ * each rank's list is its shard's exact top-k, the result equals an
+ * unsharded sine_query. */
+int sine_merge_shards(int device, int P, int64_t B, int k, const int64_t *ids_dev,
+                      const double *sims_dev, int64_t rank_stride, int64_t *out_ids,
+                      double *out_sims, int32_t *out_counts, void *stream);
 /* Float-hex text of row blocks, byte-identical to the reference's
  * snapshot / record writers (" ".join(float(c).hex() ...), index.py:343-346,
  * model.py:237) and read back bit-exactly like float.fromhex (index.py:370,

@@ -1896,6 +1896,25 @@ int sine_kernel_launches(sine_index_t* h, int64_t* n) {
     return guarded([&] { *n = h->launches; });
 }
 
+int sine_merge_shards(int device, int P, int64_t B, int k, const int64_t* ids_dev, const double* sims_dev,
+                      int64_t rank_stride, int64_t* out_ids, double* out_sims, int32_t* out_counts, void* stream) {
+    return guarded([&] {
+        if (P < 1 || B < 0 || k < 1) fail(SINE_EINVAL, "bad shard merge shape");
+        if (B == 0) return;
+        const size_t smem = static_cast<size_t>(P) * k * 16;
+        if (smem > 160 * 1024) fail(SINE_EINVAL, "P * k too large for the shard merge");
+        CK(cudaSetDevice(device));
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(shard_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            attr = true;
+        }
+        shard_merge_kernel<<<static_cast<unsigned>(B), kShardMergeThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+            ids_dev, sims_dev, P, B, k, rank_stride ? rank_stride : B * k, out_ids, out_sims, out_counts);
+        CK(cudaGetLastError());
+    });
+}
+
 int64_t sine_hex_bound(int64_t n, int64_t d, int with_ids) {
     return n * ((with_ids ? hexio::kMaxId : 0) + d * (hexio::kMaxTok + 1) + 1);
 }

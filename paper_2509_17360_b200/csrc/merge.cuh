@@ -257,3 +257,51 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
 }
 
 }  // namespace sine
+
+namespace sine {
+
+// Row-sharded stage-1: merge the P per-rank exact top-k lists of each query
+// (the all-gather output: rank r's [B][k] block at r * rank_stride, id -1 =
+// padding) into the global top-k
+// with the reference comparator (similarity desc, id asc; index.py:45).
+// One CTA per query; entries are ranked in shared memory.
+constexpr int kShardMergeThreads = 128;
+
+__global__ void __launch_bounds__(kShardMergeThreads)
+    shard_merge_kernel(const int64_t* ids, const double* sims, int P, int64_t B, int k, int64_t rank_stride,
+                       int64_t* out_ids, double* out_sims, int32_t* out_counts) {
+    extern __shared__ uint8_t sm_raw[];
+    const int m = P * k;
+    double* ss = reinterpret_cast<double*>(sm_raw);
+    int64_t* si = reinterpret_cast<int64_t*>(ss + m);
+    __shared__ int nvalid;
+    const int64_t q = blockIdx.x;
+    if (threadIdx.x == 0) nvalid = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {
+        const int r = e / k, j = e - r * k;
+        const size_t o = static_cast<size_t>(r) * rank_stride + static_cast<size_t>(q) * k + j;
+        si[e] = ids[o];
+        ss[e] = sims[o];
+        if (ids[o] >= 0) atomicAdd(&nvalid, 1);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {
+        if (si[e] < 0) continue;
+        int rnk = 0;
+        for (int f = 0; f < m; ++f)
+            if (si[f] >= 0 && cand_before64(ss[f], si[f], ss[e], si[e])) ++rnk;
+        if (rnk < k) {
+            out_ids[q * k + rnk] = si[e];
+            out_sims[q * k + rnk] = ss[e];
+        }
+    }
+    const int n = min(nvalid, k);
+    for (int r = n + threadIdx.x; r < k; r += blockDim.x) {
+        out_ids[q * k + r] = -1;
+        out_sims[q * k + r] = 0.0;
+    }
+    if (threadIdx.x == 0) out_counts[q] = n;
+}
+
+}  // namespace sine

@@ -20,6 +20,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _native as N
 from .errors import ValidationError
 
 
@@ -109,19 +110,37 @@ class ShardedCosineIndex:
         mi, ms, mc = merge_topk(g_sims.view(self.world, B, k), g_ids.view(self.world, B, k), k)
         return mi.cpu().numpy(), ms.cpu().numpy(), mc.cpu().numpy()
 
-    def query_device(self, q: torch.Tensor, k: int, min_similarity: float = -1.0):
-        """Device-resident variant (NCCL): q is a CUDA float64 [B, d] tensor;
-        the local scan is enqueued on torch's current stream, so the
-        all-gather and the merge follow it without a host round trip."""
+    def query_device(self, q: torch.Tensor, k: int, min_similarity: float = -1.0, *, certify: bool = True,
+                     cert_out: torch.Tensor | None = None):
+        """Device-resident variant (NCCL): q is a CUDA float64 [B, d] tensor.
+        The local scan writes ids and similarity bits into one int64 block
+        [2, B, k] on torch's current stream; ONE all-gather moves every
+        rank's block and the library's shard-merge kernel produces the
+        global top-k -- no host round trip.  certify=False skips the
+        per-call certificate sync; pass cert_out (uint8 [B], device) to log
+        the local certificates for a later check."""
         B = q.shape[0]
         stream = torch.cuda.current_stream().cuda_stream
-        ids = torch.empty((B, k), dtype=torch.int64, device=q.device)
-        sims = torch.empty((B, k), dtype=torch.float64, device=q.device)
+        block = torch.empty((2, B, k), dtype=torch.int64, device=q.device)
         counts = torch.empty((B,), dtype=torch.int32, device=q.device)
-        self.local.query_device(B, q.data_ptr(), k, min_similarity, ids.data_ptr(), sims.data_ptr(),
-                                counts.data_ptr(), stream)
-        g_ids = torch.empty((self.world * B, k), dtype=torch.int64, device=q.device)
-        g_sims = torch.empty((self.world * B, k), dtype=torch.float64, device=q.device)
-        dist.all_gather_into_tensor(g_ids, ids, group=self.group)
-        dist.all_gather_into_tensor(g_sims, sims, group=self.group)
-        return merge_topk(g_sims.view(self.world, B, k), g_ids.view(self.world, B, k), k)
+        self.local.query_device(B, q.data_ptr(), k, min_similarity, block[0].data_ptr(), block[1].data_ptr(),
+                                counts.data_ptr(), stream, certify=certify)
+        if cert_out is not None:
+            self.local.copy_certificates(B, cert_out.data_ptr(), stream)
+        g = torch.empty((self.world, 2, B, k), dtype=torch.int64, device=q.device)
+        dist.all_gather_into_tensor(g.view(-1), block.view(-1), group=self.group)
+        return merge_gathered_blocks(g)
+
+
+def merge_gathered_blocks(g: torch.Tensor):
+    """g: CUDA int64 [P, 2, B, k] -- per rank, ids then similarity bits (the
+    all-gather of ShardedCosineIndex.query_device's blocks).  One device
+    kernel (sine_merge_shards) -> (ids [B, k] -1 padded, sims, counts)."""
+    P, _, B, k = g.shape
+    out_ids = torch.empty((B, k), dtype=torch.int64, device=g.device)
+    out_sims = torch.empty((B, k), dtype=torch.float64, device=g.device)
+    out_cnt = torch.empty((B,), dtype=torch.int32, device=g.device)
+    N.check(N.load_library().sine_merge_shards(g.device.index, P, B, k, g.data_ptr(), g[0, 1].data_ptr(), 2 * B * k,
+                                               out_ids.data_ptr(), out_sims.data_ptr(), out_cnt.data_ptr(),
+                                               torch.cuda.current_stream().cuda_stream))
+    return out_ids, out_sims, out_cnt

@@ -67,3 +67,46 @@ def test_sharded_gpu_shards_equal_oracle():
             p.join(300)
         assert all(p.exitcode == 0 for p in procs)
         assert dict(out) == {0: True, 1: True}
+
+
+def test_device_shard_merge_equals_unsharded():
+    """The query_device data path on one GPU: P shard indexes produce their
+    [2, B, k] blocks (ids + similarity bits) exactly as each rank would, the
+    blocks are stacked as the all-gather would lay them out, and the
+    library's shard-merge kernel must equal the unsharded index (ids
+    bit-exact, fp64 similarities identical), ties across shards included."""
+    import torch
+    sys.path.insert(0, ROOT)
+    from paper_2509_17360_b200 import GpuCosineIndex
+    from paper_2509_17360_b200.sharded import merge_gathered_blocks, merge_topk
+    rng = np.random.default_rng(4)
+    n, d, B = 24000, 128, 64
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    rows[500:520] = rows[3]  # identical rows land on every shard
+    ids = rng.permutation(10 * n)[:n]
+    full = GpuCosineIndex(d)
+    full.insert_batch(ids, rows)
+    q = rows[rng.integers(0, n, B)] + 0.3 * rng.standard_normal((B, d))
+    q[0] = rows[3]
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    qd = torch.from_numpy(q).cuda()
+    for P in (2, 3, 8):
+        shards = [GpuCosineIndex(d) for _ in range(P)]
+        for r in range(P):
+            shards[r].insert_batch(ids[r::P], rows[r::P])
+        for k, ms in ((10, -1.0), (7, 0.2), (16, 0.9)):
+            blocks = []
+            for sh in shards:
+                blk = torch.empty((2, B, k), dtype=torch.int64, device="cuda")
+                cnt = torch.empty((B,), dtype=torch.int32, device="cuda")
+                sh.query_device(B, qd.data_ptr(), k, ms, blk[0].data_ptr(), blk[1].data_ptr(), cnt.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream)
+                blocks.append(blk)
+            gi, gs, gc = merge_gathered_blocks(torch.stack(blocks))
+            ti, ts, tc = merge_topk(torch.stack([b[1].view(torch.float64) for b in blocks]),
+                                    torch.stack([b[0] for b in blocks]), k)
+            wi, ws, wc = full.query_batch(q, k, ms)
+            assert gi.cpu().numpy().tolist() == wi.tolist() == ti.cpu().numpy().tolist()
+            assert gc.cpu().numpy().tolist() == wc.tolist()
+            np.testing.assert_array_equal(gs.cpu().numpy(), ws)
