@@ -356,13 +356,18 @@ def run_ours(args):
         for s in range(args.warmup):
             qh.array[:] = qs[s]
             idx.query_into(qh.array, K, TAU, oi.array, os_.array, oc.array)
+        lat = []
         t0 = time.perf_counter()
         for s in range(args.warmup, nsteps):
+            t1 = time.perf_counter()
             qh.array[:] = qs[s]
             idx.query_into(qh.array, K, TAU, oi.array, os_.array, oc.array)
+            lat.append(time.perf_counter() - t1)
         t_e2e = time.perf_counter() - t0
+        lat_ms = np.array(lat) * 1e3
         e2e = {"value": b * args.steps / t_e2e, "unit": "lookups/s", "h2d_bytes_per_step": b * DIM * 8,
                "d2h_bytes_per_step": b * K * 16 + b * 4,
+               "latency_ms": {"p50": float(np.percentile(lat_ms, 50)), "p99": float(np.percentile(lat_ms, 99))},
                "api": "GpuCosineIndex.query_into (sine_query C ABI), pinned host buffers"}
 
     regimes = []
