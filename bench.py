@@ -815,21 +815,25 @@ def measure_trace(rows, n_ops=2000, cpu_ops=24):
     shared = M.EmbeddingVector((1.0,))
     out = {"workload": f"config E: {n} SEs x d={d}, 80% lookup (70% Zipf reuse) / 15% admit at capacity / "
                        f"5% evict_until_fits, constant-time judge stub"}
-    for batched in (False, True):
-        ops = trace_ops(n, d, n_ops, rng, rows)
-        emb = _DictEmbedder(d)
-        els = _make_elements(M, n, meta, shared)
-        usage = int(meta["size"].sum())
-        eng = P.CacheEngine(P.CacheConfig(capacity_tokens=usage), emb, _TextJudge())
-        eng.bulk_admit(els, rows, now=0.0)
-        run_trace(eng, ops[:50], emb, M, 1.0, batched)  # warm-up
-        t0 = time.perf_counter()
-        done = run_trace(eng, ops[50:], emb, M, 2.0, batched)
-        dt = time.perf_counter() - t0
-        out["batched_ops_per_s" if batched else "ops_per_s"] = done / dt
-        st = eng.stats()
-        out["hit_rate" if not batched else "hit_rate_batched"] = st["hits"] / max(1, st["lookups"])
-        del eng, els
+    # exact fp32 mode, and bf16 fast mode (fp64 re-rank + certificate with the
+    # fp32 fallback, so the answers are the same), each one call per op and
+    # with consecutive lookups batched
+    for scan, sfx in (("fp32", ""), ("bf16", "_bf16")):
+        for batched in (False, True):
+            ops = trace_ops(n, d, n_ops, rng, rows)
+            emb = _DictEmbedder(d)
+            els = _make_elements(M, n, meta, shared)
+            usage = int(meta["size"].sum())
+            eng = P.CacheEngine(P.CacheConfig(capacity_tokens=usage), emb, _TextJudge(), scan=scan)
+            eng.bulk_admit(els, rows, now=0.0)
+            run_trace(eng, ops[:50], emb, M, 1.0, batched)  # warm-up
+            t0 = time.perf_counter()
+            done = run_trace(eng, ops[50:], emb, M, 2.0, batched)
+            dt = time.perf_counter() - t0
+            out[("batched_ops_per_s" if batched else "ops_per_s") + sfx] = done / dt
+            st = eng.stats()
+            out[("hit_rate_batched" if batched else "hit_rate") + sfx] = st["hits"] / max(1, st["lookups"])
+            del eng, els
     # CPU: the reference engine loop on the same population (bounded sample)
     from oracle import sine_oracle as O
     ops = trace_ops(n, d, cpu_ops, rng, rows)

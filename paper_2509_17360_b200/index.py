@@ -85,8 +85,8 @@ class GpuCosineIndex:
         self.device = device
         self.scan = scan
         self.rerank = rerank
-        if store_f32 is None:
-            store_f32 = scan == "fp32"
+        if store_f32 is None:  # bf16 + re-rank keeps fp32 rows: the certificate's exact fallback
+            store_f32 = scan == "fp32" or rerank
         if store_bf16 is None:
             store_bf16 = scan == "bf16"
         flags = (N.STORE_F32 if store_f32 else 0) | (N.STORE_BF16 if store_bf16 else 0) | \
