@@ -38,6 +38,7 @@ struct SelectState {
     int64_t rem;      // weight still needed inside the prefix bucket
     int64_t count;    // candidates matching the prefix
     int64_t total_w;  // first pass: live weight
+    int64_t below;    // candidates strictly below the chosen bucket (all of them when done == 2)
 };
 
 __device__ __forceinline__ double lcfu_score(const EvictCols& c, int64_t s, double now) {
@@ -226,19 +227,22 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
 __global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsigned long long* hw,
                                                          unsigned long long* hc, unsigned long long* hand,
                                                          unsigned long long* hor, int first) {
-    __shared__ unsigned long long cw[256];
+    __shared__ unsigned long long cw[256], cc[256];
     __shared__ int chosen;
     __shared__ unsigned long long before_w;
     const int t = threadIdx.x;
     if (st->done) return;
     cw[t] = hw[t];
+    cc[t] = hc[t];
     if (t == 0) chosen = -1;
     __syncthreads();
     // inclusive scan (Hillis-Steele, 256 entries)
     for (int o = 1; o < 256; o <<= 1) {
         const unsigned long long v = t >= o ? cw[t - o] : 0ull;
+        const unsigned long long u = t >= o ? cc[t - o] : 0ull;
         __syncthreads();
         cw[t] += v;
+        cc[t] += u;
         __syncthreads();
     }
     const long long rem = st->rem;
@@ -253,7 +257,9 @@ __global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsign
         if (chosen < 0) {
             // the excess is at least the whole candidate weight: all are victims
             st->done = 2;
+            st->below = static_cast<int64_t>(cc[255]);
         } else {
+            st->below = chosen ? static_cast<int64_t>(cc[chosen - 1]) : 0;
             const int nd = st->ndigits;
             st->prefix[nd >> 3] |= static_cast<uint64_t>(chosen) << (8 * (7 - (nd & 7)));
             st->rem = rem - static_cast<long long>(before_w);
@@ -344,6 +350,10 @@ __global__ void __launch_bounds__(256) collect_count_kernel(EvictCols c, const u
                                                             int mode, int32_t* counts, const uint64_t* rk = nullptr,
                                                             const int64_t* rn = nullptr) {
     __shared__ int32_t wsum[8];
+    if (mode == 2 && st->below == 0) {  // nothing below the record prefix (pass 1's histogram says so)
+        if (threadIdx.x == 0) counts[blockIdx.x] = 0;
+        return;
+    }
     const CollectPred pred = make_pred(c, k1, st, mode, rk);
     const int64_t n = rk ? *rn : c.nslots;
     const int64_t b = static_cast<int64_t>(blockIdx.x) * kColChunk;
@@ -372,6 +382,7 @@ __global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const u
                                                             const int32_t* rslot = nullptr,
                                                             const int64_t* base = nullptr) {
     __shared__ int32_t wtot[8];
+    if (mode == 2 && st->below == 0) return;
     const CollectPred pred = make_pred(c, k1, st, mode, rk);
     const int64_t n = rk ? *rn : c.nslots;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
