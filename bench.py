@@ -427,7 +427,7 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
     assert stream, "regimes must run on a non-default stream"
     cases = []
     for scan in ("fp32", "bf16"):
-        for b, reps in ((1, 20), (8, 10), (64, 5), (256, 5), (1024, 3), (4096, 3)):
+        for b, reps in ((1, 30), (8, 20), (64, 10), (256, 7), (1024, 5), (4096, 3)):
             for tau in (TAU, -1.0):
                 if b >= 256 and tau == -1.0 and b != 4096:
                     continue
@@ -452,13 +452,15 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                 run(True)
                 uncert = idx.uncertified()
                 torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(reps):
+                # events around every batch, back to back on the stream; the
+                # median per-batch time is robust to a one-off clock dip
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+                evs[0].record()
+                for r_ in range(reps):
                     run()
-                e1.record()
+                    evs[r_ + 1].record()
                 torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / reps
+                ms = float(np.median([evs[r_].elapsed_time(evs[r_ + 1]) for r_ in range(reps)]))
                 n = rows.shape[0]
                 byt = algorithmic_bytes(n, DIM, b, K, scan)
                 flops = 2.0 * n * DIM * b
