@@ -184,6 +184,9 @@ struct sine_index {
     DevBuf<uint64_t> rkeys;            // eviction candidate records: keys [n][3]
     DevBuf<int64_t> rsize, dcount;     // record sizes; device counters
     DevBuf<int32_t> rslot;             // record -> slot
+    DevBuf<uint64_t> rkeys2;           // the records after the first refinement pass
+    DevBuf<int64_t> rsize2;
+    DevBuf<int32_t> rslot2;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
     HostBuf<SelectState> st_h;
     HostBuf<unsigned long long> n_h;
@@ -1335,7 +1338,29 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     r.rsz = h->rsize.p;
     r.rn = nrec;
     const int grid_rec = grid_for(h->nlive, 256, h->num_sms);
-    for (int pass = 1; pass < 25; pass += 4) {
+    const int nbr = static_cast<int>((h->nlive + kColChunk - 1) / kColChunk);
+    h->scratch_i32.ensure(std::max(nb, nbr));
+    h->exp_off.ensure(std::max(nb, nbr) + 1);
+    // first refinement pass over the records, then shrink them once more to
+    // the records matching the longer prefix (typically ~1/256 of them): the
+    // remaining passes stream only those
+    evict_hist_kernel<<<grid_rec, 256, 0, st>>>(r);
+    evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 0);
+    h->rkeys2.ensure(3 * std::max<int64_t>(h->nlive, 1));
+    h->rsize2.ensure(std::max<int64_t>(h->nlive, 1));
+    h->rslot2.ensure(std::max<int64_t>(h->nlive, 1));
+    int64_t* nrec2 = h->dcount.p + 2;
+    collect_count_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 1, h->scratch_i32.p, h->rkeys.p, nrec);
+    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nbr, h->exp_off.p);
+    collect_write_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 1, h->exp_off.p, h->rkeys2.p, h->rslot2.p,
+                                              nullptr, nullptr, h->rsize2.p, h->rkeys.p, nrec, h->rslot.p);
+    CK(cudaMemcpyAsync(nrec2, h->exp_off.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    h->launches += 5;
+    CK(cudaGetLastError());
+    r.rk = h->rkeys2.p;
+    r.rsz = h->rsize2.p;
+    r.rn = nrec2;
+    for (int pass = 2; pass < 25; pass += 4) {
         for (int j = 0; j < 4; ++j) {
             evict_hist_kernel<<<grid_rec, 256, 0, st>>>(r);
             evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 0);
@@ -1358,9 +1383,6 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
                                              kor);
     CK(cudaMemcpyAsync(nbelow, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    const int nbr = static_cast<int>((h->nlive + kColChunk - 1) / kColChunk);
-    h->scratch_i32.ensure(std::max(nb, nbr));
-    h->exp_off.ensure(std::max(nb, nbr) + 1);
     collect_count_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->scratch_i32.p, h->rkeys.p, nrec);
     expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nbr, h->exp_off.p);
     collect_write_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
