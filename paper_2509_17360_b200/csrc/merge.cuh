@@ -210,7 +210,20 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
         for (int i = warp; i < m; i += kMergeThreads / 32) {
             const double* x = p.rows64 + static_cast<size_t>(sel_slot[i]) * p.dim;
             double a = 0.0;
-            for (int64_t t = lane; t < p.dim; t += 32) a = fma(__ldg(x + t), __ldg(q + t), a);
+            int64_t t = lane;
+            // same per-lane order as a plain strided loop (bit-identical
+            // sums), with 8 independent row loads in flight per lane
+            for (; t + 32 * 7 < p.dim; t += 32 * 8) {
+                double xv[8], qv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    xv[u] = __ldg(x + t + 32 * u);
+                    qv[u] = __ldg(q + t + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a = fma(xv[u], qv[u], a);
+            }
+            for (; t < p.dim; t += 32) a = fma(__ldg(x + t), __ldg(q + t), a);
             a = warp_sum64(a);
             if (lane == 0) sel_sim[i] = a + 0.0;
         }
