@@ -158,11 +158,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     } else {
         uint32_t nbefore, nequal;
         const uint32_t kstar = block_select<uint32_t>(
-            [&](int f, uint32_t& key) {
-                int c, e;
-                if (!flat_ok(f, c, e)) return false;
-                key = key_at(c, e);
-                return true;
+            [&](int f, uint32_t& key) {  // pool[f] == key_at(f / kp, f % kp), no division
+                key = pool[f];
+                return key != 0u;
             },
             nflat, static_cast<uint32_t>(kp), true, 32, hist, scratch, &nbefore, &nequal);
         if (threadIdx.x == 0) bound_key = kstar;
@@ -173,8 +171,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             uint32_t b2, e2;
             idcut = block_select<uint64_t>(
                 [&](int f, uint64_t& key) {
-                    int c, e;
-                    if (!flat_ok(f, c, e) || key_at(c, e) != kstar) return false;
+                    if (pool[f] != kstar) return false;
+                    const int c = f / kp, e = f - c * kp;
                     key = i64_key(__ldg(p.ids + slot_at(c, e)));
                     return true;
                 },
