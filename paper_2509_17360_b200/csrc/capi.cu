@@ -843,22 +843,23 @@ constexpr int kGemmChunks = 32;
 constexpr float kGemmMinFloor = 0.25f;  // below it the GEMM seeds per-query floors from a sample pass
 constexpr int kGemmSeedMinTiles = 8 * 64;  // row tiles a seeded GEMM needs (the sample is 1/8 of them)
 
-bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
-                     bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
-                     cudaStream_t st) {
+template <int NQ>
+bool umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                       bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                       cudaStream_t st) {
     const bool tf32 = !bf16;
     const int64_t row_elems = tf32 ? h->stride32 : h->stride16;
     const int64_t row_bytes = row_elems * (tf32 ? 4 : 2);
     const int kblocks = static_cast<int>(row_bytes / kUmmaKB);
     const int nrt = static_cast<int>((h->nslots + kGemmRows - 1) / kGemmRows);
-    const int nqt = static_cast<int>((B + kGemmNQ - 1) / kGemmNQ);
+    const int nqt = static_cast<int>((B + NQ - 1) / NQ);
     if (static_cast<int64_t>(nrt) * nqt >= (1ll << 31)) return false;
-    const int64_t Bpad = static_cast<int64_t>(nqt) * kGemmNQ;
-    const int S = static_cast<int>(std::min<size_t>(7, (227 * 1024 - gemm_smem_bytes(0)) / (2 * 128 * kUmmaKB)));
-    const size_t smem = gemm_smem_bytes(S);
+    const int64_t Bpad = static_cast<int64_t>(nqt) * NQ;
+    const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - gemm_smem_bytes(0, NQ)) / gemm_stage_bytes(NQ)));
+    const size_t smem = gemm_smem_bytes(S, NQ);
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        CK(cudaFuncSetAttribute(umma_gemm_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
     const int nitems = nrt * nqt;
@@ -872,7 +873,7 @@ bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
     h->n_h.ensure(1);
     const void* rows = tf32 ? static_cast<const void*>(h->rows32) : static_cast<const void*>(h->rows16);
     const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots, 128);
-    const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, Bpad, 128);
+    const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, Bpad, NQ / 2);
     res_prep_queries<<<grid_for(Bpad * row_elems, 256, h->num_sms), 256, 0, st>>>(
         q_dev, static_cast<int>(B), static_cast<int>(Bpad), h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
     CK(cudaMemsetAsync(h->gcnt.p, 0, (static_cast<size_t>(B) + 1) * sizeof(uint32_t), st));
@@ -905,7 +906,7 @@ bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
         sp.rt_stride = nrt / nrt_s;
         sp.out_max = h->tmax.p;
         const int sp_pairs = std::max(1, std::min(h->num_sms / 2, nrt_s * nqt));
-        umma_gemm_kernel<<<2 * sp_pairs, kGemmThreads, smem, st>>>(qmap, rmap, sp);
+        umma_gemm_kernel<NQ><<<2 * sp_pairs, kGemmThreads, smem, st>>>(qmap, rmap, sp);
         sample_max_bound_kernel<<<static_cast<int>(B), 256, 0, st>>>(h->tmax.p, 2 * nrt_s, static_cast<int>(B), kp,
                                                                      h->gbound.p);
         h->launches += 2;
@@ -913,7 +914,7 @@ bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
         p.qthr = h->gbound.p;
     }
     const size_t tk = tbegin(h, 2, st);
-    umma_gemm_kernel<<<2 * npairs, kGemmThreads, smem, st>>>(qmap, rmap, p);
+    umma_gemm_kernel<NQ><<<2 * npairs, kGemmThreads, smem, st>>>(qmap, rmap, p);
     tend(h, tk, st);
     CK(cudaGetLastError());
     gemm_finish_kernel<<<static_cast<int>((B + 255) / 256), 256, 0, st>>>(h->gcnt.p, static_cast<int>(B), kp,
@@ -927,6 +928,21 @@ bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
     merge_launch(h, kGemmChunks, static_cast<int>(B), kp, q_dev, k, min_sim, rerank, ids_dev, sims_dev, counts_dev,
                  st, 0);
     return true;
+}
+
+// Query tile width by batch: N = 64 / 128 / 256 per pair MMA, so small
+// batches do not pay for padded query columns (kind::tf32 runs at half rate).
+bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+                     bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
+                     cudaStream_t st) {
+    if (B <= 64)
+        return umma_gemm_query_t<64>(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev,
+                                     st);
+    if (B <= 128)
+        return umma_gemm_query_t<128>(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev,
+                                      counts_dev, st);
+    return umma_gemm_query_t<256>(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev,
+                                  st);
 }
 
 void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, double min_sim, bool bf16, bool rerank,

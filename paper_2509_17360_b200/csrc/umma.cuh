@@ -1374,7 +1374,7 @@ namespace sine {
 // (pkg/src/semcache/index.py:101, :43), for B queries at once.
 // ===========================================================================
 
-constexpr int kGemmNQ = 256;      // queries per item (MMA N)
+constexpr int kGemmNQ = 256;      // max queries per item (MMA N); the kernel is templated on NQ <= 256
 constexpr int kGemmRows = 256;    // rows per item (MMA M, 128 per CTA)
 constexpr int kGemmThreads = 192;
 
@@ -1396,8 +1396,11 @@ struct GemmParams {
     uint32_t* out_max;     // sample pass: [2 * t + rank][nq] max score key of the CTA's 128 rows
 };
 
-__host__ __device__ inline size_t gemm_smem_bytes(int S) {
-    return static_cast<size_t>(S) * 2 * 128 * kUmmaKB + (2 * S + 4) * sizeof(uint64_t) + 16 + 3 * 256 * 4 + 1024;
+// per stage and CTA: 128 rows + NQ/2 queries, 128 B of K each
+__host__ __device__ inline size_t gemm_stage_bytes(int NQ) { return static_cast<size_t>(128 + NQ / 2) * kUmmaKB; }
+
+__host__ __device__ inline size_t gemm_smem_bytes(int S, int NQ) {
+    return static_cast<size_t>(S) * gemm_stage_bytes(NQ) + (2 * S + 4) * sizeof(uint64_t) + 16 + 3 * 256 * 4 + 1024;
 }
 
 __device__ __forceinline__ void gemm_append(const GemmParams& p, int q, uint32_t key, int32_t slot) {
@@ -1415,12 +1418,13 @@ __device__ __forceinline__ void gemm_append(const GemmParams& p, int q, uint32_t
 // score key over this CTA's 128 rows -> [2t + rank][nq]) or for per-query
 // admission floors (qthr, staged in shared memory per item).  A 32-score
 // chunk of a row is skipped when its max is below the chunk's smallest floor.
+template <int NQ>
 __device__ __noinline__ void gemm_epilogue_general(const GemmParams& p, uint32_t tmem, int acc, int warp, int lane,
                                                    int tid, bool live, int64_t slot, int qbase, size_t orow,
                                                    uint32_t* colmax, float* fl, uint64_t* tfull, int i) {
     if (!p.out_max) {
         const uint32_t k0 = f32_key(p.thr0);
-        for (int j = tid; j < kGemmNQ; j += 128) {
+        for (int j = tid; j < NQ; j += 128) {
             const int q = qbase + j;
             fl[j] = q < p.nq ? key_f32(max(k0, __ldg(p.qthr + q))) : INFINITY;
         }
@@ -1431,9 +1435,9 @@ __device__ __noinline__ void gemm_epilogue_general(const GemmParams& p, uint32_t
     // chunks not unrolled and appends in a bit loop: keeps the code small
     // (an unrolled 256-site append body thrashes the instruction cache)
 #pragma unroll 1
-    for (int c = 0; c < kGemmNQ / 32; ++c) {
+    for (int c = 0; c < NQ / 32; ++c) {
         uint32_t r[32];
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * kGemmNQ + c * 32;
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * NQ + c * 32;
         SINE_TMEM_LD32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (p.out_max) {
@@ -1470,7 +1474,7 @@ __device__ __noinline__ void gemm_epilogue_general(const GemmParams& p, uint32_t
     }
     if (p.out_max) {
         named_bar_sync(2, 128);
-        for (int j = tid; j < kGemmNQ; j += 128) {
+        for (int j = tid; j < NQ; j += 128) {
             const int q = qbase + j;
             if (q < p.nq) p.out_max[orow * p.nq + q] = colmax[j];
             colmax[j] = 0u;
@@ -1479,16 +1483,18 @@ __device__ __noinline__ void gemm_epilogue_general(const GemmParams& p, uint32_t
     }
 }
 
+template <int NQ>
 __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
                      const __grid_constant__ GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages, nkb = p.kblocks;
-    constexpr size_t kStage = 128 * kUmmaKB;  // 16 KB: 128 rows (or queries) x 128 B of K
+    constexpr size_t kStage = 128 * kUmmaKB;        // 16 KB: 128 rows x 128 B of K
+    constexpr size_t kStageB = (NQ / 2) * kUmmaKB;  // this CTA's NQ/2 queries x 128 B of K
     uint8_t* sa = smem;
     uint8_t* sb = smem + S * kStage;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * S * kStage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * (kStage + kStageB));
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
@@ -1515,7 +1521,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
     }
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512));
+                     "r"(2 * NQ));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
@@ -1537,12 +1543,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
             for (int w = pair; w < nitems; w += npair) {
                 const int t = w / p.nqt, g = w - (w / p.nqt) * p.nqt;
                 const int r0 = t * p.rt_stride * kGemmRows + rank * 128;
-                const int q0 = g * kGemmNQ + rank * 128;
+                const int q0 = g * NQ + rank * (NQ / 2);
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(empty + s, ph ^ 1);
-                    if (rank == 0) mbar_arrive_expect_tx(full + s, 4u * static_cast<uint32_t>(kStage));
+                    if (rank == 0) mbar_arrive_expect_tx(full + s, 2u * static_cast<uint32_t>(kStage + kStageB));
                     tma_load_2d_pair(sa + s * kStage, &rmap, leader_addr(full + s), kb * kb_elems, r0, pol_rows);
-                    tma_load_2d_pair(sb + s * kStage, &qmap, leader_addr(full + s), kb * kb_elems, q0, pol_q);
+                    tma_load_2d_pair(sb + s * kStageB, &qmap, leader_addr(full + s), kb * kb_elems, q0, pol_q);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -1553,7 +1559,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
     } else if (warp == 5) {
         // ---------------- MMA issuer (leader only): D[256 rows, 256 queries] ----------------
         if (rank == 0 && lane == 0) {
-            const uint32_t idesc = umma_idesc(p.tf32, kGemmRows, kGemmNQ);
+            const uint32_t idesc = umma_idesc(p.tf32, kGemmRows, NQ);
             int s = 0;
             uint32_t ph = 0;
             int i = 0;
@@ -1561,12 +1567,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
                 const int acc = i & 1;
                 mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + acc * kGemmNQ;
+                const uint32_t d = tmem + acc * NQ;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(full + s, ph);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + s * kStage);
-                    const uint32_t b0 = smem_u32(sb + s * kStage);
+                    const uint32_t b0 = smem_u32(sb + s * kStageB);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t ad = umma_smem_desc(a0 + kk * 32);
@@ -1597,19 +1603,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
             const int64_t slot = static_cast<int64_t>(t) * p.rt_stride * kGemmRows + rank * 128 + tid;
             const uint32_t vw = slot < p.nslots ? __ldg(p.valid + (slot >> 5)) : 0u;
             const bool live = ((vw >> (slot & 31)) & 1u) != 0;
-            const int qbase = g * kGemmNQ;
+            const int qbase = g * NQ;
             if (p.out_max || p.qthr) {
                 // sample pass (per-query max over the rows) or per-query
                 // admission floors: the general, slower epilogue
-                gemm_epilogue_general(p, tmem, acc, warp, lane, tid, live, slot, qbase,
+                gemm_epilogue_general<NQ>(p, tmem, acc, warp, lane, tid, live, slot, qbase,
                                       static_cast<size_t>(2 * t + rank), colmax, floors + acc * kGemmNQ, tfull, i);
             } else {
             mbar_wait(tfull + acc, (i >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < kGemmNQ / 32; c += 2) {
+            for (int c = 0; c < NQ / 32; c += 2) {
                 uint32_t r0[32], r1[32];
-                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * kGemmNQ + c * 32;
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * NQ + c * 32;
                 SINE_TMEM_LD32(taddr, r0);
                 SINE_TMEM_LD32(taddr + 32, r1);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -1651,7 +1657,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) __cluster_dims__(2, 1, 1)
     cluster_sync_all();
     if (warp == 5) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * NQ));
     }
 }
 

@@ -405,7 +405,7 @@ def test_tiled_gemm_matches_oracle(pkg, d):
         idx.insert_batch(ids, rows)
         idx.remove_batch(ids[dead[:100]])  # tombstones only (below the compaction trigger)
         idx.remove_batch(ids[dead[100:]])
-        for bq, ms in ((B, 0.9), (300, 0.5)):
+        for bq, ms in ((B, 0.9), (300, 0.5), (100, 0.9), (50, 0.5)):  # N = 256 / 256 / 128 / 64 tiles
             got = idx.query_batch(q[:bq], 10, ms, gemm=True)
             assert idx.gemm_overflows() == 0
             for j in range(bq):
@@ -491,10 +491,10 @@ def test_tiled_gemm_seeded_low_threshold(pkg):
     for scan in ("fp32", "bf16"):
         idx = pkg.GpuCosineIndex(d, scan=scan)
         idx.insert_batch(np.arange(n), rows)
-        for k, ms in ((10, -1.0), (20, 0.1)):
-            got = idx.query_batch(q, k, ms, gemm=True)
+        for k, ms, bq in ((10, -1.0, B), (20, 0.1, B), (10, -1.0, 60)):
+            got = idx.query_batch(q[:bq], k, ms, gemm=True)
             assert idx.gemm_overflows() == 0
-            for j in range(B):
+            for j in range(bq):
                 want = ora.query(q[j], k, ms)
                 assert got[0][j, :got[2][j]].tolist() == [c.id for c in want], (scan, k, ms, j)
                 np.testing.assert_allclose(got[1][j, :got[2][j]], [c.similarity for c in want], atol=1e-12, rtol=0)
