@@ -568,21 +568,23 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
     stream = torch.cuda.current_stream().cuda_stream
     out = {"workload": f"config C at P=1: {n} SEs x d={d}, k={k}, tau={TAU}, rows generated on the device",
            "rows": n, "dim": d, "k": k, "store_f32": store_f32, "load_s": load_s, "regimes": []}
-    cases = [("bf16", 1, 10), ("bf16", 64, 5), ("bf16", 4096, 2)]
+    # HBM-bound batches first, the power-heavy tensor-bound ones last
+    cases = [("bf16", 1, 10), ("bf16", 64, 5)]
     if store_f32:
-        cases += [("fp32", 1, 10), ("fp32", 64, 5), ("fp32", 4096, 1)]
+        cases += [("fp32", 1, 10), ("fp32", 64, 5)]
+    cases += [("bf16", 4096, 2)] + ([("fp32", 4096, 2)] if store_f32 else [])
     for scan, b, reps in cases:
         run = lambda: idx.query_device(b, q.data_ptr(), k, TAU, ids.data_ptr(), sims.data_ptr(),  # noqa: E731
                                        cnt.data_ptr(), stream, scan=scan, certify=False)
         run()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        evs[0].record()
+        for r_ in range(reps):
             run()
-        e1.record()
+            evs[r_ + 1].record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
+        ms = float(np.median([evs[r_].elapsed_time(evs[r_ + 1]) for r_ in range(reps)]))
         got = ids[:b, 0].cpu().numpy()
         planted = np.arange(0, b, 2)
         # a planted query must return its source row iff cos >= tau (random
