@@ -586,7 +586,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 // 2-D K-major map: inner dim = row elements (box = one 128-B swizzle row),
 // outer dim = rows (box = 128), SWIZZLE_128B, out-of-bounds rows read as 0.
-CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int64_t rows, int box_rows = 128) {
+CUtensorMap encode_kmajor_map(const void* base, bool tf32, int64_t row_elems, int64_t rows, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_elems), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * (tf32 ? 4 : 2))};
@@ -598,6 +598,31 @@ CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int6
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(SINE_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
     return m;
+}
+
+// Encoded maps are reused across calls (the small-batch path launches with
+// the same row and query maps every time): a per-thread cache keyed by the
+// full map description.
+CUtensorMap make_kmajor_map(const void* base, bool tf32, int64_t row_elems, int64_t rows, int box_rows = 128) {
+    struct Entry {
+        const void* base;
+        bool tf32;
+        int64_t row_elems, rows;
+        int box_rows;
+        CUtensorMap map;
+    };
+    static thread_local Entry cache[8];
+    static thread_local int next = 0, used = 0;
+    for (int i = 0; i < used; ++i) {
+        const Entry& e = cache[i];
+        if (e.base == base && e.tf32 == tf32 && e.row_elems == row_elems && e.rows == rows && e.box_rows == box_rows)
+            return e.map;
+    }
+    Entry e{base, tf32, row_elems, rows, box_rows, encode_kmajor_map(base, tf32, row_elems, rows, box_rows)};
+    cache[next] = e;
+    next = (next + 1) % 8;
+    used = std::min(used + 1, 8);
+    return e.map;
 }
 
 constexpr int kUmmaMinBatch = 1;
@@ -640,8 +665,21 @@ int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(max_clusters * CS);
-    int active = 0;  // clusters the GPU can hold at once (persistent grid: one wave)
-    CK(cudaOccupancyMaxActiveClusters(&active, kern, &cfg));
+    // clusters the GPU can hold at once (persistent grid: one wave); the
+    // answer depends only on the kernel, cluster shape and shared memory
+    static std::mutex occ_mu;
+    static std::unordered_map<size_t, int> occ;
+    int active = 0;
+    {
+        std::lock_guard<std::mutex> g(occ_mu);
+        auto it = occ.find(smem);
+        if (it != occ.end()) active = it->second;
+    }
+    if (!active) {
+        CK(cudaOccupancyMaxActiveClusters(&active, kern, &cfg));
+        std::lock_guard<std::mutex> g(occ_mu);
+        occ[smem] = active;
+    }
     const int ncl = std::max(1, std::min(max_clusters, active));
     cfg.gridDim = dim3(ncl * CS);
     CK(cudaLaunchKernelEx(&cfg, kern, qmap, rmap, p));
