@@ -363,12 +363,40 @@ def run_ours(args):
             qh.array[:] = qs[s]
             idx.query_into(qh.array, K, TAU, oi.array, os_.array, oc.array)
             lat.append(time.perf_counter() - t1)
-        t_e2e = time.perf_counter() - t0
+        t_seq = time.perf_counter() - t0
         lat_ms = np.array(lat) * 1e3
+        # the serving pattern: 4 batches in flight through the async C ABI
+        # (sine_query_submit / sine_query_wait), every step's H2D from pinned
+        # memory and D2H of its results inside the timed region
+        depth = 4
+        slots = [tuple(Nat.PinnedArray(sh_, dt) for sh_, dt in (((b, DIM), np.float64), ((b, K), np.int64),
+                                                                ((b, K), np.float64), ((b,), np.int32)))
+                 for _ in range(depth)]
+        from collections import deque
+
+        def run_async(s0, s1):
+            inflight = deque()
+            for s in range(s0, s1):
+                if len(inflight) == depth:
+                    idx.wait_ticket(inflight.popleft())
+                qh_, oi_, os2, oc_ = slots[s % depth]
+                qh_.array[:] = qs[s]
+                inflight.append(idx.submit_into(qh_.array, K, TAU, oi_.array, os2.array, oc_.array))
+            while inflight:
+                idx.wait_ticket(inflight.popleft())
+
+        run_async(0, args.warmup)
+        t0 = time.perf_counter()
+        run_async(args.warmup, nsteps)
+        t_e2e = time.perf_counter() - t0
         e2e = {"value": b * args.steps / t_e2e, "unit": "lookups/s", "h2d_bytes_per_step": b * DIM * 8,
                "d2h_bytes_per_step": b * K * 16 + b * 4,
-               "latency_ms": {"p50": float(np.percentile(lat_ms, 50)), "p99": float(np.percentile(lat_ms, 99))},
-               "api": "GpuCosineIndex.query_into (sine_query C ABI), pinned host buffers"}
+               "api": f"GpuCosineIndex.submit_into / wait_ticket (sine_query_submit / sine_query_wait C ABI), "
+                      f"{depth} batches in flight, pinned host buffers",
+               "sequential": {"value": b * args.steps / t_seq,
+                              "api": "GpuCosineIndex.query_into (sine_query C ABI), one batch at a time",
+                              "latency_ms": {"p50": float(np.percentile(lat_ms, 50)),
+                                             "p99": float(np.percentile(lat_ms, 99))}}}
 
     regimes = []
     if world == 1 and not args.no_regimes:

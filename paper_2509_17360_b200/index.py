@@ -225,6 +225,21 @@ class GpuCosineIndex:
                                      N.ptr(ids, ctypes.c_int64), N.ptr(sims, ctypes.c_double),
                                      N.ptr(counts, ctypes.c_int32)))
 
+    def submit_into(self, q: np.ndarray, k: int, min_similarity: float, ids: np.ndarray, sims: np.ndarray,
+                    counts: np.ndarray, *, scan: str | None = None, rerank: bool | None = None) -> int:
+        """Asynchronous query_into (sine_query_submit): the caller's buffers
+        (pinned host memory) must stay untouched until wait_ticket(ticket)
+        returns; up to 16 batches in flight, executed in submission order."""
+        t = ctypes.c_int64()
+        N.check(self._lib.sine_query_submit(self._h, q.shape[0], q.ctypes.data, int(k), float(min_similarity),
+                                            self._mode(scan, rerank), ids.ctypes.data, sims.ctypes.data,
+                                            counts.ctypes.data, ctypes.byref(t)))
+        return t.value
+
+    def wait_ticket(self, ticket: int) -> None:
+        """Block until a submit_into batch's results (certified) are in its buffers."""
+        N.check(self._lib.sine_query_wait(self._h, int(ticket)))
+
     def query_device(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                      counts_ptr: int, stream: int | None = None, *, scan: str | None = None,
                      rerank: bool | None = None, cuda_core: bool = False, umma_v1: bool = False,

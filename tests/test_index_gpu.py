@@ -528,3 +528,30 @@ def test_unordered_id_batches_remove_and_requery(pkg):
     got = idx.query_batch(q, 7, -1.0)
     for j in range(20):
         assert got[0][j, :got[2][j]].tolist() == [c.id for c in ora.query(q[j], 7, -1.0)]
+
+
+def test_submit_into_pipelined_matches_query_batch(pkg):
+    """Several batches in flight through sine_query_submit/wait with
+    caller-owned pinned buffers return exactly query_batch's answers."""
+    from paper_2509_17360_b200 import _native as N
+    rng = np.random.default_rng(41)
+    n, d, B = 30000, 256, 3
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    idx = pkg.GpuCosineIndex(d)
+    idx.insert_batch(np.arange(n), rows)
+    qs = rows[rng.integers(0, n, (6, B))] + 0.02 * rng.standard_normal((6, B, d))
+    qs /= np.linalg.norm(qs, axis=2, keepdims=True)
+    bufs = [(N.PinnedArray((B, d), np.float64), N.PinnedArray((B, 5), np.int64), N.PinnedArray((B, 5), np.float64),
+             N.PinnedArray((B,), np.int32)) for _ in range(6)]
+    tickets = []
+    for s in range(6):
+        q, i, sm, c = bufs[s]
+        q.array[:] = qs[s]
+        tickets.append(idx.submit_into(q.array, 5, 0.5, i.array, sm.array, c.array))
+    for s in range(6):
+        idx.wait_ticket(tickets[s])
+        want = idx.query_batch(qs[s], 5, 0.5)
+        np.testing.assert_array_equal(bufs[s][1].array, want[0])
+        np.testing.assert_array_equal(bufs[s][2].array, want[1])
+        np.testing.assert_array_equal(bufs[s][3].array, want[2])
