@@ -555,3 +555,29 @@ def test_submit_into_pipelined_matches_query_batch(pkg):
         np.testing.assert_array_equal(bufs[s][1].array, want[0])
         np.testing.assert_array_equal(bufs[s][2].array, want[1])
         np.testing.assert_array_equal(bufs[s][3].array, want[2])
+
+
+@pytest.mark.parametrize("k", [60, 112])
+def test_large_k_all_tensor_core_paths(pkg, k):
+    """k' = k + 16 up to the 128-entry device lists: resident (B=8), CTA
+    pair (B=100, bf16), tiled GEMM (B=300) and the CUDA-core scan agree
+    with the oracle at low and mid thresholds (dense warm-up rounds, sparse
+    inserts, seeded GEMM floors)."""
+    rng = np.random.default_rng(k)
+    n, d = 20000, 128
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((300, d))
+    q[:100] = rows[rng.integers(0, n, 100)] + 0.2 * rng.standard_normal((100, d))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(np.arange(n), rows)
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(np.arange(n), rows)
+        for B, ms, kw in ((8, -1.0, {}), (100, 0.1, {}), (300, -1.0, {"gemm": True}), (8, 0.1, {"cuda_core": True})):
+            got = idx.query_batch(q[:B], k, ms, **kw)
+            for j in range(0, B, 7):
+                want = ora.query(q[j], k, ms)
+                assert got[0][j, :got[2][j]].tolist() == [c.id for c in want], (scan, B, ms, kw, j)
+                np.testing.assert_allclose(got[1][j, :got[2][j]], [c.similarity for c in want], atol=1e-12, rtol=0)
