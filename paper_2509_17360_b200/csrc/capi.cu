@@ -1367,7 +1367,10 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     a.first = 1;
     a.st = h->st.p;
     a.hw = hw, a.hc = hc, a.hand = hand, a.hor = hor;
-    evict_hist_kernel<<<grid_all, 256, 0, st>>>(a);
+    if (policy == 0)
+        evict_pass1_lcfu_kernel<<<grid_all, 256, 0, st>>>(a);
+    else
+        evict_hist_kernel<<<grid_all, 256, 0, st>>>(a);
     evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 1);
     // the slots of the chosen prefix bucket -> dense records (slot order):
     // later passes stream 32 B per candidate instead of gathering columns

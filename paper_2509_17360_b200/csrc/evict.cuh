@@ -222,6 +222,115 @@ __global__ void __launch_bounds__(256) evict_hist_kernel(const HistArgs a) {
     }
 }
 
+// Pass 1 for LCFU over every slot, 4 slots per thread in flight: all
+// column loads of a group are issued before any score is computed (the
+// pass is load-latency bound), then each score is keyed, cached in k1 and
+// histogrammed on its first digit exactly as evict_hist_kernel does.
+__global__ void __launch_bounds__(256) evict_pass1_lcfu_kernel(const HistArgs a) {
+    __shared__ uint32_t swl[256], swh[256], sc[256];
+    __shared__ unsigned long long band, bor;
+    swl[threadIdx.x] = 0;
+    swh[threadIdx.x] = 0;
+    sc[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        band = ~0ull;
+        bor = 0ull;
+    }
+    __syncthreads();
+    constexpr int U = 4;
+    const int64_t n = a.c.nslots;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = 256ll * gridDim.x;
+    uint64_t vand = ~0ull, vor = 0ull;
+    for (int64_t i0 = blockIdx.x * 256ll + (threadIdx.x & ~31); i0 < n; i0 += U * stride) {
+        double lf[U], lc[U], ll[U], ls[U], ex[U];
+        int64_t size[U];
+        uint32_t vw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t s = i0 + u * stride + lane;
+            const bool in = s < n;
+            vw[u] = in ? __ldg(a.c.valid + (s >> 5)) : 0u;
+            lf[u] = in ? __ldg(a.c.lf + s) : 0.0;
+            lc[u] = in ? __ldg(a.c.lc + s) : 0.0;
+            ll[u] = in ? __ldg(a.c.ll + s) : 0.0;
+            ls[u] = in ? __ldg(a.c.ls + s) : 0.0;
+            ex[u] = in ? __ldg(a.c.expiration + s) : 0.0;
+            size[u] = in ? __ldg(a.c.size + s) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t s = i0 + u * stride + lane;
+            const bool act = s < n && ((vw[u] >> (s & 31)) & 1u);
+            uint32_t dg = 0;
+            if (act) {
+                double v = 0.0;  // cal_score (engine.py:33-48): exact order, no FMA
+                if (size[u] != 0 && !(__dsub_rn(ex[u], a.now) <= 0.0)) {
+                    v = __dmul_rn(lf[u], lc[u]);
+                    v = __dmul_rn(v, ll[u]);
+                    v = __dmul_rn(v, ls[u]);
+                    v = __ddiv_rn(v, static_cast<double>(size[u]));
+                }
+                const uint64_t k0 = f64_key(v);
+                a.k1[s] = k0;
+                dg = static_cast<uint32_t>(k0 >> 56);
+                vand &= k0;
+                vor |= k0;
+            }
+            const uint64_t sz = act ? static_cast<uint64_t>(size[u]) : 0ull;
+            uint32_t rem = __ballot_sync(0xffffffffu, act);
+            const uint32_t peers = __match_any_sync(0xffffffffu, act ? dg : 0xffffffffu);
+            const bool group_leader = act && (__ffs(peers) - 1) == lane;
+            if (__popc(__ballot_sync(0xffffffffu, group_leader)) > 4) {
+                if (act) {
+                    smem_add64(&swl[dg], &swh[dg], sz);
+                    atomicAdd(&sc[dg], 1u);
+                }
+                rem = 0;
+            }
+            while (rem) {
+                const int leader = __ffs(rem) - 1;
+                const uint32_t ldg = __shfl_sync(0xffffffffu, dg, leader);
+                const bool mine = act && dg == ldg;
+                const uint32_t grp = __ballot_sync(0xffffffffu, mine);
+                unsigned long long v = mine ? sz : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == leader) {
+                    smem_add64(&swl[ldg], &swh[ldg], v);
+                    atomicAdd(&sc[ldg], static_cast<uint32_t>(__popc(grp)));
+                }
+                rem &= ~grp;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        vand &= __shfl_xor_sync(0xffffffffu, vand, o);
+        vor |= __shfl_xor_sync(0xffffffffu, vor, o);
+    }
+    if (lane == 0 && (vor | ~vand)) {
+        atomicAnd(&band, static_cast<unsigned long long>(vand));
+        atomicOr(&bor, static_cast<unsigned long long>(vor));
+    }
+    __syncthreads();
+    if (sc[threadIdx.x]) {
+        atomicAdd(a.hw + threadIdx.x, (static_cast<unsigned long long>(swh[threadIdx.x]) << 32) | swl[threadIdx.x]);
+        atomicAdd(a.hc + threadIdx.x, static_cast<unsigned long long>(sc[threadIdx.x]));
+    }
+    if (threadIdx.x == 0) {
+        if (bor | ~band) {
+            atomicAnd(a.hand, band);
+            atomicOr(a.hor, bor);
+        }
+        // words 1 and 2 were not read: reported as varying
+        atomicAnd(a.hand + 1, 0ull);
+        atomicOr(a.hor + 1, ~0ull);
+        atomicAnd(a.hand + 2, 0ull);
+        atomicOr(a.hor + 2, ~0ull);
+    }
+}
+
 // One CTA: choose the digit bucket where the cumulative weight reaches rem,
 // then skip the following digits that are constant over that bucket.
 __global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsigned long long* hw,
@@ -305,16 +414,20 @@ struct CollectPred {
     int mode;  // 0: prefix <= T (victims), 1: prefix == T (candidates), 2: prefix < T
     uint64_t pre[3];
 
-    __device__ __forceinline__ bool operator()(int64_t s, uint64_t* k) const {
+    // need_keys = false: only the predicate (counting passes skip the
+    // created_at / id gathers when the primary word decides)
+    __device__ __forceinline__ bool operator()(int64_t s, uint64_t* k, bool need_keys = true) const {
         if (rk) {
             k[0] = rk[3 * s], k[1] = rk[3 * s + 1], k[2] = rk[3 * s + 2];
         } else {
-            if (!valid_bit(c.valid, s)) return false;
+            // both loads issued before the validity test (no dependency chain)
+            const uint32_t vw = __ldg(c.valid + (s >> 5));
             k[0] = k1[s];
+            if (!((vw >> (s & 31)) & 1u)) return false;
             if (nd <= 8 && !all) {  // the first word decides; the rest only when taken
                 const int cmp = prefix_cmp(k, pre, nd);
                 const bool take = mode == 0 ? cmp <= 0 : (mode == 1 ? cmp == 0 : cmp < 0);
-                if (take) {
+                if (take && need_keys) {
                     k[1] = f64_key(c.created[s]);
                     k[2] = i64_key(c.ids[s]);
                 }
@@ -360,7 +473,8 @@ __global__ void __launch_bounds__(256) collect_count_kernel(EvictCols c, const u
     const int64_t e = min(b + kColChunk, n);
     int32_t cnt = 0;
     uint64_t k[3];
-    for (int64_t i = b + threadIdx.x; i < e; i += 256) cnt += pred(i, k) ? 1 : 0;
+#pragma unroll 4
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) cnt += pred(i, k, false) ? 1 : 0;
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
     __syncthreads();
