@@ -165,6 +165,19 @@ int sine_gemm_overflows(sine_index_t *h, int64_t *n);
 int sine_merge_shards(int device, int P, int64_t B, int k, const int64_t *ids_dev,
                       const double *sims_dev, int64_t rank_stride, int64_t *out_ids,
                       double *out_sims, int32_t *out_counts, void *stream);
+/* Batched HashedBagEmbedder (embedder.py:34-60): B queries already
+ * tokenized on the host (embedder.tokenize, embedder.py:23-25) as UTF-8
+ * bytes; token t is tok_bytes[tok_off[t] .. tok_off[t+1]), query b owns
+ * tokens q_off[b] .. q_off[b+1]) (at least one -> else SINE_EINVAL, "cannot
+ * embed text with no tokens").  Keyed BLAKE2b-64 of every token and the
+ * bucket counts run on `device`; out_rows (host, [B][dim]) receives
+ * counts / (sum(c*c) ** 0.5), bit-identical to the reference.
+ * sine_blake2b64: blake2b(msg, key=key.to_bytes(8,'little'), digest_size=8)
+ * as a little-endian integer (host; the same code the kernel runs). */
+int sine_embed_hashed_bag(int device, uint64_t seed, int64_t dim, const uint8_t *tok_bytes,
+                          int64_t nbytes, const int64_t *tok_off, int64_t ntok,
+                          const int64_t *q_off, int64_t B, double *out_rows);
+uint64_t sine_blake2b64(const uint8_t *msg, int64_t len, uint64_t key);
 /* Float-hex text of row blocks, byte-identical to the reference's
  * snapshot / record writers (" ".join(float(c).hex() ...), index.py:343-346,
  * model.py:237) and read back bit-exactly like float.fromhex (index.py:370,

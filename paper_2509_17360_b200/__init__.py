@@ -5,10 +5,13 @@ Public surface (drop-in for the reference `semcache` hot path):
 * `GpuCosineIndex`  -- ExactCosineIndex contract (index.py:49-120) on HBM.
 * `CacheEngine`     -- semcache.engine.CacheEngine with device eviction.
 * `ShardedCosineIndex` -- row-sharded index over torch.distributed (NCCL).
+* `GpuHashedBagEmbedder` -- HashedBagEmbedder (embedder.py:34-60) with a
+  batched device hashing path.
 """
 
 from .errors import RetriableError, SemcacheError, ValidationError
 from .index import Candidate, GpuCosineIndex, check_vector
+from .embedder import GpuHashedBagEmbedder
 from .engine import AdmitOutcome, CacheEngine, LookupOutcome, StageTimings, cal_score
 from .model import (CacheConfig, EmbeddingVector, SemanticElement, SemanticKey, make_element,
                     token_count)
@@ -17,6 +20,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AdmitOutcome", "CacheConfig", "CacheEngine", "Candidate", "EmbeddingVector", "GpuCosineIndex",
+    "GpuHashedBagEmbedder",
     "LookupOutcome", "RetriableError", "SemanticElement", "SemanticKey", "SemcacheError",
     "StageTimings", "ValidationError", "cal_score", "check_vector", "make_element", "token_count",
 ]

@@ -32,6 +32,7 @@
 
 #include "../../include/sine_b200.h"
 #include "common.cuh"
+#include "embed.cuh"
 #include "evict.cuh"
 #include "hexio.cuh"
 #include "merge.cuh"
@@ -1991,6 +1992,52 @@ int sine_merge_shards(int device, int P, int64_t B, int k, const int64_t* ids_de
         shard_merge_kernel<<<static_cast<unsigned>(B), kShardMergeThreads, smem, static_cast<cudaStream_t>(stream)>>>(
             ids_dev, sims_dev, P, B, k, rank_stride ? rank_stride : B * k, out_ids, out_sims, out_counts);
         CK(cudaGetLastError());
+    });
+}
+
+uint64_t sine_blake2b64(const uint8_t* msg, int64_t len, uint64_t key) { return blake2b64_keyed(msg, len, key); }
+
+int sine_embed_hashed_bag(int device, uint64_t seed, int64_t dim, const uint8_t* tok_bytes, int64_t nbytes,
+                          const int64_t* tok_off, int64_t ntok, const int64_t* q_off, int64_t B, double* out_rows) {
+    return guarded([&] {
+        if (dim < 1 || B < 0 || ntok < 0) fail(SINE_EINVAL, "bad embedding batch shape");
+        if (B == 0) return;
+        for (int64_t b = 0; b < B; ++b)
+            if (q_off[b + 1] <= q_off[b]) fail(SINE_EINVAL, "cannot embed text with no tokens");
+        if (q_off[0] != 0 || q_off[B] != ntok) fail(SINE_EINVAL, "query token ranges do not cover the tokens");
+        CK(cudaSetDevice(device));
+        std::vector<int32_t> tok_q(ntok);
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t t = q_off[b]; t < q_off[b + 1]; ++t) tok_q[t] = static_cast<int32_t>(b);
+        DevBuf<uint8_t> dbytes;
+        DevBuf<int64_t> doff;
+        DevBuf<int32_t> dq;
+        DevBuf<double> dcounts;
+        dbytes.ensure(std::max<int64_t>(nbytes, 1));
+        doff.ensure(ntok + 1);
+        dq.ensure(std::max<int64_t>(ntok, 1));
+        dcounts.ensure(B * dim);
+        cudaStream_t st = nullptr;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (nbytes) CK(cudaMemcpyAsync(dbytes.p, tok_bytes, nbytes, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(doff.p, tok_off, (ntok + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dq.p, tok_q.data(), ntok * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(dcounts.p, 0, B * dim * sizeof(double), st));
+        embed_count_kernel<<<grid_for(ntok, 128, 148), 128, 0, st>>>(dbytes.p, doff.p, ntok, dq.p, seed, dim,
+                                                                      dcounts.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out_rows, dcounts.p, B * dim * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamDestroy(st));
+        // counts / (sum(c * c) ** 0.5): integer-valued sums are exact in any
+        // order; the power is taken with the host libm like CPython's x ** 0.5
+        for (int64_t b = 0; b < B; ++b) {
+            double* r = out_rows + b * dim;
+            double ss = 0.0;
+            for (int64_t j = 0; j < dim; ++j) ss += r[j] * r[j];
+            const double norm = std::pow(ss, 0.5);
+            for (int64_t j = 0; j < dim; ++j) r[j] = r[j] / norm;
+        }
     });
 }
 

@@ -180,3 +180,29 @@ def test_snapshot_bytes_parse_matches_reference_reader():
     assert (d, s) == (d2, s2) == (6, 3)
     assert ids.tolist() == [e[0] for e in entries]
     assert got.tobytes() == np.stack([e[1] for e in entries]).tobytes()
+
+
+def test_blake2b64_matches_hashlib_goldens():
+    """The device BLAKE2b (RFC 7693, keyed, 8-byte digest) that buckets the
+    embedder's tokens equals hashlib on the reference's golden digests and
+    on fresh random messages."""
+    import hashlib
+    import json
+    from paper_2509_17360_b200 import _native as N
+    lib = N.load_library()
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "embed_golden.json"), encoding="utf-8"))
+    for g in gold["blake2b"]:
+        m = bytes.fromhex(g["msg"])
+        assert lib.sine_blake2b64(m, len(m), g["key"]) == g["digest"]
+    rng = np.random.default_rng(9)
+    for n in list(range(0, 260, 7)) + [1000]:
+        m = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        key = int(rng.integers(0, 2 ** 63))
+        want = int.from_bytes(hashlib.blake2b(m, key=key.to_bytes(8, "little"), digest_size=8).digest(), "little")
+        assert lib.sine_blake2b64(m, len(m), key) == want
+
+
+def test_embedder_tokenize_matches_reference_rules():
+    from paper_2509_17360_b200.embedder import tokenize
+    assert tokenize("Hello, World! héllo  WORLD...x") == ["hello", "world", "héllo", "world", "x"]
+    assert tokenize("...!!!") == []

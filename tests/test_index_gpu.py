@@ -581,3 +581,26 @@ def test_large_k_all_tensor_core_paths(pkg, k):
                 want = ora.query(q[j], k, ms)
                 assert got[0][j, :got[2][j]].tolist() == [c.id for c in want], (scan, B, ms, kw, j)
                 np.testing.assert_allclose(got[1][j, :got[2][j]], [c.similarity for c in want], atol=1e-12, rtol=0)
+
+
+def test_gpu_embedder_matches_reference_goldens(pkg):
+    """GpuHashedBagEmbedder reproduces the reference HashedBagEmbedder's
+    vectors bit for bit (goldens from the reference), batched and single."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "embed_golden.json"), encoding="utf-8"))
+    texts = gold["texts"]
+    for case in gold["cases"]:
+        emb = pkg.GpuHashedBagEmbedder(case["dimension"], seed=case["seed"])
+        got = emb.embed_batch(texts)
+        for row, want in zip(got, case["vectors"]):
+            dense = np.zeros(case["dimension"])
+            for i, h in want:
+                dense[i] = float.fromhex(h)
+            assert row.tobytes() == dense.tobytes()
+        one = emb.embed(texts[0])
+        assert one.components == tuple(got[0].tolist())
+    with pytest.raises(pkg.ValidationError):
+        pkg.GpuHashedBagEmbedder(256).embed_batch(["ok text", "?!"])
+    with pytest.raises(pkg.ValidationError):
+        pkg.GpuHashedBagEmbedder(4)
