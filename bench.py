@@ -407,6 +407,9 @@ def run_ours(args):
     persistence = None
     if world == 1 and not args.no_trace:
         persistence = measure_persistence(rows)
+    embedder = None
+    if world == 1 and not args.no_trace:
+        embedder = measure_embedder()
     eviction = None
     if world == 1 and not args.no_evict:
         del idx
@@ -442,7 +445,7 @@ def run_ours(args):
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
                 "gpu_launches": int(launches), "uncertified_steps": uncertified,
                 "regimes": regimes, "eviction": eviction, "trace": trace, "config_c": config_c,
-                "persistence": persistence}
+                "persistence": persistence, "embedder": embedder}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -545,6 +548,34 @@ def measure_persistence(rows, n=200_000):
             "round_trip_bit_exact": exact, "text_identical_to_reference_writer": bool(same),
             "cpu_baseline": {"save_rows_per_s": m / ref_save, "load_rows_per_s": m / ref_load, "cores": 1,
                              "kind": "port", "sample": f"{m} rows: float.hex / float.fromhex (reference writer)"}}
+
+
+# ------------------------------------------------ embedder
+
+def measure_embedder(n=4096, dim=768):
+    """Batched query embeddings (HashedBagEmbedder, d=768): texts/s through
+    GpuHashedBagEmbedder.embed_batch vs the reference algorithm (oracle
+    restatement: hashlib BLAKE2b per token, Python counts) on one core."""
+    from paper_2509_17360_b200 import GpuHashedBagEmbedder
+    from oracle import sine_oracle as O
+
+    rng = np.random.default_rng(13)
+    vocab = [f"w{i}" for i in range(5000)] + ["weather", "paris", "capital", "search", "agent", "tool"]
+    texts = [" ".join(vocab[j] for j in rng.integers(0, len(vocab), rng.integers(4, 24))) for _ in range(n)]
+    emb = GpuHashedBagEmbedder(dim, seed=1)
+    emb.embed_batch(texts[:64])
+    t0 = time.perf_counter()
+    got = emb.embed_batch(texts)
+    gpu_s = time.perf_counter() - t0
+    m = 512
+    t0 = time.perf_counter()
+    ref = [O.hashed_bag_embed(t, dim, 1) for t in texts[:m]]
+    cpu_s = time.perf_counter() - t0
+    same = all(got[j].tolist() == list(ref[j]) for j in range(m))
+    return {"workload": f"{n} texts (4-23 tokens), dimension {dim}, seed 1", "texts_per_s": n / gpu_s,
+            "identical_to_reference_algorithm": same,
+            "cpu_baseline": {"texts_per_s": m / cpu_s, "cores": 1, "kind": "port",
+                             "sample": f"{m} texts: hashlib BLAKE2b per token + Python counts (embedder.py:49-60)"}}
 
 
 # ------------------------------------------------ config C: 10M x 1024, k=20

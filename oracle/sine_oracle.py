@@ -369,3 +369,30 @@ class OracleEngine:
                 if self.usage <= self.capacity:
                     break
         return removed
+
+
+# ------------------------------------------------------------ embedder
+
+import hashlib as _hashlib  # noqa: E402
+import string as _string  # noqa: E402
+
+_PUNCT = str.maketrans({c: " " for c in _string.punctuation})  # src/embedder.py:20
+
+
+def tokenize(text: str) -> list[str]:
+    """src/embedder.py:23-25."""
+    return text.lower().translate(_PUNCT).split()
+
+
+def hashed_bag_embed(text: str, dimension: int, seed: int) -> tuple:
+    """HashedBagEmbedder._bucket + embed (src/embedder.py:49-60)."""
+    key = seed.to_bytes(8, "little", signed=False)
+    tokens = tokenize(text)
+    if not tokens:
+        raise OracleValidationError("cannot embed text with no tokens")
+    counts = [0.0] * dimension
+    for tok in tokens:
+        d = _hashlib.blake2b(tok.encode("utf-8"), key=key, digest_size=8).digest()
+        counts[int.from_bytes(d, "little") % dimension] += 1.0
+    norm = sum(c * c for c in counts) ** 0.5
+    return tuple(c / norm for c in counts)

@@ -190,3 +190,18 @@ def test_log_base_invariance_restated():
         a = O.cal_score(f, 0.005, 400.0, 7, 13, 10.0, 0.0)
         b = O.cal_score(f, 0.005, 400.0, 7, 13, 10.0, 0.0, log=math.log10)
         assert a == pytest.approx(b * math.log(10) ** 4, rel=1e-9)
+
+
+def test_oracle_embedder_matches_reference_goldens():
+    """The oracle's HashedBagEmbedder restatement equals the reference's
+    vectors (embed_golden.json, produced by the reference)."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "embed_golden.json"), encoding="utf-8"))
+    for case in gold["cases"]:
+        for text, want in zip(gold["texts"], case["vectors"]):
+            got = O.hashed_bag_embed(text, case["dimension"], case["seed"])
+            dense = [0.0] * case["dimension"]
+            for i, h in want:
+                dense[i] = float.fromhex(h)
+            assert list(got) == dense
