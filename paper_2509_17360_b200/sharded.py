@@ -96,7 +96,15 @@ class ShardedCosineIndex:
             self.local.remove_batch(mine)
 
     def query_batch(self, queries, k: int, min_similarity: float = -1.0):
-        """Exact top-k over all shards; returns numpy (ids, sims, counts)."""
+        """Exact top-k over all shards; returns numpy (ids, sims, counts).
+        With NCCL the host queries go to the device once and take the
+        device path (one all-gather + the shard-merge kernel)."""
+        if dist.get_backend(self.group) == "nccl":
+            from .index import check_matrix
+            q = torch.from_numpy(check_matrix(queries, self.dimension)).to(
+                torch.device("cuda", torch.cuda.current_device()))
+            mi, ms, mc = self.query_device(q, k, min_similarity)
+            return mi.cpu().numpy(), ms.cpu().numpy(), mc.cpu().numpy()
         ids, sims, _ = self.local.query_batch(queries, k, min_similarity)
         dev = torch.device("cuda", torch.cuda.current_device()) \
             if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
