@@ -507,17 +507,11 @@ __global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const u
     int32_t cnt = 0;
     uint64_t vand[3] = {~0ull, ~0ull, ~0ull}, vor[3] = {0, 0, 0};
     uint64_t k[3];
+    // predicates only (no key gathers): 16 rounds of independent loads
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         const int64_t i = w0 + j * 32 + lane;
-        const bool take = i < n && pred(i, k);
-        if (take) {
-#pragma unroll
-            for (int w = 0; w < 3; ++w) {
-                vand[w] &= k[w];
-                vor[w] |= k[w];
-            }
-        }
+        const bool take = i < n && pred(i, k, false);
         m[j] = __ballot_sync(0xffffffffu, take);
         cnt += __popc(m[j]);
     }
@@ -533,15 +527,22 @@ __global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const u
             const int64_t at = off + __popc(m[j] & lt);
             const int64_t slot = rk ? rslot[i] : i;
             out_slot[at] = static_cast<int32_t>(slot);
-            if (out_k) {
+            if (out_k || kand) {  // the taken entries' keys, gathered once
+                uint64_t kk[3];
                 if (rk) {
-                    out_k[3 * at] = rk[3 * i];
-                    out_k[3 * at + 1] = rk[3 * i + 1];
-                    out_k[3 * at + 2] = rk[3 * i + 2];
+                    kk[0] = rk[3 * i], kk[1] = rk[3 * i + 1], kk[2] = rk[3 * i + 2];
                 } else {
-                    out_k[3 * at] = k1[i];
-                    out_k[3 * at + 1] = f64_key(c.created[i]);
-                    out_k[3 * at + 2] = i64_key(c.ids[i]);
+                    kk[0] = k1[i], kk[1] = f64_key(c.created[i]), kk[2] = i64_key(c.ids[i]);
+                }
+                if (out_k) {
+                    out_k[3 * at] = kk[0];
+                    out_k[3 * at + 1] = kk[1];
+                    out_k[3 * at + 2] = kk[2];
+                }
+#pragma unroll
+                for (int w = 0; w < 3; ++w) {
+                    vand[w] &= kk[w];
+                    vor[w] |= kk[w];
                 }
             }
             if (out_size) out_size[at] = c.size[slot];
