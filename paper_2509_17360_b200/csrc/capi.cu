@@ -879,11 +879,12 @@ void umma_pair_query(sine_index* h, int64_t B, const double* q_dev, int k, int k
 // query's candidates overflowed the chunk capacity; the caller then runs the
 // list-keeping kernels.
 constexpr int kGemmChunks = 32;
+constexpr int kGemmDone = 0, kGemmOverflow = 1, kGemmNotApplicable = 2;
 constexpr float kGemmMinFloor = 0.25f;  // below it the GEMM seeds per-query floors from a sample pass
 constexpr int kGemmSeedMinTiles = 8 * 64;  // row tiles a seeded GEMM needs (the sample is 1/8 of them)
 
 template <int NQ>
-bool umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+int umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
                        bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
                        cudaStream_t st) {
     const bool tf32 = !bf16;
@@ -892,7 +893,7 @@ bool umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int
     const int kblocks = static_cast<int>(row_bytes / kUmmaKB);
     const int nrt = static_cast<int>((h->nslots + kGemmRows - 1) / kGemmRows);
     const int nqt = static_cast<int>((B + NQ - 1) / NQ);
-    if (static_cast<int64_t>(nrt) * nqt >= (1ll << 31)) return false;
+    if (static_cast<int64_t>(nrt) * nqt >= (1ll << 31)) return kGemmNotApplicable;
     const int64_t Bpad = static_cast<int64_t>(nqt) * NQ;
     const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - gemm_smem_bytes(0, NQ)) / gemm_stage_bytes(NQ)));
     const size_t smem = gemm_smem_bytes(S, NQ);
@@ -938,7 +939,7 @@ bool umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int
         // tile maxima; the kp-th largest is a lower bound on the kp-th best
         // score and becomes the query's admission floor in the main pass
         const int nrt_s = std::max(kp, nrt / 8);
-        if (nrt_s > nrt) return false;
+        if (nrt_s > nrt) return kGemmNotApplicable;  // too few row tiles to seed floors
         h->tmax.ensure(static_cast<size_t>(2 * nrt_s) * B);
         GemmParams sp = p;
         sp.nrt = nrt_s;
@@ -963,15 +964,15 @@ bool umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int
     uint32_t* ovf = reinterpret_cast<uint32_t*>(h->n_h.p);
     CK(cudaMemcpyAsync(ovf, h->gcnt.p + B, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (*ovf) return false;
+    if (*ovf) return kGemmOverflow;
     merge_launch(h, kGemmChunks, static_cast<int>(B), kp, q_dev, k, min_sim, rerank, ids_dev, sims_dev, counts_dev,
                  st, 0);
-    return true;
+    return kGemmDone;
 }
 
 // Query tile width by batch: N = 64 / 128 / 256 per pair MMA, so small
 // batches do not pay for padded query columns (kind::tf32 runs at half rate).
-bool umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
+int umma_gemm_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, float thr0, double min_sim,
                      bool bf16, bool rerank, int64_t* ids_dev, double* sims_dev, int32_t* counts_dev,
                      cudaStream_t st) {
     if (B <= 64)
@@ -1023,9 +1024,10 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
         const bool gemm_auto = !(mode & SINE_SCAN_NO_GEMM) && !force_v1 && B > per_pass && gemm_floor_ok &&
                                !(mode & (SINE_SCAN_PAIR | SINE_SCAN_CLUSTER));
         if ((mode & SINE_SCAN_GEMM) || gemm_auto) {
-            if (umma_gemm_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st))
-                return;
-            ++h->gemm_overflows;  // candidates overflowed: fall through to the list-keeping kernels
+            const int r = umma_gemm_query(h, B, q_dev, k, kp, thr0, min_sim, bf16, rerank, ids_dev, sims_dev,
+                                          counts_dev, st);
+            if (r == kGemmDone) return;
+            if (r == kGemmOverflow) ++h->gemm_overflows;  // fall through to the list-keeping kernels
         }
         // measured per-query cost on B200 (1M x 768): resident bf16 ~4.8 us,
         // resident tf32 ~17 us (32-query groups), streaming v1 ~6 us; the
