@@ -201,6 +201,30 @@ def test_lookup_batch_matches_sequential_when_no_purge(pkg):
     assert a.stats() == b.stats()
 
 
+def test_lookup_batch_with_gpu_embedder(pkg):
+    """lookup_batch embeds all keys in one GpuHashedBagEmbedder.embed_batch
+    call; outcomes equal sequential lookups through the same embedder."""
+    emb = pkg.GpuHashedBagEmbedder(64, seed=3)
+    judge = G.StubJudge()
+    a = pkg.CacheEngine(pkg.CacheConfig(capacity_tokens=10_000), emb, judge)
+    b = pkg.CacheEngine(pkg.CacheConfig(capacity_tokens=10_000), emb, judge)
+    texts = [f"topic{t:02d} w{t % 3} {x}" for t in range(12) for x in ("alpha", "beta")]
+    for i, text in enumerate(texts):
+        e = emb.embed(text)
+        for eng in (a, b):
+            eng.admit(pkg.make_element(pkg.SemanticKey(text, "search"), f"v{i}", e, 5, 400.0, 0.005, 0.0, 3600.0),
+                      now=0.0)
+    keys = [pkg.SemanticKey(f"topic{t:02d} w{(t + 1) % 3} {x}", "search") for t in range(12) for x in
+            ("alpha", "gamma")]
+    seq = [a.lookup(k, 1.0) for k in keys]
+    bat = b.lookup_batch(keys, 1.0)
+    for s_, t in zip(seq, bat):
+        assert (s_.kind, s_.element_id, s_.similarity, s_.candidates_considered, s_.judged) == \
+               (t.kind, t.element_id, t.similarity, t.candidates_considered, t.judged)
+        assert s_.query_embedding == t.query_embedding
+    assert a.stats() == b.stats()
+
+
 @pytest.mark.parametrize("shuffled", [False, True])
 def test_large_purge_and_select_match_oracle(pkg, shuffled):
     """1M SEs, config-D metadata: the device purge (ascending ids) followed
