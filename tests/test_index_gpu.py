@@ -381,7 +381,7 @@ def test_cta_pair_kernel_fp32_d768(pkg):
             assert a[0][j, :a[2][j]].tolist() == [c.id for c in want]
 
 
-@pytest.mark.parametrize("d", [64, 384, 768])
+@pytest.mark.parametrize("d", [1, 64, 200, 384, 768])
 def test_tiled_gemm_matches_oracle(pkg, d):
     """The large-batch tiled GEMM (256 x 256 CTA-pair tiles, all query tiles
     in one launch) on ragged row and query tiles, with tombstones: ids
@@ -407,7 +407,8 @@ def test_tiled_gemm_matches_oracle(pkg, d):
         idx.remove_batch(ids[dead[100:]])
         for bq, ms in ((B, 0.9), (300, 0.5), (100, 0.9), (50, 0.5)):  # N = 256 / 256 / 128 / 64 tiles
             got = idx.query_batch(q[:bq], 10, ms, gemm=True)
-            assert idx.gemm_overflows() == 0
+            if d > 1:  # at d = 1 every same-sign row scores 1: dense, overflows, falls back (still exact)
+                assert idx.gemm_overflows() == 0
             for j in range(bq):
                 want = ora.query(q[j], 10, ms)
                 assert got[0][j, :got[2][j]].tolist() == [c.id for c in want], (scan, bq, ms, j)
