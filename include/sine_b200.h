@@ -123,6 +123,15 @@ int sine_query_device(sine_index_t *h, int64_t B, const double *q_dev, int k,
                       double min_sim, uint32_t mode, int64_t *ids_dev,
                       double *sims_dev, int32_t *counts_dev, void *stream);
 
+/* sine_query_device that also writes the per-query exactness certificates
+ * (B bytes, 1 = provably the exact answer) to cert_dev on the stream, so a
+ * pipelined caller checks them later without a sync or an extra copy;
+ * SINE_CERTIFY is ignored here (a 0 means: re-run that query, e.g. with
+ * SINE_SCAN_CUDA_CORE). */
+int sine_query_device_cert(sine_index_t *h, int64_t B, const double *q_dev, int k,
+                           double min_sim, uint32_t mode, int64_t *ids_dev, double *sims_dev,
+                           int32_t *counts_dev, uint8_t *cert_dev, void *stream);
+
 /* Asynchronous sine_query: enqueue the batch (host buffers, ideally pinned,
  * which must stay valid until the wait) and return a ticket; up to 16
  * batches in flight.  sine_query_wait blocks until the batch's results are

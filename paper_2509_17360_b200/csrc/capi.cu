@@ -163,6 +163,7 @@ struct sine_index {
     DevBuf<double> o_sims;
     DevBuf<int32_t> o_cnt;
     DevBuf<uint8_t> cert;         // per-query exactness certificates
+    uint8_t* cert_out = nullptr;  // sine_query_device_cert: certificates go straight to the caller
     int64_t uncertified = 0;      // queries re-run by the last certify pass
     float cur_thr0 = 0.f;         // admission floor of the running query
     double cur_err = 0.0;         // its filter error bound
@@ -727,8 +728,10 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
         if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
         const ResSmem L = res_smem_layout(S, NQ, kblocks, kp);
+        h->gbound.ensure(static_cast<size_t>(kMaxCS) * NQmax);
         res_prep_queries<<<grid_for(static_cast<int64_t>(CS) * NQ * row_elems, 256, h->num_sms), 256, 0, st>>>(
-            q_dev + q0 * h->dim, nq, CS * NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
+            q_dev + q0 * h->dim, nq, CS * NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p, h->gbound.p,
+            static_cast<int64_t>(CS) * NQ);
         const CUtensorMap qmap = make_kmajor_map(h->qbf.p, tf32, row_elems, static_cast<int64_t>(CS) * NQ, NQ);
         const CUtensorMap rmap = make_kmajor_map(rows, tf32, row_elems, h->nslots, kUmmaN / CS);
         ResParams p{};
@@ -742,9 +745,7 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.stages = S;
         p.tf32 = tf32 ? 1 : 0;
         p.slot_ids = h->ids_ascending ? 1 : 0;
-        h->gbound.ensure(static_cast<size_t>(kMaxCS) * NQmax);
-        CK(cudaMemsetAsync(h->gbound.p, 0, static_cast<size_t>(CS) * NQ * sizeof(uint32_t), st));
-        p.gbound = h->gbound.p;
+        p.gbound = h->gbound.p;  // zeroed by res_prep_queries
         p.tile_stride = 1;
         p.valid = h->valid;
         p.ids = h->ids;
@@ -820,8 +821,7 @@ void umma_pair_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int
     for (int64_t q0 = 0; q0 < B; q0 += NQ) {
         const int nq = static_cast<int>(std::min<int64_t>(NQ, B - q0));
         res_prep_queries<<<grid_for(static_cast<int64_t>(NQ) * row_elems, 256, h->num_sms), 256, 0, st>>>(
-            q_dev + q0 * h->dim, nq, NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p);
-        CK(cudaMemsetAsync(h->gbound.p, 0, NQ * sizeof(uint32_t), st));
+            q_dev + q0 * h->dim, nq, NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p, h->gbound.p, NQ);
         ResParams p{};
         p.nslots = h->nslots;
         p.ntiles = ntiles;
@@ -1237,7 +1237,8 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.rerank = rerank ? 1 : 0;
     m.thr0 = h->cur_thr0;
     m.err = h->cur_err;
-    m.cert = h->cert.p ? h->cert.p + (cert_off) : nullptr;
+    uint8_t* cert_base = h->cert_out ? h->cert_out : h->cert.p;  // caller's device log when given
+    m.cert = cert_base ? cert_base + (cert_off) : nullptr;
     m.debug = getenv("SINE_DEBUG_CERT") ? 1 : 0;
     m.gbound = h->gbound.p;  // every stage-1 kernel publishes its admission bounds here
     m.out_ids = ids_dev;
@@ -1819,6 +1820,24 @@ int sine_query_device(sine_index_t* h, int64_t B, const double* q_dev, int k, do
         query_device_impl(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
         if (mode & SINE_CERTIFY)
             h->uncertified = certify_and_fix(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
+    });
+}
+
+int sine_query_device_cert(sine_index_t* h, int64_t B, const double* q_dev, int k, double min_sim, uint32_t mode,
+                           int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, uint8_t* cert_dev,
+                           void* stream) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        struct Reset {
+            sine_index* h;
+            ~Reset() { h->cert_out = nullptr; }
+        } reset{h};
+        h->cert_out = cert_dev;
+        if (h->nlive == 0 || !(mode & SINE_RERANK_F64))  // nothing to prove: every answer is exact
+            CK(cudaMemsetAsync(cert_dev, 1, B, st));
+        query_device_impl(h, B, q_dev, k, min_sim, mode & ~SINE_CERTIFY, ids_dev, sims_dev, counts_dev, st);
     });
 }
 

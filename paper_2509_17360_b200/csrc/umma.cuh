@@ -984,8 +984,13 @@ __global__ void __launch_bounds__(256) sample_max_bound_kernel(const uint32_t* t
 }
 
 // q64 [nq][dim] -> zero-padded [Nq][stride] bf16 or fp32 (TMA source).
+// Also zeroes the launch's chip-wide admission bounds (zero_n entries of
+// `zero`, nullable) -- one launch instead of a memset plus a launch.
 __global__ void res_prep_queries(const double* q64, int nq, int Nq, int64_t dim, int64_t stride, int tf32,
-                                 void* out) {
+                                 void* out, uint32_t* zero = nullptr, int64_t zero_n = 0) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < zero_n;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        zero[t] = 0u;
     const int64_t total = static_cast<int64_t>(Nq) * stride;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {

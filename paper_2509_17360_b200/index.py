@@ -256,6 +256,17 @@ class GpuCosineIndex:
                                             ctypes.c_void_p(counts_ptr),
                                             ctypes.c_void_p(stream) if stream else None))
 
+    def query_device_cert(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
+                          counts_ptr: int, cert_ptr: int, stream: int | None = None, *, scan: str | None = None,
+                          rerank: bool | None = None) -> None:
+        """query_device writing the exactness certificates (uint8 [B], device)
+        to `cert_ptr` on the stream: no sync; the caller re-runs any 0."""
+        N.check(self._lib.sine_query_device_cert(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
+                                                 float(min_similarity), self._mode(scan, rerank),
+                                                 ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
+                                                 ctypes.c_void_p(counts_ptr), ctypes.c_void_p(cert_ptr),
+                                                 ctypes.c_void_p(stream) if stream else None))
+
     def query_batch_async(self, queries, k: int, min_similarity: float = -1.0, *, check: bool = True,
                           scan: str | None = None, rerank: bool | None = None) -> "PendingQuery":
         """Start a batched stage-1 on the device and return immediately; the

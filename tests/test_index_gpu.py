@@ -605,3 +605,36 @@ def test_gpu_embedder_matches_reference_goldens(pkg):
         pkg.GpuHashedBagEmbedder(256).embed_batch(["ok text", "?!"])
     with pytest.raises(pkg.ValidationError):
         pkg.GpuHashedBagEmbedder(4)
+
+
+def test_query_device_cert_logs_certificates(pkg):
+    """query_device_cert: same answers as query_batch, certificates written
+    to the caller's device buffer (1 for clear answers, 0 for a dense
+    cluster whose bf16 filter cannot prove the cut)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(51)
+    n, d, B = 20000, 128, 40
+    rows = rng.standard_normal((n, d))
+    rows[:3000] = rows[0] + 0.02 * rng.standard_normal((3000, d))  # dense cluster
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    q = rng.standard_normal((B, d))
+    q[0] = rows[0]
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    for scan in ("fp32", "bf16"):
+        idx = pkg.GpuCosineIndex(d, scan=scan)
+        idx.insert_batch(np.arange(n), rows)
+        qd = torch.from_numpy(q).cuda()
+        ids = torch.empty((B, 10), dtype=torch.int64, device="cuda")
+        sims = torch.empty((B, 10), dtype=torch.float64, device="cuda")
+        cnt = torch.empty((B,), dtype=torch.int32, device="cuda")
+        cert = torch.full((B,), 7, dtype=torch.uint8, device="cuda")
+        idx.query_device_cert(B, qd.data_ptr(), 10, 0.5, ids.data_ptr(), sims.data_ptr(), cnt.data_ptr(),
+                              cert.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        c = cert.cpu().numpy()
+        assert set(c.tolist()) <= {0, 1} and c[1:].all()
+        want = idx.query_batch(q, 10, 0.5)  # certified (re-runs any uncertified query)
+        got_ids = ids.cpu().numpy()
+        for j in range(B):
+            if c[j]:
+                assert got_ids[j].tolist() == want[0][j].tolist()
