@@ -432,7 +432,9 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.scan == "fp32" else "bf16",
+                "scaling": "strong", "vs_baseline": None, "dtype": "tf32+f64" if args.scan == "fp32" else "bf16+f64",
+                "dtype_note": "tensor-core filter over fp32 (read as tf32) or bf16 rows with fp32 accumulation; "
+                              "the final k' candidates re-scored in fp64 (exactness certificate, fp32 fallback)",
                 "data": "synthetic: standard-normal rows normalised in float64 (seed 1); queries half planted "
                         "near-duplicates (cos 0.88-0.99), half random",
                 "config": {"workload": f"config B: {args.rows} SEs x d={DIM}, k={K}, batch {b}, "
