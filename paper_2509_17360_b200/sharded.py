@@ -131,10 +131,12 @@ class ShardedCosineIndex:
         stream = torch.cuda.current_stream().cuda_stream
         block = torch.empty((2, B, k), dtype=torch.int64, device=q.device)
         counts = torch.empty((B,), dtype=torch.int32, device=q.device)
-        self.local.query_device(B, q.data_ptr(), k, min_similarity, block[0].data_ptr(), block[1].data_ptr(),
-                                counts.data_ptr(), stream, certify=certify)
-        if cert_out is not None:
-            self.local.copy_certificates(B, cert_out.data_ptr(), stream)
+        if cert_out is not None:  # certificates straight into the caller's device log
+            self.local.query_device_cert(B, q.data_ptr(), k, min_similarity, block[0].data_ptr(),
+                                         block[1].data_ptr(), counts.data_ptr(), cert_out.data_ptr(), stream)
+        else:
+            self.local.query_device(B, q.data_ptr(), k, min_similarity, block[0].data_ptr(), block[1].data_ptr(),
+                                    counts.data_ptr(), stream, certify=certify)
         g = torch.empty((self.world, 2, B, k), dtype=torch.int64, device=q.device)
         dist.all_gather_into_tensor(g.view(-1), block.view(-1), group=self.group)
         return merge_gathered_blocks(g)
