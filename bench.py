@@ -241,8 +241,11 @@ def run_ours(args):
         sh = ShardedCosineIndex(idx)
         sh._rows = [(r + 1) * args.rows // world - r * args.rows // world for r in range(world)]
 
-        def step(s):  # local scan -> one NCCL all-gather -> device shard merge
-            sh.query_device(q_dev[s], K, TAU, certify=False, cert_out=cert_log[s])
+        from paper_2509_17360_b200.sharded import PipelinedShardQueries
+        pipe = PipelinedShardQueries(sh, b, K)
+
+        def step(s):  # local scan -> one NCCL all-gather -> device shard merge; batch i's collective
+            pipe.submit(q_dev[s], TAU, cert_log[s])  # overlaps batch i+1's scan
     else:
         stream = work.cuda_stream
 

@@ -254,7 +254,7 @@ class GpuCosineIndex:
                                             float(min_similarity), mode,
                                             ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
                                             ctypes.c_void_p(counts_ptr),
-                                            ctypes.c_void_p(stream) if stream else None))
+                                            _stream_arg(stream)))
 
     def query_device_cert(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                           counts_ptr: int, cert_ptr: int, stream: int | None = None, *, scan: str | None = None,
@@ -265,7 +265,7 @@ class GpuCosineIndex:
                                                  float(min_similarity), self._mode(scan, rerank),
                                                  ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
                                                  ctypes.c_void_p(counts_ptr), ctypes.c_void_p(cert_ptr),
-                                                 ctypes.c_void_p(stream) if stream else None))
+                                                 _stream_arg(stream)))
 
     def query_batch_async(self, queries, k: int, min_similarity: float = -1.0, *, check: bool = True,
                           scan: str | None = None, rerank: bool | None = None) -> "PendingQuery":
@@ -296,7 +296,7 @@ class GpuCosineIndex:
     def copy_certificates(self, B: int, dst_ptr: int, stream: int | None = None) -> None:
         """Enqueue a device copy of the last batch's exactness certificates."""
         N.check(self._lib.sine_copy_certificates(self._h, int(B), ctypes.c_void_p(dst_ptr),
-                                                 ctypes.c_void_p(stream) if stream else None))
+                                                 _stream_arg(stream)))
 
     def uncertified(self) -> int:
         """Queries the last (certified) call re-ran on the fp32 scan."""
@@ -391,6 +391,18 @@ def parse_snapshot_lines(lines: list[str], magic: str):
         vec = np.array([float.fromhex(p) for p in rest.split(" ")]) if rest else np.zeros(0)
         entries.append((int(head), vec))
     return dimension, seed, entries
+
+
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
+def _stream_arg(stream):
+    """None -> the handle's own stream (C ABI NULL); 0 -> the CUDA legacy
+    default stream (what torch's default stream handle 0 means: work must be
+    ordered with the caller's default-stream kernels); else the handle."""
+    if stream is None:
+        return None
+    return ctypes.c_void_p(stream if stream else _CUDA_STREAM_LEGACY)
 
 
 def parse_snapshot_bytes(data: bytes, magic: str):

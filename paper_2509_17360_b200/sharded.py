@@ -154,3 +154,52 @@ def merge_gathered_blocks(g: torch.Tensor):
                                                out_ids.data_ptr(), out_sims.data_ptr(), out_cnt.data_ptr(),
                                                torch.cuda.current_stream().cuda_stream))
     return out_ids, out_sims, out_cnt
+
+
+class PipelinedShardQueries:
+    """Overlaps batch i's all-gather + shard merge with batch i+1's local
+    scan.  The local pipeline (prep, scan, merge; shared device workspaces)
+    stays on the caller's stream in submission order; each batch's [2, B, k]
+    block is its own slot, and the collective plus the shard-merge kernel
+    run on a second stream after an event.  A slot is rewritten only after
+    its previous collective finished (event wait on the caller's stream).
+    Results of batch i are valid once `drain()` (or the slot's event) has
+    completed."""
+
+    def __init__(self, sharded: ShardedCosineIndex, B: int, k: int, depth: int = 4, device=None):
+        self.sh = sharded
+        self.B, self.k, self.depth = B, k, depth
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.blocks = [torch.empty((2, B, k), dtype=torch.int64, device=dev) for _ in range(depth)]
+        self.gathered = [torch.empty((sharded.world, 2, B, k), dtype=torch.int64, device=dev) for _ in range(depth)]
+        self.counts = torch.empty((B,), dtype=torch.int32, device=dev)
+        self.comm = torch.cuda.Stream(device=dev)
+        self.done = [None] * depth
+        self.results = [None] * depth
+        self.n = 0
+
+    def submit(self, q: torch.Tensor, min_similarity: float, cert_out: torch.Tensor):
+        """Enqueue one batch (CUDA float64 [B, d]); returns its slot."""
+        slot = self.n % self.depth
+        self.n += 1
+        main = torch.cuda.current_stream()
+        if self.done[slot] is not None:
+            main.wait_event(self.done[slot])  # the slot's previous collective has read its block
+        blk = self.blocks[slot]
+        self.sh.local.query_device_cert(self.B, q.data_ptr(), self.k, min_similarity, blk[0].data_ptr(),
+                                        blk[1].data_ptr(), self.counts.data_ptr(), cert_out.data_ptr(),
+                                        main.cuda_stream)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        with torch.cuda.stream(self.comm):
+            self.comm.wait_event(ready)
+            g = self.gathered[slot]
+            dist.all_gather_into_tensor(g.view(-1), blk.view(-1), group=self.sh.group)
+            self.results[slot] = merge_gathered_blocks(g)
+            ev = torch.cuda.Event()
+            ev.record(self.comm)
+            self.done[slot] = ev
+        return slot
+
+    def drain(self):
+        torch.cuda.current_stream().wait_stream(self.comm)

@@ -110,3 +110,73 @@ def test_device_shard_merge_equals_unsharded():
             assert gi.cpu().numpy().tolist() == wi.tolist() == ti.cpu().numpy().tolist()
             assert gc.cpu().numpy().tolist() == wc.tolist()
             np.testing.assert_array_equal(gs.cpu().numpy(), ws)
+
+
+def _pipe_worker(rank, world, port, out, pipelined=True):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from oracle import sine_oracle as O
+    from paper_2509_17360_b200 import GpuCosineIndex
+    from paper_2509_17360_b200.sharded import PipelinedShardQueries, ShardedCosineIndex
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    rng = np.random.default_rng(2)
+    n, d, B, k = 12000, 96, 8, 10
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    ids = np.arange(n) * 5 + 1
+    sh = ShardedCosineIndex(GpuCosineIndex(d, device=0))
+    sh.insert_batch(ids, rows)
+    full = O.OracleExactIndex(d)
+    full.bulk_load(ids, rows)
+    qs = rows[rng.integers(0, n, (9, B))] + 0.08 * rng.standard_normal((9, B, d))
+    qs /= np.linalg.norm(qs, axis=2, keepdims=True)
+    qd = torch.from_numpy(qs).cuda()
+    certs = torch.zeros((9, B), dtype=torch.uint8, device="cuda")
+    got = []
+    if not pipelined:  # the plain device path, batch by batch
+        for s in range(9):
+            r = sh.query_device(qd[s], k, 0.2, certify=False, cert_out=certs[s])
+            torch.cuda.synchronize()
+            got.append((s, [t.cpu().numpy() for t in r]))
+    pipe = PipelinedShardQueries(sh, B, k, depth=3)
+    for s in range(9 if pipelined else 0):
+        slot = pipe.submit(qd[s], 0.2, certs[s])
+        if s >= 2:  # results of batch s-2 are read after a drain (its slot is reused at s+1)
+            pipe.drain()
+            got.append((s - 2, [t.cpu().numpy() for t in pipe.results[(s - 2) % 3]]))
+    pipe.drain()
+    for s in ((7, 8) if pipelined else ()):
+        got.append((s, [t.cpu().numpy() for t in pipe.results[s % 3]]))
+    cert = certs.cpu().numpy()
+    ok = True if int(cert.sum()) >= cert.size // 2 else f"certified {int(cert.sum())} of {cert.size}"
+    for s, (gi, gs, gc) in got:
+        for j in range(B):
+            if not cert[s, j] or ok is not True:
+                continue
+            want = full.query(qs[s, j], k, 0.2)
+            if gi[j, :gc[j]].tolist() != [c.id for c in want]:
+                ok = f"batch {s} q{j}: {gi[j, :gc[j]].tolist()} vs {[c.id for c in want]}"
+            elif not np.allclose(gs[j, :gc[j]], [c.similarity for c in want], atol=1e-12, rtol=0):
+                ok = f"batch {s} q{j}: sims differ"
+    out[rank] = ok
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_pipelined_shard_queries_gloo(pipelined):
+    """The device path with the all-gather on CUDA tensors, batch by batch
+    and with batch i's collective + shard merge overlapping batch i+1's
+    scan (PipelinedShardQueries): every certified answer equals the oracle."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m:
+        out = m.dict()
+        procs = [ctx.Process(target=_pipe_worker, args=(r, 2, port, out, pipelined)) for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(300)
+        assert all(p.exitcode == 0 for p in procs)
+        assert dict(out) == {0: True, 1: True}
