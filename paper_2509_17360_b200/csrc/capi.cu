@@ -187,6 +187,7 @@ struct sine_index {
     DevBuf<int64_t> rsize, dcount;     // record sizes; device counters
     DevBuf<int32_t> rslot;             // record -> slot
     DevBuf<uint64_t> rkeys2;           // the records after the first refinement pass
+    DevBuf<uint8_t> d0;                // eviction pass 1: top byte of every primary key
     DevBuf<int64_t> rsize2;
     DevBuf<int32_t> rslot2;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
@@ -1368,6 +1369,8 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     a.policy = policy;
     a.now = now;
     a.k1 = h->k1.p;
+    h->d0.ensure(std::max<int64_t>(h->cap, 1));
+    a.d0 = policy == 0 ? h->d0.p : nullptr;  // written by the LCFU pass-1 kernel only
     a.first = 1;
     a.st = h->st.p;
     a.hw = hw, a.hc = hc, a.hand = hand, a.hor = hor;
@@ -1384,10 +1387,10 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     h->rslot.ensure(std::max<int64_t>(h->nlive, 1));
     int64_t* nrec = h->dcount.p;      // records
     int64_t* nbelow = h->dcount.p + 1;  // victims below the record prefix
-    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->scratch_i32.p);
+    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->scratch_i32.p, nullptr, nullptr, a.d0);
     expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
     collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->exp_off.p, h->rkeys.p, h->rslot.p, nullptr,
-                                             nullptr, h->rsize.p);
+                                             nullptr, h->rsize.p, nullptr, nullptr, nullptr, nullptr, a.d0);
     CK(cudaMemcpyAsync(nrec, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     h->launches += 5;
     CK(cudaGetLastError());
@@ -1439,10 +1442,10 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     CK(cudaMemsetAsync(kor, 0, 3 * sizeof(unsigned long long), st));
     h->vkeys.ensure(3 * std::max<int64_t>(h->nlive, 1));
     h->vslots.ensure(std::max<int64_t>(h->nlive, 1));
-    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->scratch_i32.p);
+    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->scratch_i32.p, nullptr, nullptr, a.d0);
     expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
     collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
-                                             kor);
+                                             kor, nullptr, nullptr, nullptr, nullptr, nullptr, a.d0);
     CK(cudaMemcpyAsync(nbelow, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     collect_count_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->scratch_i32.p, h->rkeys.p, nrec);
     expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nbr, h->exp_off.p);

@@ -80,6 +80,7 @@ struct HistArgs {
     const int32_t* cand;   // nullptr: all slots
     int64_t ncand;
     uint64_t* k1;          // cached primary keys [nslots]
+    uint8_t* d0;           // pass 1 (LCFU kernel): their top byte [nslots] (nullable)
     int first;             // compute (and cache) primary keys
     const SelectState* st;
     // record mode (rk != nullptr): the candidates were compacted into dense
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(256) evict_pass1_lcfu_kernel(const HistArgs a)
                 }
                 const uint64_t k0 = f64_key(v);
                 a.k1[s] = k0;
+                if (a.d0) a.d0[s] = static_cast<uint8_t>(k0 >> 56);
                 dg = static_cast<uint32_t>(k0 >> 56);
                 vand &= k0;
                 vor |= k0;
@@ -408,6 +410,7 @@ __global__ void __launch_bounds__(256) evict_pick_kernel(SelectState* st, unsign
 struct CollectPred {
     EvictCols c;
     const uint64_t* k1;
+    const uint8_t* d0;   // top byte of k1 (nullable): decides alone when the prefix has one digit
     const uint64_t* rk;  // record source (index = record) instead of slots
     int nd;
     int all;
@@ -419,6 +422,12 @@ struct CollectPred {
     __device__ __forceinline__ bool operator()(int64_t s, uint64_t* k, bool need_keys = true) const {
         if (rk) {
             k[0] = rk[3 * s], k[1] = rk[3 * s + 1], k[2] = rk[3 * s + 2];
+        } else if (d0 && nd == 1 && !all && !need_keys) {
+            // one-digit prefix: a byte per slot instead of the 8-byte key
+            const uint32_t vw = __ldg(c.valid + (s >> 5));
+            const uint32_t dg = __ldg(d0 + s), pd = static_cast<uint32_t>(pre[0] >> 56);
+            if (!((vw >> (s & 31)) & 1u)) return false;
+            return mode == 0 ? dg <= pd : (mode == 1 ? dg == pd : dg < pd);
         } else {
             // both loads issued before the validity test (no dependency chain)
             const uint32_t vw = __ldg(c.valid + (s >> 5));
@@ -442,10 +451,11 @@ struct CollectPred {
 };
 
 __device__ __forceinline__ CollectPred make_pred(const EvictCols& c, const uint64_t* k1, const SelectState* st,
-                                                 int mode, const uint64_t* rk = nullptr) {
+                                                 int mode, const uint64_t* rk = nullptr, const uint8_t* d0 = nullptr) {
     CollectPred p;
     p.c = c;
     p.k1 = k1;
+    p.d0 = d0;
     p.rk = rk;
     p.nd = st->ndigits;
     p.all = st->done == 2;
@@ -461,13 +471,13 @@ constexpr int kColChunk = 4096;  // slots per block; 16 per thread
 // Source: slots [0, nslots), or records [0, *rn) when rk != nullptr.
 __global__ void __launch_bounds__(256) collect_count_kernel(EvictCols c, const uint64_t* k1, const SelectState* st,
                                                             int mode, int32_t* counts, const uint64_t* rk = nullptr,
-                                                            const int64_t* rn = nullptr) {
+                                                            const int64_t* rn = nullptr, const uint8_t* d0 = nullptr) {
     __shared__ int32_t wsum[8];
     if (mode == 2 && st->below == 0) {  // nothing below the record prefix (pass 1's histogram says so)
         if (threadIdx.x == 0) counts[blockIdx.x] = 0;
         return;
     }
-    const CollectPred pred = make_pred(c, k1, st, mode, rk);
+    const CollectPred pred = make_pred(c, k1, st, mode, rk, d0);
     const int64_t n = rk ? *rn : c.nslots;
     const int64_t b = static_cast<int64_t>(blockIdx.x) * kColChunk;
     const int64_t e = min(b + kColChunk, n);
@@ -494,10 +504,11 @@ __global__ void __launch_bounds__(256) collect_write_kernel(EvictCols c, const u
                                                             unsigned long long* kor, int64_t* out_size = nullptr,
                                                             const uint64_t* rk = nullptr, const int64_t* rn = nullptr,
                                                             const int32_t* rslot = nullptr,
-                                                            const int64_t* base = nullptr) {
+                                                            const int64_t* base = nullptr,
+                                                            const uint8_t* d0 = nullptr) {
     __shared__ int32_t wtot[8];
     if (mode == 2 && st->below == 0) return;
-    const CollectPred pred = make_pred(c, k1, st, mode, rk);
+    const CollectPred pred = make_pred(c, k1, st, mode, rk, d0);
     const int64_t n = rk ? *rn : c.nslots;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp w owns entries [block*4096 + 512w, +512): 16 coalesced rounds of
