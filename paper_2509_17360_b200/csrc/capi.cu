@@ -1240,7 +1240,7 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.err = h->cur_err;
     uint8_t* cert_base = h->cert_out ? h->cert_out : h->cert.p;  // caller's device log when given
     m.cert = cert_base ? cert_base + (cert_off) : nullptr;
-    m.debug = getenv("SINE_DEBUG_CERT") ? 1 : 0;
+    m.debug = getenv("SINE_DEBUG_MERGE") ? 2 : (getenv("SINE_DEBUG_CERT") ? 1 : 0);
     m.gbound = h->gbound.p;  // every stage-1 kernel publishes its admission bounds here
     m.out_ids = ids_dev;
     m.out_sims = sims_dev;

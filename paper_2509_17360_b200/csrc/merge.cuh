@@ -111,10 +111,29 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) ns[c] = p.in_n[c * nq + qi];
     if (threadIdx.x == 0) nsel = 0;
     __syncthreads();
-    // stage the pooled keys once: every radix pass below reads shared memory
-    for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
-        const int c = f / kp, e = f - c * kp;
-        pool[f] = e < ns[c] ? p.in_key[(static_cast<size_t>(c) * nq + qi) * kp + e] : 0u;
+    // stage the pooled keys once: every radix pass below reads shared memory.
+    // Loads go out 16 per thread before any store (the staging is latency
+    // bound), and keys below the chip-wide admission bound are dropped: that
+    // bound is <= the true k'-th best key (every CTA's k'-th best is), so
+    // they cannot make the top k' -- the selection then touches only the
+    // few hundred live keys instead of every list entry.
+    const uint32_t gb = p.gbound ? p.gbound[qi] : 0u;
+    for (int f0 = 0; f0 < nflat; f0 += 16 * kMergeThreads) {
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int f = f0 + j * kMergeThreads + threadIdx.x;
+            v[j] = 0u;
+            if (f < nflat) {
+                const int c = f / kp, e = f - c * kp;
+                if (e < ns[c]) v[j] = __ldg(p.in_key + (static_cast<size_t>(c) * nq + qi) * kp + e);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int f = f0 + j * kMergeThreads + threadIdx.x;
+            if (f < nflat) pool[f] = v[j] >= gb ? v[j] : 0u;
+        }
     }
     __syncthreads();
 
@@ -126,9 +145,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     auto key_at = [&](int c, int e) { return pool[c * kp + e]; };
     auto slot_at = [&](int c, int e) { return p.in_slot[(static_cast<size_t>(c) * nq + qi) * kp + e]; };
 
-    // total candidates
+    // total live candidates (after the admission-bound prefilter)
     uint32_t local = 0;
-    for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) local += ns[c];
+    for (int f = threadIdx.x; f < nflat; f += kMergeThreads) local += pool[f] != 0u ? 1u : 0u;
     const uint32_t before_me = block_excl_scan(local, scratch);
     if (threadIdx.x == kMergeThreads - 1) scratch[12] = before_me + local;
     __syncthreads();
@@ -210,7 +229,17 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             double a = 0.0;
             int64_t t = lane;
             // same per-lane order as a plain strided loop (bit-identical
-            // sums), with 8 independent row loads in flight per lane
+            // sums), with 16 independent row loads in flight per lane
+            for (; t + 32 * 15 < p.dim; t += 32 * 16) {
+                double xv[16], qv[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    xv[u] = __ldg(x + t + 32 * u);
+                    qv[u] = __ldg(q + t + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) a = fma(xv[u], qv[u], a);
+            }
             for (; t + 32 * 7 < p.dim; t += 32 * 8) {
                 double xv[8], qv[8];
 #pragma unroll
