@@ -213,6 +213,13 @@ struct sine_index {
 
 namespace {
 
+// programmatic dependent launch between query prep -> scan -> merge
+// (SINE_NO_PDL=1 turns it off, for A/B timing)
+bool pdl_enabled() {
+    static const bool on = getenv("SINE_NO_PDL") == nullptr;
+    return on;
+}
+
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 __global__ void convert_rows_kernel(const double* __restrict__ src, int64_t n, int64_t dim, float* rows32,
@@ -685,6 +692,11 @@ int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams
     }
     const int ncl = std::max(1, std::min(max_clusters, active));
     cfg.gridDim = dim3(ncl * CS);
+    cudaLaunchAttribute at2[2] = {at[0], {}};
+    at2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap setup with the query prep
+    at2[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at2;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     CK(cudaLaunchKernelEx(&cfg, kern, qmap, rmap, p));
     return ncl;
 }
@@ -1253,7 +1265,19 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     const size_t pool_bytes = static_cast<size_t>(ncta) * kp * sizeof(uint32_t);
     if (pool_bytes > 160 * 1024) fail(SINE_EINVAL, "candidate pool exceeds the merge kernel's shared memory");
     const size_t tm = tbegin(h, 1, st);
-    merge_kernel<<<nq, kMergeThreads, pool_bytes, st>>>(m);
+    // PDL: the merge CTAs are scheduled while the scan drains and wait on
+    // the device (griddepcontrol.wait) for its lists instead of a host launch
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(nq);
+    cfg.blockDim = dim3(kMergeThreads);
+    cfg.dynamicSmemBytes = pool_bytes;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, merge_kernel, m));
     tend(h, tm, st);
     ++h->launches;
     CK(cudaGetLastError());

@@ -220,4 +220,13 @@ __device__ __forceinline__ bool valid_bit(const uint32_t* valid, int64_t slot) {
     return (__ldg(valid + (slot >> 5)) >> (slot & 31)) & 1u;
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// stream predecessor is still running; pdl_wait() blocks the calling thread
+// until that predecessor grid has completed and its writes are visible (a
+// no-op when the kernel was launched without the attribute).  pdl_trigger()
+// lets the successor be scheduled once every CTA of this grid has issued it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace sine

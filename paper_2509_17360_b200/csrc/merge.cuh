@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     __shared__ uint32_t nsel;
 
     extern __shared__ uint32_t pool[];  // [ncta * kp] candidate keys, 0 = empty
+    pdl_wait();  // launched early (PDL): the scan's lists are complete past this point
     const int qi = blockIdx.x;
     const int kp = p.kp, nq = p.nq;
     const int nflat = p.ncta * kp;

@@ -697,6 +697,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int kb_elems = p.tf32 ? kUmmaKB / 4 : kUmmaKB / 2;
+    pdl_trigger();  // every CTA is resident: the merge may be scheduled as SMs free up
 
     if (warp == 4) {
         // ---------------- TMA producer ----------------
@@ -705,15 +706,24 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmap)) : "memory");
             const uint64_t pol_rows = l2_evict_first_policy();
             const uint64_t pol_q = l2_evict_last_policy();
-            // this CTA's query group, once
-            mbar_arrive_expect_tx(qfull, static_cast<uint32_t>(nkb) * NQ * kUmmaKB);
-            for (int kb = 0; kb < nkb; ++kb)
-                tma_load_2d(sq + static_cast<size_t>(kb) * NQ * kUmmaKB, &qmap, qfull, kb * kb_elems, crank * NQ,
-                            pol_q);
-            int s = 0;
+            // this CTA's query group, once.  The rows do not depend on the
+            // query-prep kernel, so the first S row stages are issued before
+            // waiting for it (PDL); the queries follow.
+            bool qdone = false;
+            auto load_q = [&]() {
+                pdl_wait();
+                mbar_arrive_expect_tx(qfull, static_cast<uint32_t>(nkb) * NQ * kUmmaKB);
+                for (int kb = 0; kb < nkb; ++kb)
+                    tma_load_2d(sq + static_cast<size_t>(kb) * NQ * kUmmaKB, &qmap, qfull, kb * kb_elems,
+                                crank * NQ, pol_q);
+                qdone = true;
+            };
+            int s = 0, issued = 0;
             uint32_t ph = 0;
             for (int t = cid; t < p.ntiles; t += ncl) {
                 for (int kb = 0; kb < nkb; ++kb) {
+                    if (!qdone && issued == S) load_q();
+                    ++issued;
                     mbar_wait(empty + s, ph ^ 1);
                     mbar_arrive_expect_tx(full + s, kUmmaN * kUmmaKB);
                     uint8_t* dst = sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB + crank * kSliceRows * kUmmaKB;
@@ -729,6 +739,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     }
                 }
             }
+            if (!qdone) load_q();
         }
     } else if (warp == 5) {
         // ---------------- MMA issuer: D[128 rows, NQ] += A(rows) . B(queries)^T ----------------
@@ -772,6 +783,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         }
     } else {
         // ---------------- epilogue: thread = row ----------------
+        pdl_wait();  // the admission bounds come from the query-prep kernel
         const int tid = threadIdx.x;  // 0..127 == TMEM lane == row within tile
         const bool slot_ids = p.slot_ids != 0;
         int i = 0;
@@ -988,6 +1000,7 @@ __global__ void __launch_bounds__(256) sample_max_bound_kernel(const uint32_t* t
 // `zero`, nullable) -- one launch instead of a memset plus a launch.
 __global__ void res_prep_queries(const double* q64, int nq, int Nq, int64_t dim, int64_t stride, int tf32,
                                  void* out, uint32_t* zero = nullptr, int64_t zero_n = 0) {
+    pdl_trigger();  // the scan may start its setup (barriers, TMEM, first row tiles) now
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < zero_n;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x)
         zero[t] = 0u;
