@@ -500,15 +500,20 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                 run(True)
                 uncert = idx.uncertified()
                 torch.cuda.synchronize()
-                # events around every batch, back to back on the stream; the
-                # median per-batch time is robust to a one-off clock dip
-                evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
-                evs[0].record()
-                for r_ in range(reps):
-                    run()
-                    evs[r_ + 1].record()
-                torch.cuda.synchronize()
-                ms = float(np.median([evs[r_].elapsed_time(evs[r_ + 1]) for r_ in range(reps)]))
+                # three groups of `reps` batches back to back on the stream,
+                # two events per group (an event between batches would break
+                # the programmatic-dependent-launch chain, as in the headline
+                # pass); the median group mean is robust to a one-off clock dip
+                grp = []
+                for _ in range(3):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for r_ in range(reps):
+                        run()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    grp.append(e0.elapsed_time(e1) / reps)
+                ms = float(np.median(grp))
                 n = rows.shape[0]
                 byt = algorithmic_bytes(n, DIM, b, K, scan)
                 flops = 2.0 * n * DIM * b

@@ -198,6 +198,12 @@ struct sine_index {
     struct Ticket {
         cudaEvent_t done = nullptr;
         HostBuf<uint8_t> cert;
+        // pinned (UVA-mapped) result staging the merge kernel writes straight
+        // into: no device->host copies on the stream between batches
+        HostBuf<int64_t> sids;
+        HostBuf<double> ssims;
+        HostBuf<int32_t> scnt;
+        bool zero_copy = false;
         bool busy = false, certify = false;
         int64_t B = 0;
         int k = 0;
@@ -1603,7 +1609,7 @@ int sine_destroy(sine_index_t* h) {
         h->st_h.release(), h->n_h.release(), h->cnt_h.release(), h->cert_h.release();
         for (auto& t : h->tickets) {
             if (t.done) cudaEventDestroy(t.done);
-            t.cert.release();
+            t.cert.release(), t.sids.release(), t.ssims.release(), t.scnt.release();
         }
         for (auto& e : h->ev) cudaEventDestroy(e);
         cudaStreamDestroy(h->stream);
@@ -1783,15 +1789,36 @@ int sine_query_submit(sine_index_t* h, int64_t B, const double* q, int k, double
         h->o_sims.ensure(B * k);
         h->o_cnt.ensure(B);
         CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
         t.certify = (mode & SINE_RERANK_F64) && (h->flags & SINE_STORE_F32) && h->nlive > 0;
-        if (t.certify) {
-            t.cert.ensure(B);
-            CK(cudaMemcpyAsync(t.cert.p, h->cert.p, B, cudaMemcpyDeviceToHost, h->stream));
+        if (t.certify) t.cert.ensure(B);
+        t.zero_copy = h->nlive > 0;
+        if (t.zero_copy) {
+            // results land in this ticket's pinned staging (mapped into the
+            // device address space); sine_query_wait copies them out
+            t.sids.ensure(B * k);
+            t.ssims.ensure(B * k);
+            t.scnt.ensure(B);
+            int64_t* d_ids;
+            double* d_sims;
+            int32_t* d_cnt;
+            uint8_t* d_cert = nullptr;
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_ids), t.sids.p, 0));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_sims), t.ssims.p, 0));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_cnt), t.scnt.p, 0));
+            if (t.certify) CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_cert), t.cert.p, 0));
+            struct Reset {
+                sine_index* h;
+                ~Reset() { h->cert_out = nullptr; }
+            } reset{h};
+            h->cert_out = d_cert;
+            query_device_impl(h, B, h->q64.p, k, min_sim, mode, d_ids, d_sims, d_cnt, h->stream);
+        } else {
+            query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
+            if (t.certify) CK(cudaMemcpyAsync(t.cert.p, h->cert.p, B, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
         }
-        CK(cudaMemcpyAsync(out_ids, h->o_ids.p, B * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaMemcpyAsync(out_sims, h->o_sims.p, B * k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaMemcpyAsync(out_counts, h->o_cnt.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaEventRecord(t.done, h->stream));
         t.busy = true;
         t.B = B, t.k = k, t.min_sim = min_sim, t.mode = mode;
@@ -1815,6 +1842,11 @@ int sine_query_wait(sine_index_t* h, int64_t ticket) {
         auto& t = h->tickets[ticket];
         t.busy = false;
         h->uncertified = 0;
+        if (t.zero_copy) {
+            std::memcpy(t.ids, t.sids.p, t.B * t.k * sizeof(int64_t));
+            std::memcpy(t.sims, t.ssims.p, t.B * t.k * sizeof(double));
+            std::memcpy(t.counts, t.scnt.p, t.B * sizeof(int32_t));
+        }
         if (!t.certify) return;
         // re-run uncertified queries on the fp32 scan from the caller's host
         // copy (the device workspace may already hold a later batch)
