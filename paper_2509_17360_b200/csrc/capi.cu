@@ -195,6 +195,9 @@ struct sine_index {
     HostBuf<unsigned long long> n_h;
     HostBuf<int32_t> cnt_h;
     HostBuf<uint8_t> cert_h;
+    HostBuf<int64_t> ids_zc;  // sine_query's mapped result staging
+    HostBuf<double> sims_zc;
+    HostBuf<int32_t> cnt_zc;
     struct Ticket {
         cudaEvent_t done = nullptr;
         HostBuf<uint8_t> cert;
@@ -1607,6 +1610,7 @@ int sine_destroy(sine_index_t* h) {
         h->vpack.release(), h->vpack_out.release(), h->vkey_out.release(), h->vslots_out.release();
         h->exp_off.release(), h->sel_h.release(), h->gbound.release();
         h->st_h.release(), h->n_h.release(), h->cnt_h.release(), h->cert_h.release();
+        h->ids_zc.release(), h->sims_zc.release(), h->cnt_zc.release();
         for (auto& t : h->tickets) {
             if (t.done) cudaEventDestroy(t.done);
             t.cert.release(), t.sids.release(), t.ssims.release(), t.scnt.release();
@@ -1737,10 +1741,47 @@ int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_si
         h->o_sims.ensure(B * k);
         h->o_cnt.ensure(B);
         CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        const bool certify = (mode & SINE_RERANK_F64) && (h->flags & SINE_STORE_F32) && h->nlive > 0;
+        if (h->nlive > 0) {
+            // results (and certificates) written by the merge kernel straight
+            // into pinned, device-mapped staging: one host sync, no copies
+            h->ids_zc.ensure(B * k);
+            h->sims_zc.ensure(B * k);
+            h->cnt_zc.ensure(B);
+            if (certify) h->cert_h.ensure(B);
+            int64_t* d_ids;
+            double* d_sims;
+            int32_t* d_cnt;
+            uint8_t* d_cert = nullptr;
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_ids), h->ids_zc.p, 0));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_sims), h->sims_zc.p, 0));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_cnt), h->cnt_zc.p, 0));
+            if (certify) CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_cert), h->cert_h.p, 0));
+            {
+                struct Reset {
+                    sine_index* h;
+                    ~Reset() { h->cert_out = nullptr; }
+                } reset{h};
+                h->cert_out = d_cert;
+                query_device_impl(h, B, h->q64.p, k, min_sim, mode, d_ids, d_sims, d_cnt, h->stream);
+            }
+            CK(cudaStreamSynchronize(h->stream));
+            h->uncertified = 0;
+            if (certify)  // re-runs write the same mapped staging, synchronised
+                h->uncertified = certify_and_fix(h, B, h->q64.p, k, min_sim, mode, d_ids, d_sims, d_cnt, h->stream,
+                                                 h->cert_h.p);
+            std::memcpy(out_ids, h->ids_zc.p, B * k * sizeof(int64_t));
+            std::memcpy(out_sims, h->sims_zc.p, B * k * sizeof(double));
+            std::memcpy(out_counts, h->cnt_zc.p, B * sizeof(int32_t));
+            if (h->timing) {
+                CK(cudaEventElapsedTime(&h->t_scan, h->ev[0], h->ev[1]));
+                CK(cudaEventElapsedTime(&h->t_merge, h->ev[1], h->ev[2]));
+            }
+            return;
+        }
         query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
         // results and certificates come back together: one host sync in the
         // common (all certified) case
-        const bool certify = (mode & SINE_RERANK_F64) && (h->flags & SINE_STORE_F32) && h->nlive > 0;
         if (certify) {
             h->cert_h.ensure(B);
             CK(cudaMemcpyAsync(h->cert_h.p, h->cert.p, B, cudaMemcpyDeviceToHost, h->stream));
