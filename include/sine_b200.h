@@ -132,10 +132,12 @@ int sine_query_device_cert(sine_index_t *h, int64_t B, const double *q_dev, int 
                            double min_sim, uint32_t mode, int64_t *ids_dev, double *sims_dev,
                            int32_t *counts_dev, uint8_t *cert_dev, void *stream);
 
-/* Asynchronous sine_query: enqueue the batch (host buffers, ideally pinned,
- * which must stay valid until the wait) and return a ticket; up to 16
- * batches in flight.  sine_query_wait blocks until the batch's results are
- * in the output buffers, after the exactness certificate check. */
+/* Asynchronous sine_query: enqueue the batch (host buffers, which must stay
+ * valid until the wait; pinned queries upload fastest) and return a ticket;
+ * up to 16 batches in flight.  The device writes each ticket's results into
+ * pinned, device-mapped staging owned by the handle; sine_query_wait blocks
+ * until the batch is done, copies them into the output buffers and runs the
+ * exactness certificate check. */
 int sine_query_submit(sine_index_t *h, int64_t B, const double *q, int k, double min_sim,
                       uint32_t mode, int64_t *out_ids, double *out_sims,
                       int32_t *out_counts, int64_t *ticket);
