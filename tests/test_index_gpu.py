@@ -638,3 +638,62 @@ def test_query_device_cert_logs_certificates(pkg):
         for j in range(B):
             if c[j]:
                 assert got_ids[j].tolist() == want[0][j].tolist()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_mapped_result_staging_sync_and_async(pkg, scan):
+    """sine_query / sine_query_submit write results through pinned, device-
+    mapped staging (no device->host copies): plain (unpinned) numpy output
+    buffers, batch and k growing between tickets, an uncertified query
+    re-run through the async path, and an empty index (the copy branch)."""
+    rng = np.random.default_rng(77)
+    d, n = 256, 4000
+    base = rng.standard_normal(d)
+    base /= np.linalg.norm(base)
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    for i in range(300):                       # dense cluster: forces a certificate failure
+        g = rows[i] - (rows[i] @ base) * base
+        g /= np.linalg.norm(g)
+        c = 0.999 - i * 2e-5
+        rows[i] = c * base + np.sqrt(1 - c * c) * g
+    ids = rng.permutation(10 * n)[:n]
+    empty = pkg.GpuCosineIndex(d, scan=scan, store_f32=True, store_bf16=True)
+    qe = np.ascontiguousarray(rows[:2])
+    oi, osm, oc = np.zeros((2, 4), np.int64), np.ones((2, 4)), np.full(2, 9, np.int32)
+    empty.query_into(qe, 4, -1.0, oi, osm, oc)
+    assert oc.tolist() == [0, 0] and (oi == -1).all()
+    t = empty.submit_into(qe, 4, -1.0, oi, osm, oc)
+    empty.wait_ticket(t)
+    assert oc.tolist() == [0, 0] and (oi == -1).all()
+
+    idx = pkg.GpuCosineIndex(d, scan=scan, store_f32=True, store_bf16=True)
+    idx.insert_batch(ids, rows)
+    ora = O.OracleExactIndex(d)
+    ora.bulk_load(ids, rows)
+    plan = [(1, 5), (3, 12), (2, 40), (5, 3)]  # (B, k): staging grows and shrinks
+    batches, tickets = [], []
+    for s, (B, k) in enumerate(plan):
+        q = rows[rng.integers(300, n, B)] + 0.01 * rng.standard_normal((B, d))
+        if s == 2:
+            q[0] = base                        # the uncertified one
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        q = np.ascontiguousarray(q)
+        out = (np.zeros((B, k), np.int64), np.zeros((B, k)), np.zeros(B, np.int32))
+        batches.append((q, k, out))
+        tickets.append(idx.submit_into(q, k, -1.0, *out))
+    for (q, k, out), t in zip(batches, tickets):
+        idx.wait_ticket(t)
+        for j in range(q.shape[0]):
+            want = ora.query(q[j], k, -1.0)
+            assert out[0][j, :out[2][j]].tolist() == [c.id for c in want]
+            np.testing.assert_allclose(out[1][j, :out[2][j]], [c.similarity for c in want], atol=1e-12)
+    # synchronous path, same staging reused at another shape
+    q, k, _ = batches[2]
+    out = (np.zeros((q.shape[0], k), np.int64), np.zeros((q.shape[0], k)), np.zeros(q.shape[0], np.int32))
+    idx.query_into(q, k, -1.0, *out)
+    for j in range(q.shape[0]):
+        want = ora.query(q[j], k, -1.0)
+        assert out[0][j, :out[2][j]].tolist() == [c.id for c in want]
+    assert idx.uncertified() >= 1
