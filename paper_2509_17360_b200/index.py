@@ -228,8 +228,10 @@ class GpuCosineIndex:
     def submit_into(self, q: np.ndarray, k: int, min_similarity: float, ids: np.ndarray, sims: np.ndarray,
                     counts: np.ndarray, *, scan: str | None = None, rerank: bool | None = None) -> int:
         """Asynchronous query_into (sine_query_submit): the caller's buffers
-        (pinned host memory) must stay untouched until wait_ticket(ticket)
-        returns; up to 16 batches in flight, executed in submission order."""
+        must stay untouched until wait_ticket(ticket) returns (pinned queries
+        upload fastest; the device writes results into the handle's mapped
+        staging and wait_ticket copies them out); up to 16 batches in
+        flight, executed in submission order."""
         t = ctypes.c_int64()
         N.check(self._lib.sine_query_submit(self._h, q.shape[0], q.ctypes.data, int(k), float(min_similarity),
                                             self._mode(scan, rerank), ids.ctypes.data, sims.ctypes.data,
