@@ -769,6 +769,13 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.slot_ids = h->ids_ascending ? 1 : 0;
         p.gbound = h->gbound.p;  // zeroed by res_prep_queries
         p.tile_stride = 1;
+        // a single query over fp32 rows: FFMA on the staged tiles instead of
+        // N = 16 MMAs that are 15/16 padding.  Same box, config B, B = 1:
+        // fp32 2166-2177 vs 1851-1862 lookups/s (kernel 0.451 vs 0.521 ms);
+        // bf16 rows lose (3611 vs 3760: twice the FMAs per byte), so they
+        // keep the MMAs.  SINE_NO_FFMA=1 keeps the MMAs, for A/B timing.
+        static const bool ffma_on = getenv("SINE_NO_FFMA") == nullptr;
+        p.ffma = ffma_on && tf32 && CS == 1 && nq == 1 && NQ == 16 ? 1 : 0;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;

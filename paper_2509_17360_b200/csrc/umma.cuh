@@ -407,6 +407,8 @@ struct ResParams {
     int slot_ids;     // slot order == id order (ties resolved without loads)
     uint32_t* gbound;  // [nq] chip-wide admission bound per query (f32 keys)
     int tile_stride;   // 1 = every tile; >1 = sample pass over every tile_stride-th tile
+    int ffma;          // 1 = single query: the epilogue warps take the dot products with FFMA
+                       //     straight from the TMA-staged tiles (no MMAs)
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -662,7 +664,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, CS);  // released by the MMA commits of every CTA in the cluster
+            // released by the MMA commits of every CTA in the cluster, or by
+            // the four epilogue warps in the FFMA (single-query) mode
+            mbar_init(empty + s, p.ffma ? 4 : CS);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
@@ -743,7 +747,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         }
     } else if (warp == 5) {
         // ---------------- MMA issuer: D[128 rows, NQ] += A(rows) . B(queries)^T ----------------
-        if (lane == 0) {
+        if (lane == 0 && !p.ffma) {
             const uint32_t idesc = umma_idesc(p.tf32, kUmmaN, NQ);
             mbar_wait(qfull, 0);
             int s = 0;
@@ -787,6 +791,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         const int tid = threadIdx.x;  // 0..127 == TMEM lane == row within tile
         const bool slot_ids = p.slot_ids != 0;
         int i = 0;
+        int fs = 0;  // FFMA mode: this thread's view of the stage ring
+        uint32_t fph = 0;
+        if (p.ffma) mbar_wait(qfull, 0);
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
             const int64_t slot = static_cast<int64_t>(t) * p.tile_stride * kUmmaN + tid;
@@ -799,21 +806,62 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 if (g) thr[tid] = fmaxf(thr[tid], key_f32(g));
             }
             named_bar_sync(2, 128);
-            mbar_wait(tfull + acc, (i >> 1) & 1);
-            tc_fence_after();
             float sc[NQ];
+            if (p.ffma) {
+                // one query: 768 FMAs per row per tile on the CUDA cores, read
+                // from the 128B-swizzled stages (16-B chunk c of row r sits at
+                // chunk c ^ (r & 7)); query row 0 of each K block is unswizzled
+                float a0 = 0.0f, a1 = 0.0f;
+                const int sw = tid & 7;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full + fs, fph);
+                    const uint8_t* rowp = sa + static_cast<size_t>(fs) * kUmmaN * kUmmaKB + tid * kUmmaKB;
+                    const uint8_t* qp = sq + static_cast<size_t>(kb) * NQ * kUmmaKB;
 #pragma unroll
-            for (int c = 0; c < NQ / 16; ++c) {
-                uint32_t r[16];
-                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * NQ + c * 16;
-                SINE_TMEM_LD16(taddr, r);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+                        const uint4 qv = *reinterpret_cast<const uint4*>(qp + (c << 4));
+                        if (p.tf32) {
+                            a0 = fmaf(__uint_as_float(xv.x), __uint_as_float(qv.x), a0);
+                            a1 = fmaf(__uint_as_float(xv.y), __uint_as_float(qv.y), a1);
+                            a0 = fmaf(__uint_as_float(xv.z), __uint_as_float(qv.z), a0);
+                            a1 = fmaf(__uint_as_float(xv.w), __uint_as_float(qv.w), a1);
+                        } else {
+                            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
-                for (int j = 0; j < 16; ++j) sc[c * 16 + j] = __uint_as_float(r[j]) + 0.0f;
+                            for (int u = 0; u < 4; ++u) {
+                                a0 = fmaf(__uint_as_float(xw[u] << 16), __uint_as_float(qw[u] << 16), a0);
+                                a1 = fmaf(__uint_as_float(xw[u] & 0xffff0000u), __uint_as_float(qw[u] & 0xffff0000u),
+                                          a1);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + fs);
+                    if (++fs == S) {
+                        fs = 0;
+                        fph ^= 1;
+                    }
+                }
+                sc[0] = (a0 + a1) + 0.0f;
+#pragma unroll
+                for (int j = 1; j < NQ; ++j) sc[j] = 0.0f;
+            } else {
+                mbar_wait(tfull + acc, (i >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < NQ / 16; ++c) {
+                    uint32_t r[16];
+                    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + acc * NQ + c * 16;
+                    SINE_TMEM_LD16(taddr, r);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) sc[c * 16 + j] = __uint_as_float(r[j]) + 0.0f;
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + acc);  // TMEM buffer free for tile i+2
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty + acc);  // TMEM buffer free for tile i+2
             if (p.out_max) {
                 tile_max_out<NQ>(sc, live, nq_local, wball, p.out_max + static_cast<size_t>(t) * p.nq + crank * NQ,
                                  warp, lane, tid);
