@@ -1,0 +1,194 @@
+"""Full-size stage-1 parity at the BASELINE configs.
+
+Config B (1M SEs x d=768, k=10) and config C (10M x 1024, k=20) are run
+through the same entry points the bench times -- the B=1 fp32 path (FFMA
+epilogue over TMA-staged tiles), B=64 and B=4096 in both modes, and the
+async submit/wait C ABI -- and every answer is compared with the float64
+ground truth of the reference algorithm (`ExactCosineIndex.query`,
+pkg/src/semcache/index.py:94-102; `_rank` :42-46) computed on the device
+by `tests/_truth.py`.  Both thresholds: tau_sim 0.9 (the engine's call
+sites) and -1 (every row admitted)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from _truth import Truth, check_query, planted_queries, unit_rows
+
+pytestmark = pytest.mark.gpu
+
+N_B, D_B, K_B = 1_000_000, 768, 10
+TAUS = (0.9, -1.0)
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    if not t.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return t
+
+
+@pytest.fixture(scope="module")
+def config_b(torch):
+    import paper_2509_17360_b200 as P
+    x = unit_rows(torch, N_B, D_B, seed=1)
+    idx = P.GpuCosineIndex(D_B, store_f32=True, store_bf16=True, capacity=N_B)
+    idx.insert_device(np.arange(N_B), x.data_ptr())
+    rng = np.random.default_rng(3)
+    src = x[torch.from_numpy(rng.integers(0, N_B, 16)).cuda()].cpu().numpy()
+    q64 = planted_queries(src, 32, D_B, seed=4)                       # 64 queries
+    src2 = x[torch.from_numpy(rng.integers(0, N_B, 1024)).cuda()].cpu().numpy()
+    q4096 = planted_queries(src2, 2048, D_B, seed=5)                  # 4096 queries
+    t64, t4096 = Truth(torch, q64, K_B), Truth(torch, q4096, K_B)
+    t64.add_chunk(x, 0)
+    t4096.add_chunk(x, 0)
+    del x
+    torch.cuda.empty_cache()
+    yield idx, q64, t64, q4096, t4096
+    idx.close()
+
+
+def _check_batch(ids, sims, counts, q_truth, rows, k, tau, tag):
+    for j in rows:
+        tid, tsim = q_truth.answer(j, tau)
+        check_query(ids[j], sims[j], counts[j], tid, tsim, k, tau, f"{tag} q{j}")
+
+
+@pytest.mark.parametrize("tau", TAUS)
+def test_config_b_single_query_fp32_headline_path(config_b, tau):
+    """The timed headline step: B=1, fp32 exact mode + fp64 re-rank, 64
+    queries (32 planted incl. 16 exact copies), each its own call."""
+    idx, q, truth, _, _ = config_b
+    hits = 0
+    for j in range(q.shape[0]):
+        ids, sims, counts = idx.query_batch(q[j:j + 1], K_B, tau, scan="fp32")
+        tid, tsim = truth.answer(j, tau)
+        check_query(ids[0], sims[0], counts[0], tid, tsim, K_B, tau, f"B=1 tau={tau} q{j}")
+        hits += int(counts[0] > 0)
+    if tau == 0.9:
+        assert hits >= 16  # every exact copy is a hit at similarity 1
+    # the reference-shaped API on a few of them
+    for j in range(4):
+        got = idx.query(q[j], k=K_B, min_similarity=tau)
+        tid, tsim = truth.answer(j, tau)
+        check_query(np.array([c.id for c in got] + [-1] * (K_B - len(got))),
+                    np.array([c.similarity for c in got] + [0.0] * (K_B - len(got))), len(got),
+                    tid, tsim, K_B, tau, f"query() q{j}")
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+@pytest.mark.parametrize("tau", TAUS)
+def test_config_b_batch_64(config_b, scan, tau):
+    idx, q, truth, _, _ = config_b
+    ids, sims, counts = idx.query_batch(q, K_B, tau, scan=scan)
+    _check_batch(ids, sims, counts, truth, range(q.shape[0]), K_B, tau, f"B=64 {scan} tau={tau}")
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+@pytest.mark.parametrize("tau", TAUS)
+def test_config_b_batch_4096(config_b, scan, tau):
+    idx, _, _, q, truth = config_b
+    ids, sims, counts = idx.query_batch(q, K_B, tau, scan=scan)
+    _check_batch(ids, sims, counts, truth, range(q.shape[0]), K_B, tau, f"B=4096 {scan} tau={tau}")
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_config_b_async_submit_wait(config_b, scan):
+    """The e2e API the bench times: sine_query_submit / sine_query_wait,
+    4 batches in flight, B=1 each."""
+    from paper_2509_17360_b200 import _native as N
+    idx, q, truth, _, _ = config_b
+    depth, tau = 4, 0.9
+    bufs = [(N.PinnedArray((1, D_B), np.float64), N.PinnedArray((1, K_B), np.int64),
+             N.PinnedArray((1, K_B), np.float64), N.PinnedArray((1,), np.int32)) for _ in range(depth)]
+    inflight = []
+    for j in range(q.shape[0] + depth):
+        if len(inflight) == depth or j >= q.shape[0]:
+            if not inflight:
+                break
+            jj, t = inflight.pop(0)
+            idx.wait_ticket(t)
+            _, oi, os_, oc = bufs[jj % depth]
+            tid, tsim = truth.answer(jj, tau)
+            check_query(oi.array[0], os_.array[0], oc.array[0], tid, tsim, K_B, tau, f"async {scan} q{jj}")
+        if j < q.shape[0]:
+            qh, oi, os_, oc = bufs[j % depth]
+            qh.array[0] = q[j]
+            inflight.append((j, idx.submit_into(qh.array, K_B, tau, oi.array, os_.array, oc.array, scan=scan)))
+
+
+def test_config_b_bf16_fast_mode_recall(config_b):
+    """bf16 fast mode without the fp64 re-rank: similarities within the
+    north star's 2e-2 and recall@10 against the float64 truth (stated in
+    DESIGN.md; asserted >= 0.95 at tau -1 over 4096 queries)."""
+    idx, _, _, q, truth = config_b
+    ids, sims, counts = idx.query_batch(q, K_B, -1.0, scan="bf16", rerank=False)
+    found = total = 0
+    for j in range(q.shape[0]):
+        tid, tsim = truth.answer(j, -1.0)
+        want = set(tid[:K_B].tolist())
+        got = ids[j, :counts[j]]
+        found += len(want & set(got.tolist()))
+        total += len(want)
+        # every returned similarity is within 2e-2 of that row's true cosine
+        pos = {int(i): s for i, s in zip(truth.pool_ids[j], truth.pool_sims[j])}
+        for i, s in zip(got.tolist(), sims[j, :counts[j]].tolist()):
+            if i in pos:
+                assert abs(s - pos[i]) < 2e-2
+    recall = found / total
+    print(f"bf16 fast-mode recall@10 at config B (4096 queries, tau -1): {recall:.5f}")
+    assert recall >= 0.95
+
+
+# --------------------------------------------------------------- config C
+
+N_C, D_C, K_C, CHUNK_C = 10_000_000, 1024, 20, 1_000_000
+
+
+@pytest.fixture(scope="module")
+def config_c(torch, config_b):
+    import gc
+    import paper_2509_17360_b200 as P
+    idx_b = config_b[0]
+    idx_b.close()  # free config B's 10.7 GB first
+    gc.collect()
+    torch.cuda.empty_cache()
+    idx = P.GpuCosineIndex(D_C, store_f32=True, store_bf16=True, capacity=N_C)
+    rng = np.random.default_rng(9)
+    picks = np.sort(rng.choice(N_C, 8, replace=False))
+    src = []
+    for c in range(N_C // CHUNK_C):
+        x = unit_rows(torch, CHUNK_C, D_C, seed=100 + c)
+        idx.insert_device(np.arange(c * CHUNK_C, (c + 1) * CHUNK_C), x.data_ptr())
+        for p in picks[(picks >= c * CHUNK_C) & (picks < (c + 1) * CHUNK_C)]:
+            src.append(x[int(p - c * CHUNK_C)].cpu().numpy())
+        del x
+    q = planted_queries(np.asarray(src), 16, D_C, seed=10)            # 32 queries
+    truth = Truth(torch, q, K_C)
+    for c in range(N_C // CHUNK_C):
+        x = unit_rows(torch, CHUNK_C, D_C, seed=100 + c)
+        truth.add_chunk(x, c * CHUNK_C)
+        del x
+    torch.cuda.empty_cache()
+    yield idx, q, truth
+    idx.close()
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+@pytest.mark.parametrize("tau", TAUS)
+def test_config_c_batch_32(config_c, scan, tau):
+    idx, q, truth = config_c
+    ids, sims, counts = idx.query_batch(q, K_C, tau, scan=scan)
+    _check_batch(ids, sims, counts, truth, range(q.shape[0]), K_C, tau, f"C B=32 {scan} tau={tau}")
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_config_c_single_queries(config_c, scan):
+    idx, q, truth = config_c
+    for j in range(8):
+        for tau in TAUS:
+            ids, sims, counts = idx.query_batch(q[j:j + 1], K_C, tau, scan=scan)
+            tid, tsim = truth.answer(j, tau)
+            check_query(ids[0], sims[0], counts[0], tid, tsim, K_C, tau, f"C B=1 {scan} tau={tau} q{j}")
