@@ -15,7 +15,7 @@
  *                                 model.py:85-110, engine.py:330-334)
  *   sine_remove                  ExactCosineIndex.remove     index.py:80-92
  *   sine_size / sine_ids         __len__ / ids()             index.py:64-69
- *   sine_get_rows                snapshot_lines() rows       index.py:104-107
+ *   sine_get_rows / sine_snapshot  snapshot_lines() rows     index.py:104-107
  *   sine_query[_device]          ExactCosineIndex.query      index.py:94-102
  *                                + _rank                     index.py:42-46
  *                                (batched: B independent queries)
@@ -109,8 +109,16 @@ int sine_insert_device(sine_index_t *h, int64_t n, const int64_t *ids,
 int sine_remove(sine_index_t *h, int64_t n, const int64_t *ids);
 
 int sine_size(sine_index_t *h, int64_t *live, int64_t *slots);
+/* Live ids in the reference's order (ExactCosineIndex._ids: insertion
+ * order, the last id swapped into a removed id's place, index.py:71-92).
+ * Writes min(*n, cap) ids; *n = the live count. */
 int sine_ids(sine_index_t *h, int64_t *out, int64_t cap, int64_t *n);
 int sine_get_rows(sine_index_t *h, int64_t n, const int64_t *ids, double *out);
+/* Atomic snapshot (snapshot_lines, index.py:104-107): the ids in sine_ids
+ * order and their fp64 rows [n][dim], under one hold of the handle lock.
+ * *n = the live count; fails with SINE_EINVAL (buffers untouched) when
+ * cap < *n. */
+int sine_snapshot(sine_index_t *h, int64_t cap, int64_t *ids, double *rows, int64_t *n);
 
 /* B queries, host float64 [B, dim].  Outputs (host): ids [B, k] (-1 padded),
  * sims [B, k], counts [B].  Each query's result equals

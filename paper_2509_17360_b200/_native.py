@@ -52,6 +52,7 @@ _SIGS = {
     "sine_size": (ctypes.c_int, [ctypes.c_void_p, _i64p, _i64p]),
     "sine_ids": (ctypes.c_int, [ctypes.c_void_p, _i64p, ctypes.c_int64, _i64p]),
     "sine_get_rows": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _i64p, _f64p]),
+    "sine_snapshot": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _i64p, _f64p, _i64p]),
     "sine_query": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _f64p, ctypes.c_int, ctypes.c_double,
                                   ctypes.c_uint32, _i64p, _f64p, _i32p]),
     "sine_query_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,

@@ -21,7 +21,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -97,6 +99,17 @@ struct DevBuf {
     }
 };
 
+// a device bitmap owned by shared tickets (freed with the last owner)
+struct DevBitmap {
+    uint32_t* p = nullptr;
+    DevBitmap() = default;
+    DevBitmap(const DevBitmap&) = delete;
+    DevBitmap& operator=(const DevBitmap&) = delete;
+    ~DevBitmap() {
+        if (p) cudaFree(p);
+    }
+};
+
 template <typename T>
 struct HostBuf {
     T* p = nullptr;
@@ -140,9 +153,22 @@ struct sine_index {
     std::vector<int64_t> ids_h;   // by slot
     std::vector<uint8_t> live_h;  // by slot
     std::unordered_map<int64_t, int64_t> pos;
+    // the reference's id order (ExactCosineIndex._ids, index.py:71-92):
+    // appended on insert, swap-last on removal.  ids() and the snapshot
+    // follow it, so they are byte-identical to the reference after any
+    // sequence of inserts and removals.
+    std::vector<int64_t> order_slot;  // position -> slot
+    std::vector<int64_t> order_pos;   // slot -> position (-1 once removed)
 
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
+    // Query workspaces (q64, lkey/lslot/ln, gbound, qbf, cert, ...) and the
+    // store itself are used by kernels on the handle's stream and on caller
+    // streams (sine_query_device*): every entry point orders its work after
+    // the previous user's (ws_acquire), so a later call cannot overwrite a
+    // workspace, or reallocate rows, under kernels still running elsewhere.
+    cudaStream_t ws_stream = nullptr;  // last stream that enqueued store/workspace work
+    cudaEvent_t ws_ev = nullptr;       // recorded after that work when it was a caller stream
     bool timing = false;
     // accumulated per-kernel device time (CUDA events on the launch stream)
     struct Timed {
@@ -208,6 +234,8 @@ struct sine_index {
         HostBuf<int32_t> scnt;
         bool zero_copy = false;
         bool busy = false, certify = false;
+        int64_t nslots = 0;                            // store slots at submission
+        std::shared_ptr<DevBitmap> valid_snap;  // bitmap at submission (set on the first later removal)
         int64_t B = 0;
         int k = 0;
         double min_sim = 0.0;
@@ -218,6 +246,14 @@ struct sine_index {
         int32_t* counts = nullptr;
     };
     std::vector<Ticket> tickets;
+    // submit-time snapshots for certificate re-runs: the store is append-only
+    // between compactions, so a ticket's snapshot is (its nslots, the
+    // validity bitmap before the first tombstone written after it).  The
+    // bitmap is copied lazily -- only when a removal lands while certified
+    // tickets are in flight -- and compaction waits until they drain.
+    int64_t snap_nslots = -1;            // scan override during a re-run
+    const uint32_t* snap_valid = nullptr;
+    bool compact_pending = false;
 };
 
 namespace {
@@ -230,6 +266,32 @@ bool pdl_enabled() {
 }
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+void ws_acquire(sine_index* h, cudaStream_t st) {
+    if (h->ws_stream && h->ws_stream != st) {
+        if (h->ws_stream == h->stream) CK(cudaEventRecord(h->ws_ev, h->stream));
+        CK(cudaStreamWaitEvent(st, h->ws_ev, 0));  // caller-stream users recorded ws_ev on release
+    }
+    h->ws_stream = st;
+}
+
+void ws_release(sine_index* h, cudaStream_t st) {
+    if (st != h->stream) CK(cudaEventRecord(h->ws_ev, st));  // the caller's stream may not outlive us
+}
+
+// Opt a kernel in to > 48 KB of dynamic shared memory.  The attribute is
+// per device (per context), so it is remembered per (kernel, device): an
+// index on device 1 created after one on device 0 opts in again.
+void smem_optin(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({fn, dev})) return;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({fn, dev});
+}
 
 __global__ void convert_rows_kernel(const double* __restrict__ src, int64_t n, int64_t dim, float* rows32,
                                     int64_t stride32, __nv_bfloat16* rows16, int64_t stride16) {
@@ -449,6 +511,8 @@ void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bo
     CK(cudaGetLastError());
     const bool was_ascending = h->ids_ascending;
     for (int64_t i = 0; i < n; ++i) {
+        h->order_pos.push_back(static_cast<int64_t>(h->order_slot.size()));
+        h->order_slot.push_back(s0 + i);
         h->ids_h.push_back(ids[i]);
         h->live_h.push_back(1);
         if (ids[i] <= h->max_id) h->ids_ascending = false;
@@ -501,6 +565,15 @@ void compact(sine_index* h) {
     CK(cudaStreamSynchronize(h->stream));
     std::vector<int64_t> nid(n);
     for (int64_t i = 0; i < n; ++i) nid[i] = h->ids_h[from[i]];
+    {  // slots renumbered in order: the reference order follows the rows
+        std::vector<int64_t> newslot(h->nslots, -1);
+        for (int64_t i = 0; i < n; ++i) newslot[from[i]] = i;
+        h->order_pos.assign(n, -1);
+        for (size_t p = 0; p < h->order_slot.size(); ++p) {
+            h->order_slot[p] = newslot[h->order_slot[p]];
+            h->order_pos[h->order_slot[p]] = static_cast<int64_t>(p);
+        }
+    }
     h->ids_h.swap(nid);
     h->live_h.assign(n, 1);
     h->nslots = n;
@@ -546,11 +619,7 @@ ScanCfg scan_cfg(const sine_index* h, bool bf16, int NQ) {
 
 template <typename RowT, int NQ, int CPW>
 void launch_scan_t(const ScanParams& p, int grid, int threads, size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(scan_kernel<RowT, NQ, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(scan_kernel<RowT, NQ, CPW>), 227 * 1024);
     scan_kernel<RowT, NQ, CPW><<<grid, threads, smem, st>>>(p);
 }
 
@@ -667,11 +736,7 @@ template <int NQ, int CS>
 int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters, size_t smem,
                cudaStream_t st) {
     auto kern = umma_res_kernel<NQ, CS>;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(kern), 227 * 1024);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -833,11 +898,7 @@ void umma_pair_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int
     if (L0.total + 2 * kUmmaN * kUmmaKB > 227 * 1024) fail(SINE_EINVAL, "pair plan does not fit shared memory");
     const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
     const ResSmem L = res_smem_layout(S, NQ, kblocks, kp, NQH);
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(umma_pair_kernel<NQH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(umma_pair_kernel<NQH>), 227 * 1024);
     const int npairs = std::max(1, std::min(h->num_sms / 2, ntiles));
     h->qbf.ensure(static_cast<size_t>(NQ) * row_elems * 2);
     h->lkey.ensure(static_cast<size_t>(2 * npairs) * NQ * kp);
@@ -926,11 +987,7 @@ int umma_gemm_query_t(sine_index* h, int64_t B, const double* q_dev, int k, int 
     const int64_t Bpad = static_cast<int64_t>(nqt) * NQ;
     const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - gemm_smem_bytes(0, NQ)) / gemm_stage_bytes(NQ)));
     const size_t smem = gemm_smem_bytes(S, NQ);
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(umma_gemm_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(umma_gemm_kernel<NQ>), 227 * 1024);
     const int nitems = nrt * nqt;
     const int npairs = std::max(1, std::min(h->num_sms / 2, nitems));
     h->qbf.ensure(static_cast<size_t>(Bpad) * row_elems * 2);
@@ -1085,11 +1142,7 @@ void umma_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp, do
     const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / stage_bytes));
     if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
     const UmmaSmem L = umma_smem_layout(S, kp);
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(umma_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(umma_scan_kernel), 227 * 1024);
     h->qbf.ensure(static_cast<size_t>(kUmmaM) * row_elems * 2);  // bytes/2 units: fp32 needs 2x
     h->lkey.ensure(static_cast<size_t>(grid) * kUmmaM * kp);
     h->lslot.ensure(static_cast<size_t>(grid) * kUmmaM * kp);
@@ -1174,11 +1227,15 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
     h->cur_err = bf16 ? 4.0e-3 : 2.0e-6;
     h->cert.ensure(std::max<int64_t>(B, 1));
 
-    if (umma_eligible(h, B, bf16, mode, kp)) {
+    if (h->snap_nslots < 0 && umma_eligible(h, B, bf16, mode, kp)) {
         umma_query(h, B, q_dev, k, kp, min_sim, bf16, rerank, ids_dev, sims_dev, counts_dev, st, mode);
         return;
     }
 
+    // a snapshot re-run (sine_query_wait) scans the submit-time store: the
+    // slots that existed then, with the validity bitmap of that moment
+    const int64_t scan_slots = h->snap_nslots >= 0 ? h->snap_nslots : h->nslots;
+    const uint32_t* scan_valid = h->snap_valid ? h->snap_valid : h->valid;
     const int NQmax = scan_cfg(h, bf16, 0).NQmax;
     h->lkey.ensure(static_cast<size_t>(h->num_sms) * NQmax * kp);
     h->lslot.ensure(static_cast<size_t>(h->num_sms) * NQmax * kp);
@@ -1190,13 +1247,13 @@ void query_device_impl(sine_index* h, int64_t B, const double* q_dev, int k, dou
         while (NQ < nq) NQ <<= 1;
         const ScanCfg c = scan_cfg(h, bf16, NQ);
         const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(h->num_sms, (h->nslots + c.R - 1) / c.R)));
-        const int64_t rows_per_cta = round_up((h->nslots + grid - 1) / grid, c.R);
+            1, std::min<int64_t>(h->num_sms, (scan_slots + c.R - 1) / c.R)));
+        const int64_t rows_per_cta = round_up((scan_slots + grid - 1) / grid, c.R);
         ScanParams p{};
         p.rows = bf16 ? reinterpret_cast<const uint8_t*>(h->rows16) : reinterpret_cast<const uint8_t*>(h->rows32);
         p.row_bytes = c.row_bytes;
-        p.nslots = h->nslots;
-        p.valid = h->valid;
+        p.nslots = scan_slots;
+        p.valid = scan_valid;
         p.ids = h->ids;
         p.q64 = q_dev + q0 * h->dim;
         p.dim = h->dim;
@@ -1273,11 +1330,7 @@ void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, in
     m.out_ids = ids_dev;
     m.out_sims = sims_dev;
     m.out_counts = counts_dev;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(merge_kernel), 160 * 1024);
     const size_t pool_bytes = static_cast<size_t>(ncta) * kp * sizeof(uint32_t);
     if (pool_bytes > 160 * 1024) fail(SINE_EINVAL, "candidate pool exceeds the merge kernel's shared memory");
     const size_t tm = tbegin(h, 1, st);
@@ -1549,10 +1602,59 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     if (h->timing) CK(cudaEventElapsedTime(&h->t_evict, h->ev[3], h->ev[4]));
 }
 
+bool certify_in_flight(const sine_index* h) {
+    for (const auto& t : h->tickets)
+        if (t.busy && t.certify) return true;
+    return false;
+}
+
+// Called before a tombstone is written: certified tickets in flight that
+// have no snapshot yet get a copy of the current bitmap (their submission
+// state: nothing was removed since), enqueued ahead of the tombstone.
+void snapshot_bitmap_for_tickets(sine_index* h) {
+    std::shared_ptr<DevBitmap> snap;
+    for (auto& t : h->tickets) {
+        if (!t.busy || !t.certify || t.valid_snap) continue;
+        if (!snap) {
+            snap = std::make_shared<DevBitmap>();
+            const int64_t words = (h->nslots + 31) / 32;
+            CK(cudaMalloc(&snap->p, std::max<int64_t>(words, 1) * sizeof(uint32_t)));
+            CK(cudaMemcpyAsync(snap->p, h->valid, words * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream));
+        }
+        t.valid_snap = snap;
+    }
+}
+
+void maybe_compact(sine_index* h) {
+    const int64_t dead = h->nslots - h->nlive;
+    if (dead <= std::max<int64_t>(64, h->nlive / 4)) return;
+    if (certify_in_flight(h)) {  // slots must not move under a pending re-run
+        h->compact_pending = true;
+        return;
+    }
+    h->compact_pending = false;
+    compact(h);
+}
+
+// ExactCosineIndex.remove's bookkeeping (index.py:80-92): the last id moves
+// into the removed id's position.
+void order_remove(sine_index* h, int64_t slot) {
+    const int64_t p = h->order_pos[slot];
+    const int64_t last = h->order_slot.back();
+    if (p != static_cast<int64_t>(h->order_slot.size()) - 1) {
+        h->order_slot[p] = last;
+        h->order_pos[last] = p;
+    }
+    h->order_slot.pop_back();
+    h->order_pos[slot] = -1;
+}
+
+// slots removed in the given order (the caller's removal sequence)
 void remove_slots(sine_index* h, const std::vector<int64_t>& slots) {
     if (slots.empty()) return;
     DevBuf<int64_t> d;
     d.ensure(slots.size());
+    snapshot_bitmap_for_tickets(h);
     CK(cudaMemcpyAsync(d.p, slots.data(), slots.size() * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
     set_bits_kernel<<<grid_for(slots.size(), 256, h->num_sms), 256, 0, h->stream>>>(h->valid, d.p, slots.size(), 0);
     ++h->launches;
@@ -1562,10 +1664,33 @@ void remove_slots(sine_index* h, const std::vector<int64_t>& slots) {
     for (int64_t s : slots) {
         if (!h->ids_ascending) h->pos.erase(h->ids_h[s]);
         h->live_h[s] = 0;
+        order_remove(h, s);
     }
     h->nlive -= static_cast<int64_t>(slots.size());
-    const int64_t dead = h->nslots - h->nlive;
-    if (dead > std::max<int64_t>(64, h->nlive / 4)) compact(h);
+    maybe_compact(h);
+}
+
+// fp64 master rows of `n` slots -> host [n][dim]: one gather on the device
+// and one copy back per 256 MB chunk (snapshots of 1M rows)
+void gather_rows_host(sine_index* h, int64_t n, const int64_t* slots, double* out) {
+    if (n <= 0) return;
+    const int64_t chunk = std::max<int64_t>(1, (256ll << 20) / (h->dim * 8));
+    DevBuf<int64_t> dslots;
+    DevBuf<double> drows;
+    dslots.ensure(std::min(n, chunk));
+    drows.ensure(std::min(n, chunk) * h->dim);
+    for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+        const int64_t m = std::min(chunk, n - i0);
+        CK(cudaMemcpyAsync(dslots.p, slots + i0, m * 8, cudaMemcpyHostToDevice, h->stream));
+        gather_rows64_kernel<<<grid_for(m * h->dim, 256, h->num_sms), 256, 0, h->stream>>>(h->rows64, dslots.p, m,
+                                                                                          h->dim, drows.p);
+        ++h->launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out + i0 * h->dim, drows.p, m * h->dim * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    dslots.release();
+    drows.release();
 }
 
 }  // namespace
@@ -1596,6 +1721,8 @@ int sine_create(int device, int64_t dim, uint32_t flags, int64_t reserve_rows, s
         CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         for (auto& e : h->ev) CK(cudaEventCreate(&e));
+        CK(cudaEventCreateWithFlags(&h->ws_ev, cudaEventDisableTiming));
+        h->ws_stream = h->stream;
         if (reserve_rows > 0) grow(h, reserve_rows);
         *out = h;
     });
@@ -1605,6 +1732,7 @@ int sine_destroy(sine_index_t* h) {
     return guarded([&] {
         if (!h) return;
         cudaSetDevice(h->device);
+        if (h->ws_stream != h->stream) cudaEventSynchronize(h->ws_ev);  // caller-stream queries drain first
         cudaStreamSynchronize(h->stream);
         for (void* p : {(void*)h->rows32, (void*)h->rows16, (void*)h->rows64, (void*)h->ids, (void*)h->valid,
                         (void*)h->lf, (void*)h->lc, (void*)h->ll, (void*)h->ls, (void*)h->created,
@@ -1623,6 +1751,7 @@ int sine_destroy(sine_index_t* h) {
             t.cert.release(), t.sids.release(), t.ssims.release(), t.scnt.release();
         }
         for (auto& e : h->ev) cudaEventDestroy(e);
+        cudaEventDestroy(h->ws_ev);
         cudaStreamDestroy(h->stream);
         delete h;
     });
@@ -1632,6 +1761,7 @@ int sine_reserve(sine_index_t* h, int64_t rows) {
     return guarded([&] {
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         grow(h, rows);
     });
 }
@@ -1643,6 +1773,7 @@ int sine_insert(sine_index_t* h, int64_t n, const int64_t* ids, const double* ro
         if (!ids || !rows) fail(SINE_EINVAL, "null ids/rows");
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         if (!(flags & SINE_NO_NORM_CHECK)) check_rows_host(h, n, rows);
         check_new_ids(h, n, ids);
         append(h, n, ids, rows, false, meta);
@@ -1656,6 +1787,7 @@ int sine_insert_device(sine_index_t* h, int64_t n, const int64_t* ids, const dou
         if (n <= 0) return;
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         check_new_ids(h, n, ids);
         // the rows may come from any stream (e.g. a torch kernel that just
         // wrote them): order the copy after all prior device work
@@ -1668,6 +1800,7 @@ int sine_remove(sine_index_t* h, int64_t n, const int64_t* ids) {
     return guarded([&] {
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         std::vector<int64_t> slots;
         slots.reserve(n);
         bool asc = true;
@@ -1694,13 +1827,9 @@ int sine_size(sine_index_t* h, int64_t* live, int64_t* slots) {
 int sine_ids(sine_index_t* h, int64_t* out, int64_t cap, int64_t* n) {
     return guarded([&] {
         std::lock_guard<std::mutex> g(h->mu);
-        int64_t j = 0;
-        for (int64_t s = 0; s < h->nslots; ++s) {
-            if (!h->live_h[s]) continue;
-            if (j < cap) out[j] = h->ids_h[s];
-            ++j;
-        }
-        *n = j;
+        const int64_t m = static_cast<int64_t>(h->order_slot.size());
+        for (int64_t j = 0; j < std::min(m, cap); ++j) out[j] = h->ids_h[h->order_slot[j]];
+        *n = m;
     });
 }
 
@@ -1709,29 +1838,27 @@ int sine_get_rows(sine_index_t* h, int64_t n, const int64_t* ids, double* out) {
         if (n <= 0) return;
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         std::vector<int64_t> slots(n);
         for (int64_t i = 0; i < n; ++i) {
             slots[i] = find_slot(h, ids[i]);
             if (slots[i] < 0) fail(SINE_ENOTFOUND, "unknown id " + std::to_string(ids[i]));
         }
-        // one gather on the device, one copy back (snapshots of 1M rows)
-        const int64_t chunk = std::max<int64_t>(1, (256ll << 20) / (h->dim * 8));
-        DevBuf<int64_t> dslots;
-        DevBuf<double> drows;
-        dslots.ensure(std::min(n, chunk));
-        drows.ensure(std::min(n, chunk) * h->dim);
-        for (int64_t i0 = 0; i0 < n; i0 += chunk) {
-            const int64_t m = std::min(chunk, n - i0);
-            CK(cudaMemcpyAsync(dslots.p, slots.data() + i0, m * 8, cudaMemcpyHostToDevice, h->stream));
-            gather_rows64_kernel<<<grid_for(m * h->dim, 256, h->num_sms), 256, 0, h->stream>>>(h->rows64, dslots.p, m,
-                                                                                              h->dim, drows.p);
-            ++h->launches;
-            CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(out + i0 * h->dim, drows.p, m * h->dim * 8, cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaStreamSynchronize(h->stream));
-        }
-        dslots.release();
-        drows.release();
+        gather_rows_host(h, n, slots.data(), out);
+    });
+}
+
+int sine_snapshot(sine_index_t* h, int64_t cap, int64_t* ids, double* rows, int64_t* n) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
+        const int64_t m = static_cast<int64_t>(h->order_slot.size());
+        *n = m;
+        if (m > cap) fail(SINE_EINVAL, "snapshot buffers hold " + std::to_string(cap) + " rows, need " +
+                                           std::to_string(m));
+        for (int64_t j = 0; j < m; ++j) ids[j] = h->ids_h[h->order_slot[j]];
+        gather_rows_host(h, m, h->order_slot.data(), rows);
     });
 }
 
@@ -1743,6 +1870,7 @@ int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_si
         if (!(mode & SINE_NO_NORM_CHECK)) check_queries_host(h, B, q);
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         h->q64.ensure(B * h->dim);
         h->o_ids.ensure(B * k);
         h->o_sims.ensure(B * k);
@@ -1824,6 +1952,7 @@ int sine_query_submit(sine_index_t* h, int64_t B, const double* q, int k, double
         if (!(mode & SINE_NO_NORM_CHECK)) check_queries_host(h, B, q);
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         size_t slot = 0;
         while (slot < h->tickets.size() && h->tickets[slot].busy) ++slot;
         if (slot == h->tickets.size()) {
@@ -1839,6 +1968,8 @@ int sine_query_submit(sine_index_t* h, int64_t B, const double* q, int k, double
         CK(cudaMemcpyAsync(h->q64.p, q, B * h->dim * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         t.certify = (mode & SINE_RERANK_F64) && (h->flags & SINE_STORE_F32) && h->nlive > 0;
         if (t.certify) t.cert.ensure(B);
+        t.nslots = h->nslots;
+        t.valid_snap.reset();
         t.zero_copy = h->nlive > 0;
         if (t.zero_copy) {
             // results land in this ticket's pinned staging (mapped into the
@@ -1887,6 +2018,7 @@ int sine_query_wait(sine_index_t* h, int64_t ticket) {
         CK(cudaEventSynchronize(ev));  // without the handle lock: other calls proceed
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         auto& t = h->tickets[ticket];
         t.busy = false;
         h->uncertified = 0;
@@ -1895,25 +2027,61 @@ int sine_query_wait(sine_index_t* h, int64_t ticket) {
             std::memcpy(t.sims, t.ssims.p, t.B * t.k * sizeof(double));
             std::memcpy(t.counts, t.scnt.p, t.B * sizeof(int32_t));
         }
+        struct Retire {  // the ticket's snapshot goes; a deferred compaction may run
+            sine_index* h;
+            sine_index::Ticket& t;
+            ~Retire() {
+                t.valid_snap.reset();
+                if (h->compact_pending) try {
+                        maybe_compact(h);
+                    } catch (...) {
+                    }
+            }
+        } retire{h, t};
         if (!t.certify) return;
-        // re-run uncertified queries on the fp32 scan from the caller's host
-        // copy (the device workspace may already hold a later batch)
+        // uncertified queries are re-run on the fp32 CUDA-core scan (2e-6
+        // error bound) against the SUBMIT-time store -- the slots that
+        // existed then and the bitmap of that moment -- in one batch, from
+        // the caller's host copy of the queries (the device workspace may
+        // already hold a later batch)
+        std::vector<int64_t> redo;
+        for (int64_t b = 0; b < t.B; ++b)
+            if (!t.cert.p[b]) redo.push_back(b);
+        if (redo.empty()) return;
+        const int64_t R = static_cast<int64_t>(redo.size());
+        std::vector<double> qh(R * h->dim);
+        for (int64_t r = 0; r < R; ++r)
+            std::memcpy(qh.data() + r * h->dim, t.q + redo[r] * h->dim, h->dim * sizeof(double));
         DevBuf<double> q1;
         DevBuf<int64_t> i1;
         DevBuf<double> s1;
         DevBuf<int32_t> c1;
-        for (int64_t b = 0; b < t.B; ++b) {
-            if (t.cert.p[b]) continue;
-            if (!q1.p) q1.ensure(h->dim), i1.ensure(t.k), s1.ensure(t.k), c1.ensure(1);
-            CK(cudaMemcpyAsync(q1.p, t.q + b * h->dim, h->dim * 8, cudaMemcpyHostToDevice, h->stream));
-            query_device_impl(h, 1, q1.p, t.k, t.min_sim, SINE_SCAN_F32 | SINE_RERANK_F64 | SINE_SCAN_CUDA_CORE, i1.p,
+        q1.ensure(R * h->dim), i1.ensure(R * t.k), s1.ensure(R * t.k), c1.ensure(R);
+        CK(cudaMemcpyAsync(q1.p, qh.data(), R * h->dim * 8, cudaMemcpyHostToDevice, h->stream));
+        {
+            struct Snap {
+                sine_index* h;
+                ~Snap() { h->snap_nslots = -1, h->snap_valid = nullptr; }
+            } snap{h};
+            h->snap_nslots = t.nslots;
+            h->snap_valid = t.valid_snap ? t.valid_snap->p : nullptr;
+            query_device_impl(h, R, q1.p, t.k, t.min_sim, SINE_SCAN_F32 | SINE_RERANK_F64 | SINE_SCAN_CUDA_CORE, i1.p,
                               s1.p, c1.p, h->stream);
-            CK(cudaMemcpyAsync(t.ids + b * t.k, i1.p, t.k * 8, cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(t.sims + b * t.k, s1.p, t.k * 8, cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(t.counts + b, c1.p, 4, cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaStreamSynchronize(h->stream));
-            ++h->uncertified;
         }
+        std::vector<int64_t> ih(R * t.k);
+        std::vector<double> sh(R * t.k);
+        std::vector<int32_t> ch(R);
+        CK(cudaMemcpyAsync(ih.data(), i1.p, R * t.k * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(sh.data(), s1.p, R * t.k * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(ch.data(), c1.p, R * 4, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        for (int64_t r = 0; r < R; ++r) {
+            const int64_t b = redo[r];
+            std::memcpy(t.ids + b * t.k, ih.data() + r * t.k, t.k * 8);
+            std::memcpy(t.sims + b * t.k, sh.data() + r * t.k, t.k * 8);
+            t.counts[b] = ch[r];
+        }
+        h->uncertified = R;
         q1.release(), i1.release(), s1.release(), c1.release();
     });
 }
@@ -1923,10 +2091,13 @@ int sine_query_device(sine_index_t* h, int64_t B, const double* q_dev, int k, do
     return guarded([&] {
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        ws_acquire(h, st);
         query_device_impl(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
         if (mode & SINE_CERTIFY)
             h->uncertified = certify_and_fix(h, B, q_dev, k, min_sim, mode, ids_dev, sims_dev, counts_dev, st);
+        ws_release(h, st);
     });
 }
 
@@ -1936,7 +2107,9 @@ int sine_query_device_cert(sine_index_t* h, int64_t B, const double* q_dev, int 
     return guarded([&] {
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        ws_acquire(h, st);
         struct Reset {
             sine_index* h;
             ~Reset() { h->cert_out = nullptr; }
@@ -1945,6 +2118,7 @@ int sine_query_device_cert(sine_index_t* h, int64_t B, const double* q_dev, int 
         if (h->nlive == 0 || !(mode & SINE_RERANK_F64))  // nothing to prove: every answer is exact
             CK(cudaMemsetAsync(cert_dev, 1, B, st));
         query_device_impl(h, B, q_dev, k, min_sim, mode & ~SINE_CERTIFY, ids_dev, sims_dev, counts_dev, st);
+        ws_release(h, st);
     });
 }
 
@@ -1955,6 +2129,7 @@ int sine_update_meta(sine_index_t* h, int64_t n, const int64_t* ids, const doubl
         std::lock_guard<std::mutex> g(h->mu);
         if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata");
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         std::vector<int64_t> slots(n);
         for (int64_t i = 0; i < n; ++i) {
             slots[i] = find_slot(h, ids[i]);
@@ -1988,6 +2163,7 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
         std::lock_guard<std::mutex> g(h->mu);
         if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata");
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         *n = 0;
         if (h->nlive == 0) return;
         const int nb = static_cast<int>((h->nslots + kExpChunk - 1) / kExpChunk);
@@ -2021,18 +2197,22 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
         if (!h->ids_ascending) std::sort(out, out + total);
         if (remove) {
             // tombstone on the device straight from the slot list
+            snapshot_bitmap_for_tickets(h);
             set_bits32_kernel<<<grid_for(total, 256, h->num_sms), 256, 0, h->stream>>>(h->valid, h->vslots.p, total);
             ++h->launches;
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(h->stream));
-            for (int64_t i = 0; i < total; ++i) {
-                const int32_t sl = slots[i];
+            std::vector<int32_t> by_id(slots, slots + total);  // the reference removes sorted(expired)
+            if (!h->ids_ascending)
+                std::sort(by_id.begin(), by_id.end(),
+                          [&](int32_t a, int32_t b) { return h->ids_h[a] < h->ids_h[b]; });
+            for (int32_t sl : by_id) {
                 if (!h->ids_ascending) h->pos.erase(h->ids_h[sl]);
                 h->live_h[sl] = 0;
+                order_remove(h, sl);
             }
             h->nlive -= total;
-            const int64_t dead = h->nslots - h->nlive;
-            if (dead > std::max<int64_t>(64, h->nlive / 4)) compact(h);
+            maybe_compact(h);
         }
     });
 }
@@ -2043,6 +2223,7 @@ int sine_select_victims(sine_index_t* h, int policy, double now, int64_t excess,
         if (policy < 0 || policy > 2) fail(SINE_EINVAL, "unknown eviction policy");
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
         select_victims_impl(h, policy, now, excess, out, cap, n);
     });
 }
@@ -2112,11 +2293,7 @@ int sine_merge_shards(int device, int P, int64_t B, int k, const int64_t* ids_de
         const size_t smem = static_cast<size_t>(P) * k * 16;
         if (smem > 160 * 1024) fail(SINE_EINVAL, "P * k too large for the shard merge");
         CK(cudaSetDevice(device));
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(shard_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-            attr = true;
-        }
+        smem_optin(reinterpret_cast<const void*>(shard_merge_kernel), 160 * 1024);
         shard_merge_kernel<<<static_cast<unsigned>(B), kShardMergeThreads, smem, static_cast<cudaStream_t>(stream)>>>(
             ids_dev, sims_dev, P, B, k, rank_stride ? rank_stride : B * k, out_ids, out_sims, out_counts);
         CK(cudaGetLastError());

@@ -141,6 +141,8 @@ class GpuCosineIndex:
         return live.value
 
     def ids(self) -> list[int]:
+        """Live ids in the reference's order: insertion order, with the last
+        id swapped into a removed id's position (index.py:80-92)."""
         n = len(self)
         out = np.empty(max(n, 1), dtype=np.int64)
         got = ctypes.c_int64()
@@ -334,7 +336,7 @@ class GpuCosineIndex:
 
     def snapshot_lines(self) -> list[str]:
         """Reference snapshot format (index.py:340-354): header + one line of
-        float-hex components per id, in slot order."""
+        float-hex components per id, in `ids()` order."""
         return self.snapshot_bytes().decode().split("\n")[:-1]
 
     def snapshot_bytes(self) -> bytes:
@@ -344,11 +346,28 @@ class GpuCosineIndex:
         head, body = self._snapshot_parts()
         return head + bytes(body)
 
+    def snapshot(self):
+        """(ids int64[n], rows float64[n, dimension]) in `ids()` order, taken
+        under one hold of the handle lock (sine_snapshot), so a concurrent
+        insert or removal cannot split the two."""
+        cap = len(self) + 64
+        while True:
+            ids = np.empty(max(cap, 1), dtype=np.int64)
+            rows = np.empty((max(cap, 1), self.dimension), dtype=np.float64)
+            n = ctypes.c_int64()
+            st = self._lib.sine_snapshot(self._h, cap, N.ptr(ids, ctypes.c_int64), N.ptr(rows, ctypes.c_double),
+                                         ctypes.byref(n))
+            if st == N.SINE_EINVAL and n.value > cap:
+                cap = n.value + 64  # grew in between: retry with room
+                continue
+            N.check(st)
+            return ids[:n.value], rows[:n.value]
+
     def _snapshot_parts(self):
-        ids = self.ids()
+        ids, rows = self.snapshot()
         head = "\n".join([self.SNAPSHOT_MAGIC, f"dimension: {self.dimension}", f"seed: {self.seed}",
                           f"count: {len(ids)}"]) + "\n"
-        body = N.hex_format(self.rows(ids), ids) if ids else memoryview(b"")
+        body = N.hex_format(rows, ids) if len(ids) else memoryview(b"")
         return head.encode(), body
 
     def save(self, path: str) -> None:

@@ -47,6 +47,26 @@ def merge_topk(sims: torch.Tensor, ids: torch.Tensor, k: int):
     return i2, s2, counts
 
 
+def place_least_full(counts: np.ndarray, n: int) -> np.ndarray:
+    """Owners of n new rows, each to the least-full rank at its turn (lowest
+    rank on ties) -- the sequential greedy rule, vectorised: the j-th row
+    takes the j-th smallest (level, rank) pair with level >= counts[rank]."""
+    P = counts.shape[0]
+    if n <= 0:
+        return np.empty(0, dtype=np.int64)
+    levels = np.unique(counts)
+    parts, have = [], 0
+    for a, b in zip(levels, list(levels[1:]) + [None]):
+        elig = np.nonzero(counts <= a)[0]  # ranks already at or below level a, in rank order
+        reps = (b - a) if b is not None else -(-(n - have) // P)
+        reps = min(reps, -(-(n - have) // len(elig)))
+        parts.append(np.tile(elig, reps))
+        have += reps * len(elig)
+        if have >= n:
+            break
+    return np.concatenate(parts)[:n].astype(np.int64)
+
+
 class ShardedCosineIndex:
     """SPMD wrapper: call every method on every rank with the same args."""
 
@@ -65,21 +85,18 @@ class ShardedCosineIndex:
         return len(self._owner)
 
     def _place(self, n: int) -> np.ndarray:
-        owners = np.empty(n, dtype=np.int64)
-        for j in range(n):
-            r = int(np.argmin(self._rows))
-            owners[j] = r
-            self._rows[r] += 1
+        owners = place_least_full(np.asarray(self._rows, dtype=np.int64), n)
+        self._rows = (np.asarray(self._rows) + np.bincount(owners, minlength=self.world)).tolist()
         return owners
 
     def insert_batch(self, ids, rows) -> None:
         ids = np.asarray(ids, dtype=np.int64)
-        for i in ids.tolist():
-            if i in self._owner:
-                raise ValidationError(f"duplicate id {i}")
+        id_list = ids.tolist()
+        if len(set(id_list)) != len(id_list) or not self._owner.keys().isdisjoint(id_list):
+            dup = next(i for i in id_list if i in self._owner or id_list.count(i) > 1)
+            raise ValidationError(f"duplicate id {dup}")
         owners = self._place(ids.shape[0])
-        for i, r in zip(ids.tolist(), owners.tolist()):
-            self._owner[i] = r
+        self._owner.update(zip(id_list, owners.tolist()))
         mine = owners == self.rank
         if mine.any():
             self.local.insert_batch(ids[mine], np.asarray(rows)[mine])
@@ -163,8 +180,14 @@ class PipelinedShardQueries:
     block is its own slot, and the collective plus the shard-merge kernel
     run on a second stream after an event.  A slot is rewritten only after
     its previous collective finished (event wait on the caller's stream).
-    Results of batch i are valid once `drain()` (or the slot's event) has
-    completed."""
+
+    Exactness: each rank logs its local certificates on the device; `finish()`
+    (SPMD, every rank) combines them with one MIN all-reduce and re-runs every
+    query whose certificate failed on ANY rank through the certified path
+    (`ShardedCosineIndex.query_device`), patching the held results -- no host
+    sync per batch.  Writers must not run between `submit` and `finish` (the
+    re-run reads the store as it is then).  The last `depth` batches' results
+    are held; call `finish()` before reading them."""
 
     def __init__(self, sharded: ShardedCosineIndex, B: int, k: int, depth: int = 4, device=None):
         self.sh = sharded
@@ -177,6 +200,7 @@ class PipelinedShardQueries:
         self.done = [None] * depth
         self.results = [None] * depth
         self.n = 0
+        self._log = []  # (batch number, queries, min_similarity, cert log) since the last finish()
 
     def submit(self, q: torch.Tensor, min_similarity: float, cert_out: torch.Tensor):
         """Enqueue one batch (CUDA float64 [B, d]); returns its slot."""
@@ -199,7 +223,32 @@ class PipelinedShardQueries:
             ev = torch.cuda.Event()
             ev.record(self.comm)
             self.done[slot] = ev
+        self._log.append((self.n - 1, q, min_similarity, cert_out))
         return slot
 
     def drain(self):
         torch.cuda.current_stream().wait_stream(self.comm)
+
+    def finish(self) -> int:
+        """Drain, then re-run (on every rank) the queries any rank could not
+        certify; returns how many were re-run.  Collective: call on all ranks."""
+        self.drain()
+        log, self._log = self._log, []
+        if not log:
+            return 0
+        flags = torch.cat([c.view(-1) for _, _, _, c in log]).to(torch.int32)
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=self.sh.group)
+        bad = (flags == 0).nonzero().flatten().tolist()  # same list on every rank
+        fixed = 0
+        for f in bad:
+            b, j = divmod(f, self.B)
+            n_b, q, ms, cert = log[b]
+            ids, sims, cnt = self.sh.query_device(q[j:j + 1], self.k, ms, certify=True)
+            cert[j] = 1
+            fixed += 1
+            if n_b >= self.n - self.depth:  # results still held: patch row j
+                ri, rs, rc = self.results[n_b % self.depth]
+                ri[j].copy_(ids[0])
+                rs[j].copy_(sims[0])
+                rc[j].copy_(cnt[0])
+        return fixed

@@ -110,7 +110,7 @@ def planted_queries(rows: np.ndarray, b: int, seed: int, dup_frac: float = 0.5):
     return q
 
 
-def config_a(n=10_000, d=384, b=200, seed=7):
+def config_a(n=10_000, d=384, b=1000, seed=7):
     rows = planted_rows(n, d, seed)
     q = planted_queries(rows, b, seed + 1)
     return rows, q

@@ -206,3 +206,25 @@ def test_embedder_tokenize_matches_reference_rules():
     from paper_2509_17360_b200.embedder import tokenize
     assert tokenize("Hello, World! héllo  WORLD...x") == ["hello", "world", "héllo", "world", "x"]
     assert tokenize("...!!!") == []
+
+
+def test_vectorised_placement_equals_the_sequential_greedy_rule():
+    """sharded.place_least_full == one-row-at-a-time argmin placement
+    (least-full rank, lowest rank on ties), for ragged starting counts."""
+    from paper_2509_17360_b200.sharded import place_least_full
+
+    def greedy(c, n):
+        c, out = list(c), []
+        for _ in range(n):
+            r = int(np.argmin(c))
+            out.append(r)
+            c[r] += 1
+        return out
+
+    rng = np.random.default_rng(0)
+    for _ in range(500):
+        P = int(rng.integers(1, 9))
+        c = rng.integers(0, 7, P)
+        n = int(rng.integers(0, 50))
+        assert place_least_full(c, n).tolist() == greedy(c, n)
+    assert place_least_full(np.zeros(8, dtype=np.int64), 10_000_000).shape == (10_000_000,)

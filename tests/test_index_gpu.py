@@ -75,7 +75,7 @@ def test_remove_steps(pkg, index_golden):
     for (i, q), gold in zip(steps, index_golden["remove_steps"]):
         idx.remove(i)
         _same(idx.query(q, k=10), gold["result"])
-        assert sorted(idx.ids()) == sorted(gold["ids"])
+        assert idx.ids() == gold["ids"]  # the reference order (swap-last), not just the set
     assert len(idx) == 35
 
 
@@ -182,7 +182,7 @@ def test_removal_compaction_and_reinsert(pkg):
     fresh /= np.linalg.norm(fresh, axis=1, keepdims=True)
     idx.insert_batch(np.arange(n, n + 300), fresh)
     ora.bulk_load(np.arange(n, n + 300), fresh)
-    assert sorted(idx.ids()) == sorted(ora.ids()) and len(idx) == len(ora)
+    assert idx.ids() == ora.ids() and len(idx) == len(ora)
     for j in range(20):
         q = rows[j] if j % 2 else fresh[j]
         got = idx.query(q, 12, -1.0)
@@ -206,7 +206,7 @@ def test_snapshot_round_trip(pkg, tmp_path):
     idx.save(p)
     loaded = pkg.GpuCosineIndex.load(p)
     assert loaded.dimension == 6 and loaded.seed == 4
-    assert sorted(loaded.ids()) == sorted(idx.ids())
+    assert loaded.ids() == idx.ids()
     assert loaded.rows([5]).tobytes() == vecs[5].tobytes()  # bit-exact rows
     q = vecs[0]
     assert [(c.id, c.similarity) for c in loaded.query(q, 5)] == [(c.id, c.similarity) for c in idx.query(q, 5)]
@@ -697,3 +697,81 @@ def test_mapped_result_staging_sync_and_async(pkg, scan):
         want = ora.query(q[j], k, -1.0)
         assert out[0][j, :out[2][j]].tolist() == [c.id for c in want]
     assert idx.uncertified() >= 1
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
+def test_uncertified_rerun_answers_the_submit_time_snapshot(pkg, scan):
+    """Snapshot-atomic answers (ref SPEC.md:183, index.py:98) when the
+    certificate fails: the re-run in sine_query_wait scans the store as it
+    was at SUBMISSION, although rows were removed (some from the answer,
+    enough to trigger a compaction) and better rows inserted in between."""
+    from paper_2509_17360_b200 import _native as N
+    rng = np.random.default_rng(5)
+    d, n, k = 256, 4000, 40
+    base = rng.standard_normal(d)
+    base /= np.linalg.norm(base)
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    for i in range(300):                       # the dense cluster that defeats the fast filter
+        g = rows[i] - (rows[i] @ base) * base
+        g /= np.linalg.norm(g)
+        c = 0.999 - i * 2e-5
+        rows[i] = c * base + np.sqrt(1 - c * c) * g
+    ids = rng.permutation(10 * n)[:n] + 1
+    idx = pkg.GpuCosineIndex(d, scan=scan, store_f32=True, store_bf16=True)
+    idx.insert_batch(ids, rows)
+    q = np.stack([base, rows[3000]])
+    want = idx.query_batch(q, k, -1.0)         # synchronous: one consistent snapshot
+    assert idx.uncertified() >= 1
+    qh, oi, os_, oc = (N.PinnedArray((2, d), np.float64), N.PinnedArray((2, k), np.int64),
+                       N.PinnedArray((2, k), np.float64), N.PinnedArray((2,), np.int32))
+    qh.array[:] = q
+    t = idx.submit_into(qh.array, k, -1.0, oi.array, os_.array, oc.array)
+    gone = list(want[0][0, :10]) + [int(i) for i in ids[3200:4000] if i not in set(want[0].ravel().tolist())]
+    idx.remove_batch(gone)                     # > live/4: a compaction is due (deferred)
+    idx.insert_batch(10 * n + 1 + np.arange(5), np.tile(base, (5, 1)))  # similarity 1: would lead
+    idx.wait_ticket(t)
+    assert idx.uncertified() >= 1
+    np.testing.assert_array_equal(oi.array, want[0])
+    np.testing.assert_array_equal(os_.array, want[1])
+    np.testing.assert_array_equal(oc.array, want[2])
+    # the deferred compaction ran; the current state answers like the oracle
+    ora = O.OracleExactIndex(d)
+    keep = np.array([i not in set(gone) for i in ids.tolist()])
+    ora.bulk_load(np.concatenate([ids[keep], 10 * n + 1 + np.arange(5)]),
+                  np.concatenate([rows[keep], np.tile(base, (5, 1))]))
+    got = idx.query_batch(q, k, -1.0)
+    for j in range(2):
+        assert got[0][j, :got[2][j]].tolist() == [c.id for c in ora.query(q[j], k, -1.0)]
+
+
+def test_ids_and_snapshot_follow_the_reference_swap_last_order(pkg, tmp_path):
+    """ids() and the snapshot file are byte-identical to the reference's
+    ExactCosineIndex after removals (swap-last, index.py:80-92), one at a
+    time and in batches, across compactions and later inserts."""
+    rng = np.random.default_rng(12)
+    d, n = 16, 600
+    rows = rng.standard_normal((n, d))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    ids = (rng.permutation(5 * n)[:n] + 3).tolist()
+    idx = pkg.GpuCosineIndex(d, seed=9)
+    ora = O.OracleExactIndex(d)
+    for i, r in zip(ids, rows):
+        ora.insert(i, r)
+    idx.insert_batch(ids, rows)
+    order = rng.permutation(n)
+    for step, j in enumerate(order[:400]):     # one at a time, then in batches
+        if step < 150:
+            idx.remove(ids[j])
+        ora.remove(ids[j])
+    idx.remove_batch([ids[j] for j in order[150:400]])
+    assert idx.ids() == ora.ids()
+    extra = rng.standard_normal((7, d))
+    extra /= np.linalg.norm(extra, axis=1, keepdims=True)
+    for m, r in enumerate(extra):
+        idx.insert(10_000 + m, r)
+        ora.insert(10_000 + m, r)
+    assert idx.ids() == ora.ids()
+    want = ["exact-cosine-index", f"dimension: {d}", "seed: 9", f"count: {len(ora)}"] + \
+        [f"{i} " + " ".join(float(c).hex() for c in ora.vectors[p]) for p, i in enumerate(ora.ids())]
+    assert idx.snapshot_lines() == want
