@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 N_ROWS, DIM, K = 1_000_000, 768, 10
 TAU = 0.9  # CacheConfig.tau_sim default, the value every engine call site passes
+QUERY_SEED = 11
 METRIC = "Sine lookups/sec (1M SEs, d=768, k=10)"
 
 
@@ -86,6 +87,14 @@ def make_queries(rows, b, seed):
         q[j] = c * x + math.sqrt(1 - c * c) * g
         q[j] /= np.linalg.norm(q[j])
     return q
+
+
+def dtype_label(scan, b):
+    """What stage-1 computes in: the B=1 fp32 filter is FFMA over fp32
+    rows; fp32 batches run kind::tf32 MMAs; bf16 runs kind::f16 MMAs."""
+    if scan == "bf16":
+        return "bf16+f64"
+    return "fp32+f64" if b == 1 else "tf32+f64"
 
 
 def algorithmic_bytes(n, d, b, k, scan):
@@ -145,43 +154,86 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- CPU arm
 
+def reference_exact_index():
+    """The reference's own ExactCosineIndex (oracle/_ref/semcache, staged by
+    oracle/make_ref.sh from the reference sources) when present -> kind
+    "reference"; else the oracle restatement -> kind "port"."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "semcache")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        from semcache.index import ExactCosineIndex
+        return ExactCosineIndex, "reference"
+    return None, "port"
+
+
 def cpu_lookups(rows, queries, k, tau):
-    """The reference CPU path (oracle restatement of ExactCosineIndex.query:
-    float64 GEMV over all rows + inclusive threshold + (-sim, id) lexsort)."""
-    from oracle import sine_oracle as O
-    idx = O.OracleExactIndex(rows.shape[1], capacity=1)
-    idx._buf = rows  # direct population (SURVEY §8c)
-    idx._ids = list(range(rows.shape[0]))
+    """The reference CPU path, one `ExactCosineIndex.query` per lookup
+    (it has no batch API): `_check_vector`, the float64 GEMV over all rows,
+    the inclusive threshold and the (-sim, id) lexsort.  The index is
+    populated by direct attribute assignment (its insert is
+    O(N*d) per row).  Returns (seconds, kind)."""
+    cls, kind = reference_exact_index()
+    if cls is not None:
+        idx = cls(rows.shape[1])
+        idx._ids = list(range(rows.shape[0]))
+        idx._pos = {i: i for i in range(rows.shape[0])}
+        idx._vecs = rows
+    else:
+        from oracle import sine_oracle as O
+        idx = O.OracleExactIndex(rows.shape[1], capacity=1)
+        idx._buf = rows
+        idx._ids = list(range(rows.shape[0]))
     t0 = time.perf_counter()
     for q in queries:
-        idx.query(q, k, tau)
-    return time.perf_counter() - t0
+        idx.query(q, k, min_similarity=tau)
+    return time.perf_counter() - t0, kind
+
+
+def workload_config(args, world, shard_rows):
+    """The config dict both arms print (same workload, same query seed)."""
+    return {"workload": f"config B: {args.rows} SEs x d={DIM}, k={K}, batch {args.batch}, "
+                        f"min_similarity={TAU} (tau_sim), {args.scan} scan + fp64 re-rank",
+            "rows": args.rows, "dim": DIM, "k": K, "batch": args.batch, "scan": args.scan,
+            "rows_per_gpu": shard_rows, "query_seed": QUERY_SEED,
+            "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "no flush: the index (>= 1.5 GB) exceeds the 126 MB L2"}
+
+
+def cpu_threads():
+    return int(os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS") or os.cpu_count())
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     rows = make_rows(args.rows, DIM)
     b = args.batch
-    per_step = max(1, min(b, 4))  # bounded sample: <= 4 lookups of the batch per step
-    qs = make_queries(rows, per_step * (args.steps + args.warmup), seed=7)
+    nsteps = args.warmup + args.steps
+    qs = make_queries(rows, b * nsteps, seed=QUERY_SEED).reshape(nsteps, b, DIM)  # the GPU arm's queries
+    per_step = max(1, min(b, 4))  # bounded sample: <= 4 lookups of each step's batch
     for s in range(args.warmup):
-        cpu_lookups(rows, qs[s * per_step:(s + 1) * per_step], K, TAU)
-    t = 0.0
-    for s in range(args.warmup, args.warmup + args.steps):
-        t += cpu_lookups(rows, qs[s * per_step:(s + 1) * per_step], K, TAU)
+        cpu_lookups(rows, qs[s, :per_step], K, TAU)
+    t, kind = 0.0, "port"
+    for s in range(args.warmup, nsteps):
+        dt, kind = cpu_lookups(rows, qs[s, :per_step], K, TAU)
+        t += dt
     n = per_step * args.steps
     value = n / t
-    cores = os.cpu_count()
+    cores = cpu_threads()
+    what = "semcache.index.ExactCosineIndex.query (the reference's own code)" if kind == "reference" else \
+        "oracle/ restatement of ExactCosineIndex.query"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: standard-normal rows normalised in float64, seed 1; half planted near-dups",
-            "config": {"workload": f"config B: {args.rows} SEs x d={DIM}, k={K}, min_similarity={TAU}",
-                       "batch": b, "sampled_lookups_per_step": per_step},
-            "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": cores, "kind": "port",
-                             "sample": f"{n} lookups (numpy float64 GEMV + lexsort, all host threads)"},
+            "data": "synthetic: standard-normal rows normalised in float64 (seed 1); queries half planted "
+                    "near-duplicates (cos 0.88-0.99), half random",
+            "config": dict(workload_config(args, world, args.rows // world), sampled_lookups_per_step=per_step),
+            "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": cores, "kind": kind,
+                             "sample": f"{n} lookups ({per_step} of each step's batch): {what}, numpy float64 "
+                                       f"GEMV + lexsort, {cores} BLAS threads"},
             "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -222,7 +274,7 @@ def run_ours(args):
 
     b = args.batch
     nsteps = args.warmup + args.steps
-    qs = make_queries(rows, b * nsteps, seed=11).reshape(nsteps, b, DIM)
+    qs = make_queries(rows, b * nsteps, seed=QUERY_SEED).reshape(nsteps, b, DIM)
     q_dev = torch.from_numpy(qs).to(f"cuda:{local}")
     ids_d = torch.empty((b, K), dtype=torch.int64, device=q_dev.device)
     sims_d = torch.empty((b, K), dtype=torch.float64, device=q_dev.device)
@@ -232,10 +284,15 @@ def run_ours(args):
     # launches onto it, and the CUDA events below time exactly that stream
     work = torch.cuda.Stream()
     torch.cuda.set_stream(work)
-    # exactness certificates are logged on the device per step and all
-    # checked after the timed loop (no per-step host sync); a failing one
-    # would be re-run and reported
+    # exactness certificates are logged on the device per step; at the end
+    # of each timed pass (inside its timed region) every uncertified query
+    # is re-run on the exact fp32 path, so the timed work includes the
+    # fallback.  Every step writes its own output slot, so sampled steps can
+    # be checked against the oracle afterwards.
     cert_log = torch.zeros((nsteps, b), dtype=torch.uint8, device=q_dev.device)
+    ids_log = torch.full((nsteps, b, K), -1, dtype=torch.int64, device=q_dev.device)
+    sims_log = torch.zeros((nsteps, b, K), dtype=torch.float64, device=q_dev.device)
+    cnt_log = torch.zeros((nsteps, b), dtype=torch.int32, device=q_dev.device)
     if world > 1:
         from paper_2509_17360_b200.sharded import ShardedCosineIndex
         sh = ShardedCosineIndex(idx)
@@ -246,12 +303,24 @@ def run_ours(args):
 
         def step(s):  # local scan -> one NCCL all-gather -> device shard merge; batch i's collective
             pipe.submit(q_dev[s], TAU, cert_log[s])  # overlaps batch i+1's scan
+
+        def fix_uncertified(s0, s1):  # every rank re-runs what any rank could not certify
+            return pipe.finish()
     else:
         stream = work.cuda_stream
 
-        def step(s):  # certificates land in the device log, checked after the timed loop
-            idx.query_device_cert(b, q_dev[s].data_ptr(), K, TAU, ids_d.data_ptr(), sims_d.data_ptr(),
-                                  cnt_d.data_ptr(), cert_log[s].data_ptr(), stream)
+        def step(s):  # certificates land in the device log
+            idx.query_device_cert(b, q_dev[s].data_ptr(), K, TAU, ids_log[s].data_ptr(), sims_log[s].data_ptr(),
+                                  cnt_log[s].data_ptr(), cert_log[s].data_ptr(), stream)
+
+        def fix_uncertified(s0, s1):
+            bad = (cert_log[s0:s1] == 0).nonzero().tolist()  # one device->host read per pass
+            for s_, j_ in bad:
+                s_ += s0
+                idx.query_device(1, q_dev[s_, j_].data_ptr(), K, TAU, ids_log[s_, j_].data_ptr(),
+                                 sims_log[s_, j_].data_ptr(), cnt_log[s_, j_:j_ + 1].data_ptr(), stream,
+                                 certify=True)
+            return len(bad)
 
     def barrier():
         torch.cuda.synchronize()
@@ -263,12 +332,16 @@ def run_ours(args):
         step(s)
     barrier()
 
+    fixed_in_timed = []
+
     def timed_pass():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
+        cert_log[args.warmup:].zero_()
         ev0.record()
         for s in range(args.warmup, nsteps):
             step(s)
+        fixed_in_timed.append(fix_uncertified(args.warmup, nsteps))
         ev1.record()
         barrier()
         return ev0.elapsed_time(ev1)
@@ -301,11 +374,30 @@ def run_ours(args):
         idx.timing_totals(1, reset=True)
         idx.timing_totals(2, reset=True)
         kpass_ms = timed_pass()
-    bad = (cert_log[args.warmup:] == 0).nonzero()
-    uncertified = int(bad.shape[0])
-    if world == 1:
-        for s_, j_ in bad.tolist():  # outside the timed region: the exact fp32 re-run
-            idx.query_batch(qs[args.warmup + s_][j_:j_ + 1], K, TAU, cuda_core=True)
+    uncertified = int(fixed_in_timed[0])  # re-run inside the headline pass's timed region
+    # parity of the timed steps: 16 sampled steps (up to 4 queries each)
+    # against the oracle (numpy float64 restatement of ExactCosineIndex.query)
+    parity = None
+    steps_ = np.unique(np.linspace(args.warmup, nsteps - 1, 16).astype(int))
+    if world > 1:  # the same steps through the sharded path (collective: every rank)
+        held = [(s_, sh.query_device(q_dev[s_], K, TAU)) for s_ in steps_]
+    else:  # the timed steps' own outputs
+        held = [(s_, (ids_log[s_], sims_log[s_], cnt_log[s_])) for s_ in steps_]
+    if rank == 0:
+        from oracle import sine_oracle as O
+        ora = O.OracleExactIndex(DIM, capacity=1)
+        ora._buf = rows
+        ora._ids = list(range(args.rows))
+        checked = ok = 0
+        for s_, (ri, rs, rc) in held:
+            ri, rs, rc = ri.cpu().numpy(), rs.cpu().numpy(), rc.cpu().numpy()
+            for j_ in range(min(b, 4)):
+                want = ora.query_unchecked(qs[s_][j_], K, TAU)
+                checked += 1
+                ok += int(ri[j_, :rc[j_]].tolist() == [c.id for c in want] and
+                          np.allclose(rs[j_, :rc[j_]], [c.similarity for c in want], rtol=0, atol=1e-12))
+        parity = {"parity_sampled": ok == checked, "queries_checked": checked, "queries_equal": ok,
+                  "steps_checked": len(held), "against": "oracle/ (numpy float64 ExactCosineIndex.query)"}
     scan_ms, scan_n = idx.timing_totals(0, reset=False)
     kernel_name = "scan_kernel"
     gemm = b > (128 if args.scan == "bf16" else 64) and TAU >= 0.25  # the library's tiled-GEMM gate
@@ -439,28 +531,27 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = make_queries(rows, 48, seed=5)
-        t = cpu_lookups(rows, sample, K, TAU)
-        cpu = {"value": len(sample) / t, "unit": "lookups/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{len(sample)} lookups of config B via oracle/ (numpy float64 GEMV + lexsort, "
-                         "all host threads)"}
+        sample = qs[args.warmup:args.warmup + 48, 0]
+        t, kind = cpu_lookups(rows, sample, K, TAU)
+        cpu = {"value": len(sample) / t, "unit": "lookups/s", "cores": cpu_threads(), "kind": kind,
+               "sample": f"{len(sample)} of the timed lookups through "
+                         + ("semcache.index.ExactCosineIndex.query (oracle/_ref)" if kind == "reference"
+                            else "oracle/ (restatement)") + ": numpy float64 GEMV + lexsort, all BLAS threads"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "tf32+f64" if args.scan == "fp32" else "bf16+f64",
-                "dtype_note": "tensor-core filter over fp32 (read as tf32) or bf16 rows with fp32 accumulation; "
-                              "the final k' candidates re-scored in fp64 (exactness certificate, fp32 fallback)",
+                "scaling": "strong", "vs_baseline": None, "dtype": dtype_label(args.scan, b),
+                "dtype_note": "B=1 fp32: fp32 rows x fp32 query with FFMA (CUDA cores) from TMA-staged tiles; "
+                              "fp32 batches: tensor-core kind::tf32 filter; bf16: kind::f16 filter; fp32 "
+                              "accumulation; the final k' candidates re-scored in fp64 (exactness certificate, "
+                              "exact fp32 re-run inside the timed region when it fails)",
                 "data": "synthetic: standard-normal rows normalised in float64 (seed 1); queries half planted "
                         "near-duplicates (cos 0.88-0.99), half random",
-                "config": {"workload": f"config B: {args.rows} SEs x d={DIM}, k={K}, batch {b}, "
-                                       f"min_similarity={TAU} (tau_sim), {args.scan} scan + fp64 re-rank",
-                           "rows": args.rows, "dim": DIM, "k": K, "batch": b, "scan": args.scan,
-                           "rows_per_gpu": shard_rows,
-                           "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
-                           "l2": "no flush: the index (>= 1.5 GB) exceeds the 126 MB L2"},
+                "config": workload_config(args, world, shard_rows),
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": int(launches), "uncertified_steps": uncertified,
+                "gpu_launches": int(launches), "uncertified_rerun_in_timed_region": uncertified,
+                "parity": parity, "parity_sampled": None if parity is None else parity["parity_sampled"],
                 "regimes": regimes, "eviction": eviction, "trace": trace, "config_c": config_c,
                 "persistence": persistence, "embedder": embedder}
         print(json.dumps(line), flush=True)
@@ -491,14 +582,24 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                 ids = torch.empty((b, K), dtype=torch.int64, device="cuda")
                 sims = torch.empty((b, K), dtype=torch.float64, device="cuda")
                 cnt = torch.empty((b,), dtype=torch.int32, device="cuda")
-                # timed without the per-call certificate sync (as the headline
-                # step); the certificates are checked once, untimed, below
-                run = lambda cert=False: idx.query_device(  # noqa: E731
-                    b, q.data_ptr(), K, tau, ids.data_ptr(), sims.data_ptr(), cnt.data_ptr(), stream, scan=scan,
-                    cuda_core=path == "cuda_core", umma_v1=path == "umma_v1", pair=path == "pair",
-                    gemm=False if path == "pair" else None, certify=cert)
-                run(True)
-                uncert = idx.uncertified()
+                cert = torch.zeros((b,), dtype=torch.uint8, device="cuda")
+                # every batch logs its certificates on the device; after each
+                # group (inside its timed window) the uncertified queries are
+                # re-run on the exact fp32 path -- the fallback is timed work
+                run = lambda: idx.query_device_cert(  # noqa: E731
+                    b, q.data_ptr(), K, tau, ids.data_ptr(), sims.data_ptr(), cnt.data_ptr(), cert.data_ptr(), stream,
+                    scan=scan, cuda_core=path == "cuda_core", umma_v1=path == "umma_v1", pair=path == "pair",
+                    gemm=False if path == "pair" else None)
+
+                def fix():
+                    bad = (cert == 0).nonzero().flatten().tolist()
+                    for j in bad:
+                        idx.query_device(1, q[j].data_ptr(), K, tau, ids[j].data_ptr(), sims[j].data_ptr(),
+                                         cnt[j:j + 1].data_ptr(), stream, certify=True)
+                    return len(bad)
+
+                run()
+                uncert = fix()
                 torch.cuda.synchronize()
                 # three groups of `reps` batches back to back on the stream,
                 # two events per group (an event between batches would break
@@ -510,6 +611,8 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                     e0.record()
                     for r_ in range(reps):
                         run()
+                        if uncert:  # this batch has queries the filter cannot certify: re-run them each rep
+                            fix()
                     e1.record()
                     torch.cuda.synchronize()
                     grp.append(e0.elapsed_time(e1) / reps)
@@ -886,6 +989,63 @@ def run_trace(engine, ops, embedder, model, now0, batched):
     return done
 
 
+def trace_parity(rows, n=100_000, n_ops=200, scan="fp32", batched=False):
+    """Config E's generator on the first n rows: the first n_ops outcomes of
+    the GPU engine (hit ids, admitted ids + victims, evict_until_fits lists)
+    against the oracle engine loop (restatement of ref engine.py:160-360)."""
+    import paper_2509_17360_b200 as P
+    from paper_2509_17360_b200 import model as M
+    from oracle import sine_oracle as O
+
+    rows = rows[:n]
+    d = rows.shape[1]
+    rng = np.random.default_rng(31)
+    meta = evict_metadata(n, seed=6)
+    meta["created"] = np.zeros(n)
+    meta["expiration"] = np.where(np.arange(n) % 97 == 0, 1.5, 1.0e5)  # a few expire mid-trace
+    shared = M.EmbeddingVector((1.0,))
+    ops = trace_ops(n, d, n_ops, rng, rows)
+    emb = _DictEmbedder(d)
+    usage = int(meta["size"].sum())
+    eng = P.CacheEngine(P.CacheConfig(capacity_tokens=usage), emb, _TextJudge(), scan=scan)
+    eng.bulk_admit(_make_elements(M, n, meta, shared), rows, now=0.0)
+    oe = O.OracleEngine(d, usage, lambda t: emb.table[t], _TextJudge().score, capacity_rows=n + n_ops)
+    oe.bulk_load(_make_elements(M, n, meta, shared), rows)
+    now, same, kinds = 1.0, 0, {"lookup": 0, "admit": 0, "evict": 0}
+    i = 0
+    while i < len(ops):
+        op = ops[i]
+        now += 0.01
+        if op[0] == "lookup":
+            j = i
+            while j < len(ops) and ops[j][0] == "lookup" and (batched or j == i):
+                emb.table[ops[j][1]] = M.EmbeddingVector(tuple(ops[j][2]))
+                j += 1
+            keys = [M.SemanticKey(ops[m][1], "search") for m in range(i, j)]
+            got = [o.element_id for o in (eng.lookup_batch(keys, now) if batched else [eng.lookup(keys[0], now)])]
+            want = [oe.lookup(k_, now) for k_ in keys]
+            same += sum(int(g == w) for g, w in zip(got, want))
+            kinds["lookup"] += j - i
+            i = j
+            continue
+        if op[0] == "admit":
+            el = M.SemanticElement(M.SemanticKey(op[1], "search"), " ".join(["t"] * op[3]),
+                                   M.EmbeddingVector(tuple(op[2])), 5, 0, 400.0, 0.005, op[3], now, now + 2.0e4)
+            got = eng.admit(el, now)
+            eid, ev = oe.admit(el, now)
+            same += int(got.element_id == eid and list(got.evicted_ids) == ev)
+        else:
+            eng.config.capacity_tokens -= op[1]
+            oe.capacity -= op[1]
+            same += int(eng.evict_until_fits(now) == oe.evict_until_fits(now))
+        kinds[op[0]] += 1
+        i += 1
+    st = eng.stats()
+    return {"ops_compared": len(ops), "ops_equal": same, "equal": same == len(ops), "by_kind": kinds,
+            "rows": n, "scan": scan, "batched_lookups": batched, "hits": st["hits"],
+            "against": "oracle/ OracleEngine (restatement of ref engine.py lookup/admit/evict_until_fits)"}
+
+
 def measure_trace(rows, n_ops=2000, cpu_ops=24):
     """Config E: end-to-end cache ops/s of the GPU engine on 1M SEs (d=768)
     vs the reference engine loop (oracle restatement) on the host."""
@@ -939,7 +1099,9 @@ def measure_trace(rows, n_ops=2000, cpu_ops=24):
         else:
             oe.capacity -= op[1]
             oe.evict_until_fits(now)
-    out["cpu_baseline"] = {"value": len(ops) / (time.perf_counter() - t0), "unit": "ops/s", "cores": os.cpu_count(),
+    cpu_s = time.perf_counter() - t0
+    out["parity"] = [trace_parity(rows), trace_parity(rows, scan="bf16", batched=True)]
+    out["cpu_baseline"] = {"value": len(ops) / cpu_s, "unit": "ops/s", "cores": os.cpu_count(),
                            "kind": "port", "sample": f"{len(ops)} trace ops on the oracle engine loop "
                                                      "(numpy float64 GEMV + Python LCFU sort), same 1M SEs"}
     return out

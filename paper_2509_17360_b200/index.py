@@ -262,11 +262,13 @@ class GpuCosineIndex:
 
     def query_device_cert(self, B: int, q_ptr: int, k: int, min_similarity: float, ids_ptr: int, sims_ptr: int,
                           counts_ptr: int, cert_ptr: int, stream: int | None = None, *, scan: str | None = None,
-                          rerank: bool | None = None) -> None:
+                          rerank: bool | None = None, cuda_core: bool = False, umma_v1: bool = False,
+                          pair: bool = False, gemm: bool | None = None) -> None:
         """query_device writing the exactness certificates (uint8 [B], device)
         to `cert_ptr` on the stream: no sync; the caller re-runs any 0."""
+        mode = self._mode(scan, rerank, cuda_core, umma_v1, pair=pair, gemm=gemm)
         N.check(self._lib.sine_query_device_cert(self._h, int(B), ctypes.c_void_p(q_ptr), int(k),
-                                                 float(min_similarity), self._mode(scan, rerank),
+                                                 float(min_similarity), mode,
                                                  ctypes.c_void_p(ids_ptr), ctypes.c_void_p(sims_ptr),
                                                  ctypes.c_void_p(counts_ptr), ctypes.c_void_p(cert_ptr),
                                                  _stream_arg(stream)))
