@@ -69,6 +69,7 @@ _SIGS = {
                                            _i64p, ctypes.c_int64, _i64p]),
     "sine_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "sine_set_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "sine_set_select_cap": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "sine_last_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
                                         ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "sine_kernel_launches": (ctypes.c_int, [ctypes.c_void_p, _i64p]),

@@ -29,7 +29,6 @@
 #include <unordered_set>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <cudaTypedefs.h>
 
 #include "../../include/sine_b200.h"
@@ -39,6 +38,7 @@
 #include "hexio.cuh"
 #include "merge.cuh"
 #include "scan.cuh"
+#include "select.cuh"
 #include "umma.cuh"
 
 using namespace sine;
@@ -84,6 +84,11 @@ template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    ~DevBuf() { release(); }
     void ensure(size_t want) {
         if (want <= n) return;
         if (p) cudaFree(p);
@@ -114,6 +119,11 @@ template <typename T>
 struct HostBuf {
     T* p = nullptr;
     size_t n = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    HostBuf(HostBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    ~HostBuf() { release(); }
     void ensure(size_t want) {
         if (want <= n) return;
         if (p) cudaFreeHost(p);
@@ -193,31 +203,27 @@ struct sine_index {
     int64_t uncertified = 0;      // queries re-run by the last certify pass
     float cur_thr0 = 0.f;         // admission floor of the running query
     double cur_err = 0.0;         // its filter error bound
-    DevBuf<uint64_t> k1;
-    DevBuf<uint64_t> vkeys;
-    DevBuf<int32_t> vslots, cand, scratch_i32;
-    DevBuf<int64_t> vids;
-    DevBuf<uint8_t> cub_tmp;
-    DevBuf<unsigned long long> hist;  // hw[256] hc[256] hand[3] hor[3] counter kand[3] kor[3]
-    DevBuf<Pack2> vpack, vpack_out;
-    DevBuf<Key3> vkey_out;
-    DevBuf<int32_t> vslots_out;
+    DevBuf<int32_t> vslots, scratch_i32;  // expiry: slot list, per-block counts
+    DevBuf<int64_t> vids;                 // expired ids / victim ids
     DevBuf<int64_t> exp_off;
     DevBuf<uint32_t> gbound;        // chip-wide admission bounds of the running launch
     DevBuf<uint32_t> gcnt;          // tiled GEMM: candidates per query + overflow counter
     DevBuf<uint32_t> tmax;          // sample pass: per (tile, query) max score keys
     int64_t gemm_overflows = 0;     // GEMM launches re-run on the list-keeping kernels
-    HostBuf<unsigned long long> sel_h;  // counter + kand + kor
-    DevBuf<SelectState> st, st1;       // selection state; st1 = after pass 1 (the record prefix)
-    DevBuf<uint64_t> rkeys;            // eviction candidate records: keys [n][3]
-    DevBuf<int64_t> rsize, dcount;     // record sizes; device counters
-    DevBuf<int32_t> rslot;             // record -> slot
-    DevBuf<uint64_t> rkeys2;           // the records after the first refinement pass
-    DevBuf<uint8_t> d0;                // eviction pass 1: top byte of every primary key
-    DevBuf<int64_t> rsize2;
-    DevBuf<int32_t> rslot2;
+    // victim selection (select.cuh): records below the sampled bound, the
+    // same in bucket order, bucket of each record, splitters, per-bucket
+    // count / size, offsets, cursors, oversized buckets, control block
+    DevBuf<SelRec> srec, srec2;
+    DevBuf<uint16_t> sbid;
+    DevBuf<uint32_t> sspl, stab;
+    DevBuf<unsigned long long> sbcnt;
+    DevBuf<int64_t> sboff;
+    DevBuf<uint32_t> sbcur;
+    DevBuf<int32_t> sbig;
+    DevBuf<SelCtl> sctl;
+    int sel_cap = kSelCap;  // records sorted in smem per CTA (sine_set_select_cap lowers it in tests)
+    HostBuf<SelCtl> sctl_h;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
-    HostBuf<SelectState> st_h;
     HostBuf<unsigned long long> n_h;
     HostBuf<int32_t> cnt_h;
     HostBuf<uint8_t> cert_h;
@@ -1409,17 +1415,9 @@ EvictCols evict_cols(const sine_index* h) {
     return c;
 }
 
-struct PackDecomposer {
-    __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&> operator()(Pack2& k) const { return {k.hi, k.lo}; }
-};
-
-struct KeyDecomposer {
-    __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&, uint64_t&> operator()(Key3& k) const {
-        return {k.a, k.b, k.c};
-    }
-};
-
 // Victims are written straight into the caller's buffer (pinned or pageable).
+// Sample select (select.cuh): one pass over the store, then only the
+// records below the sampled bound are bucketed and sorted.
 void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, int64_t* out, int64_t cap,
                          int64_t* nout) {
     *nout = 0;
@@ -1427,174 +1425,67 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     if (excess <= 0 || h->nlive == 0) return;
     cudaStream_t st = h->stream;
     record(h, 3, st);
-    h->k1.ensure(std::max<int64_t>(h->cap, 1));
-    h->hist.ensure(256 * 2 + 6 + 1 + 6);
-    h->st.ensure(1);
-    h->st_h.ensure(1);
-    h->sel_h.ensure(7);
-    unsigned long long* hw = h->hist.p;
-    unsigned long long* hc = hw + 256;
-    unsigned long long* hand = hc + 256;
-    unsigned long long* hor = hand + 3;
-    unsigned long long* counter = hor + 3;
-    unsigned long long* kand = counter + 1;
-    unsigned long long* kor = kand + 3;
-    CK(cudaMemsetAsync(hw, 0, 512 * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(hand, 0xff, 3 * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(hor, 0, 3 * sizeof(unsigned long long), st));
-    SelectState s0{};
-    s0.rem = excess;
-    s0.count = h->nlive;
-    *h->st_h.p = s0;
-    CK(cudaMemcpyAsync(h->st.p, h->st_h.p, sizeof(SelectState), cudaMemcpyHostToDevice, st));
-
+    const int64_t nl = std::max<int64_t>(h->nlive, 1);
+    h->srec.ensure(nl);
+    h->srec2.ensure(nl);
+    h->sbid.ensure(nl);
+    h->vids.ensure(nl);
+    h->sspl.ensure(kSelMaxBuckets);
+    h->stab.ensure(4100);
+    h->sbcnt.ensure(2 * kSelMaxBuckets);
+    h->sboff.ensure(kSelMaxBuckets);
+    h->sbcur.ensure(kSelMaxBuckets);
+    h->sbig.ensure(kSelMaxBuckets);
+    h->sctl.ensure(1);
+    h->sctl_h.ensure(1);
+    smem_optin(reinterpret_cast<const void*>(sel_collect_kernel), kSelCollectSmem);
+    smem_optin(reinterpret_cast<const void*>(sel_bucket_kernel), kSelBucketSmem);
+    smem_optin(reinterpret_cast<const void*>(sel_sort_kernel), kSelWinSmem);
+    smem_optin(reinterpret_cast<const void*>(sel_big_kernel), kSelSortSmem);
     const EvictCols cols = evict_cols(h);
-    const int grid_all = grid_for(h->nslots, 256, h->num_sms);
-    const int nb = static_cast<int>((h->nslots + kColChunk - 1) / kColChunk);
-    h->scratch_i32.ensure(nb);
-    h->exp_off.ensure(nb + 1);
-    h->st1.ensure(1);
-    h->dcount.ensure(4);
-    h->n_h.ensure(2);
-    // pass 1 over every live slot: primary keys (cached) + the first digit
-    HistArgs a{};
-    a.c = cols;
-    a.policy = policy;
-    a.now = now;
-    a.k1 = h->k1.p;
-    h->d0.ensure(std::max<int64_t>(h->cap, 1));
-    a.d0 = policy == 0 ? h->d0.p : nullptr;  // written by the LCFU pass-1 kernel only
-    a.first = 1;
-    a.st = h->st.p;
-    a.hw = hw, a.hc = hc, a.hand = hand, a.hor = hor;
-    if (policy == 0)
-        evict_pass1_lcfu_kernel<<<grid_all, 256, 0, st>>>(a);
-    else
-        evict_hist_kernel<<<grid_all, 256, 0, st>>>(a);
-    evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 1);
-    // the slots of the chosen prefix bucket -> dense records (slot order):
-    // later passes stream 32 B per candidate instead of gathering columns
-    CK(cudaMemcpyAsync(h->st1.p, h->st.p, sizeof(SelectState), cudaMemcpyDeviceToDevice, st));
-    h->rkeys.ensure(3 * std::max<int64_t>(h->nlive, 1));
-    h->rsize.ensure(std::max<int64_t>(h->nlive, 1));
-    h->rslot.ensure(std::max<int64_t>(h->nlive, 1));
-    int64_t* nrec = h->dcount.p;      // records
-    int64_t* nbelow = h->dcount.p + 1;  // victims below the record prefix
-    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->scratch_i32.p, nullptr, nullptr, a.d0);
-    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
-    collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 1, h->exp_off.p, h->rkeys.p, h->rslot.p, nullptr,
-                                             nullptr, h->rsize.p, nullptr, nullptr, nullptr, nullptr, a.d0);
-    CK(cudaMemcpyAsync(nrec, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    h->launches += 5;
-    CK(cudaGetLastError());
-    // refinement passes over the records, enqueued four at a time (a pass
-    // after `done` returns at once); one host check per group
-    HistArgs r = a;
-    r.first = 0;
-    r.rk = h->rkeys.p;
-    r.rsz = h->rsize.p;
-    r.rn = nrec;
-    const int grid_rec = grid_for(h->nlive, 256, h->num_sms);
-    const int nbr = static_cast<int>((h->nlive + kColChunk - 1) / kColChunk);
-    h->scratch_i32.ensure(std::max(nb, nbr));
-    h->exp_off.ensure(std::max(nb, nbr) + 1);
-    // first refinement pass over the records, then shrink them once more to
-    // the records matching the longer prefix (typically ~1/256 of them): the
-    // remaining passes stream only those
-    evict_hist_kernel<<<grid_rec, 256, 0, st>>>(r);
-    evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 0);
-    h->rkeys2.ensure(3 * std::max<int64_t>(h->nlive, 1));
-    h->rsize2.ensure(std::max<int64_t>(h->nlive, 1));
-    h->rslot2.ensure(std::max<int64_t>(h->nlive, 1));
-    int64_t* nrec2 = h->dcount.p + 2;
-    collect_count_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 1, h->scratch_i32.p, h->rkeys.p, nrec);
-    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nbr, h->exp_off.p);
-    collect_write_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 1, h->exp_off.p, h->rkeys2.p, h->rslot2.p,
-                                              nullptr, nullptr, h->rsize2.p, h->rkeys.p, nrec, h->rslot.p);
-    CK(cudaMemcpyAsync(nrec2, h->exp_off.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    h->launches += 5;
-    CK(cudaGetLastError());
-    r.rk = h->rkeys2.p;
-    r.rsz = h->rsize2.p;
-    r.rn = nrec2;
-    for (int pass = 2; pass < 25; pass += 4) {
-        for (int j = 0; j < 4; ++j) {
-            evict_hist_kernel<<<grid_rec, 256, 0, st>>>(r);
-            evict_pick_kernel<<<1, 256, 0, st>>>(h->st.p, hw, hc, hand, hor, 0);
+    const int slot_tie = h->ids_ascending ? 1 : 0;
+    unsigned long long* bcnt = h->sbcnt.p;
+    unsigned long long* bw = bcnt + kSelMaxBuckets;
+    const int scap = h->sel_cap;
+    // small stores skip the sample: every live slot is a record
+    bool all = h->nlive <= scap;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        SelCtl c0{};
+        c0.all = all ? 1 : 0;
+        for (int w = 0; w < 3; ++w) c0.rand[w] = ~0ull;
+        *h->sctl_h.p = c0;
+        CK(cudaMemcpyAsync(h->sctl.p, h->sctl_h.p, sizeof(SelCtl), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(bcnt, 0, 2 * kSelMaxBuckets * sizeof(unsigned long long), st));
+        if (!all) {
+            sel_sample_kernel<<<1, 1024, 0, st>>>(cols, policy, now, h->nlive, excess, slot_tie, h->sctl.p);
+            ++h->launches;
         }
-        h->launches += 8;
+        const int64_t tiles = (h->nslots / 2 + 1 + 32 * kSelCollectU - 1) / (32 * kSelCollectU);
+        const int gcol = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>((tiles + kSelCollectThreads / 32 - 1) / (kSelCollectThreads / 32), 4ll * h->num_sms)));
+        sel_collect_kernel<<<gcol, kSelCollectThreads, kSelCollectSmem, st>>>(cols, policy, now, slot_tie, h->sctl.p,
+                                                                              h->srec.p);
+        sel_split_kernel<<<1, 1024, 0, st>>>(excess, h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, scap);
+        // bucket and scatter must split the records the same way (same grid)
+        const int grec = 2 * h->num_sms;
+        sel_bucket_kernel<<<grec, 1024, kSelBucketSmem, st>>>(h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, h->sbid.p,
+                                                              bcnt, bw);
+        sel_scan_kernel<<<1, 1024, 0, st>>>(h->sctl.p, excess, bcnt, bw, h->sboff.p, h->sbcur.p);
+        sel_scatter_kernel<<<grec, 1024, 0, st>>>(h->sctl.p, h->srec.p, h->sbid.p, h->sboff.p, h->sbcur.p,
+                                                  h->srec2.p);
+        sel_sort_kernel<<<2 * h->num_sms, kSelSortThreads, kSelWinSmem, st>>>(
+            h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
+        sel_big_kernel<<<h->num_sms, kSelSortThreads, kSelSortSmem, st>>>(
+            h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->srec.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
+        h->launches += 7;
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(h->st_h.p, h->st.p, sizeof(SelectState), cudaMemcpyDeviceToHost, st));
+        record(h, 4, st);
+        CK(cudaMemcpyAsync(h->sctl_h.p, h->sctl.p, sizeof(SelCtl), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (h->st_h.p->done) break;
+        if (!h->sctl_h.p->retry) break;
+        all = true;  // the sampled bound fell short of the excess: take every slot
     }
-    // victims = live slots below the record prefix (slot order), then the
-    // records with key <= T (slot order): equal (primary, created_at) keys
-    // fall in the same part, so the stable sort below keeps id order
-    CK(cudaMemsetAsync(kand, 0xff, 3 * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(kor, 0, 3 * sizeof(unsigned long long), st));
-    h->vkeys.ensure(3 * std::max<int64_t>(h->nlive, 1));
-    h->vslots.ensure(std::max<int64_t>(h->nlive, 1));
-    collect_count_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->scratch_i32.p, nullptr, nullptr, a.d0);
-    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nb, h->exp_off.p);
-    collect_write_kernel<<<nb, 256, 0, st>>>(cols, h->k1.p, h->st1.p, 2, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
-                                             kor, nullptr, nullptr, nullptr, nullptr, nullptr, a.d0);
-    CK(cudaMemcpyAsync(nbelow, h->exp_off.p + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    collect_count_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->scratch_i32.p, h->rkeys.p, nrec);
-    expire_scan_kernel<<<1, 1024, 0, st>>>(h->scratch_i32.p, nbr, h->exp_off.p);
-    collect_write_kernel<<<nbr, 256, 0, st>>>(cols, h->k1.p, h->st.p, 0, h->exp_off.p, h->vkeys.p, h->vslots.p, kand,
-                                              kor, nullptr, h->rkeys.p, nrec, h->rslot.p, nbelow);
-    h->launches += 6;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h->sel_h.p + 1, kand, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h->n_h.p, nbelow, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h->n_h.p + 1, h->exp_off.p + nbr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const int64_t V = static_cast<int64_t>(h->n_h.p[0]) + static_cast<int64_t>(h->n_h.p[1]);
-    (void)counter;
-    // bytes of the composite key that vary over the victims; with slot order
-    // == id order the id bytes are left to the (stable) sort's input order
-    const bool skip_id = h->ids_ascending;
-    int nvary = 0;
-    for (int d = 0; d < (skip_id ? 16 : 24); ++d) {
-        const int w = d >> 3, sh = 8 * (7 - (d & 7));
-        if (((h->sel_h.p[1 + w] >> sh) & 0xff) != ((h->sel_h.p[4 + w] >> sh) & 0xff)) ++nvary;
-    }
-    h->vids.ensure(std::max<int64_t>(V, 1));
-    if (V <= 2048) {
-        evict_small_sort_kernel<<<1, 1024, 3 * V * sizeof(uint64_t), st>>>(h->vkeys.p, h->vslots.p, h->ids,
-                                                                          static_cast<int>(V), h->vids.p);
-        ++h->launches;
-        CK(cudaGetLastError());
-    } else {
-        h->vslots_out.ensure(V);
-        size_t tmp = 0;
-        if (nvary <= 16) {
-            // sort only the bytes that vary over the victim set
-            h->vpack.ensure(V);
-            h->vpack_out.ensure(V);
-            evict_pack_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(h->vkeys.p, V, kand, kor,
-                                                                            skip_id ? 1 : 0, h->vpack.p);
-            const int end_bit = std::max(8, 8 * nvary);
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, h->vpack.p, h->vpack_out.p, h->vslots.p,
-                                               h->vslots_out.p, V, PackDecomposer{}, 0, end_bit, st));
-            h->cub_tmp.ensure(tmp);
-            CK(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, h->vpack.p, h->vpack_out.p, h->vslots.p,
-                                               h->vslots_out.p, V, PackDecomposer{}, 0, end_bit, st));
-        } else {
-            Key3* keys_in = reinterpret_cast<Key3*>(h->vkeys.p);
-            h->vkey_out.ensure(V);
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, h->vkey_out.p, h->vslots.p, h->vslots_out.p,
-                                               V, KeyDecomposer{}, st));
-            h->cub_tmp.ensure(tmp);
-            CK(cub::DeviceRadixSort::SortPairs(h->cub_tmp.p, tmp, keys_in, h->vkey_out.p, h->vslots.p,
-                                               h->vslots_out.p, V, KeyDecomposer{}, st));
-        }
-        gather_ids_kernel<<<grid_for(V, 256, h->num_sms), 256, 0, st>>>(h->vslots_out.p, h->ids, V, h->vids.p);
-        h->launches += 3;
-        CK(cudaGetLastError());
-    }
-    record(h, 4, st);
+    const int64_t V = h->sctl_h.p->V;
     if (V > cap) fail(SINE_EINVAL, "output buffer too small for the victim list");
     CK(cudaMemcpyAsync(out, h->vids.p, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1738,18 +1629,9 @@ int sine_destroy(sine_index_t* h) {
                         (void*)h->lf, (void*)h->lc, (void*)h->ll, (void*)h->ls, (void*)h->created,
                         (void*)h->expiration, (void*)h->last_access, (void*)h->freq, (void*)h->size})
             if (p) cudaFree(p);
-        h->q64.release(), h->lkey.release(), h->lslot.release(), h->ln.release();
-        h->o_ids.release(), h->o_sims.release(), h->o_cnt.release(), h->k1.release();
-        h->vkeys.release(), h->vslots.release(), h->cand.release(), h->scratch_i32.release();
-        h->vids.release(), h->cub_tmp.release(), h->hist.release(), h->st.release(), h->qbf.release();
-        h->vpack.release(), h->vpack_out.release(), h->vkey_out.release(), h->vslots_out.release();
-        h->exp_off.release(), h->sel_h.release(), h->gbound.release();
-        h->st_h.release(), h->n_h.release(), h->cnt_h.release(), h->cert_h.release();
-        h->ids_zc.release(), h->sims_zc.release(), h->cnt_zc.release();
-        for (auto& t : h->tickets) {
+        // the DevBuf / HostBuf workspaces free themselves with the handle
+        for (auto& t : h->tickets)
             if (t.done) cudaEventDestroy(t.done);
-            t.cert.release(), t.sids.release(), t.ssims.release(), t.scnt.release();
-        }
         for (auto& e : h->ev) cudaEventDestroy(e);
         cudaEventDestroy(h->ws_ev);
         cudaStreamDestroy(h->stream);
@@ -2230,6 +2112,14 @@ int sine_select_victims(sine_index_t* h, int policy, double now, int64_t excess,
 
 int sine_stream(sine_index_t* h, void** stream) {
     return guarded([&] { *stream = h->stream; });
+}
+
+int sine_set_select_cap(sine_index_t* h, int cap) {
+    return guarded([&] {
+        if (cap < 2 || cap > kSelCap) fail(SINE_EINVAL, "select cap must be in [2, 4096]");
+        std::lock_guard<std::mutex> g(h->mu);
+        h->sel_cap = cap;
+    });
 }
 
 int sine_set_timing(sine_index_t* h, int on) {

@@ -1,0 +1,1081 @@
+// Size-weighted victim prefix by sample select + bucketed block radix sort
+// (replaces round 1's multi-pass radix select and device-wide library sort).
+//
+// Reference semantics (pkg/src/semcache/engine.py):
+//   _victim_order_locked :369-383  ascending (key, created_at, id) over all
+//                                  residents; key = cal_score (lcfu),
+//                                  last_access (lru) or frequency (lfu)
+//   admit / evict loops  :321-327, :353-359  pop in that order while the
+//                                  freed size is below the excess -> the
+//                                  victims are the shortest prefix whose
+//                                  size sum reaches the excess (all of
+//                                  them when the total does not)
+//
+// Pipeline (one stream, one host sync before the result copy):
+//   1 sel_sample_kernel   one CTA: 4096 strided live slots; a weighted
+//                         radix select over their full keys finds the sample
+//                         at the size quantile of the excess plus a 6-sigma
+//                         margin; its key `hi` bounds the victim prefix with
+//                         overwhelming probability
+//   2 sel_collect_kernel  THE pass over the store (HBM-bound): each live
+//                         slot's primary key from its columns; slots with
+//                         (key, created_at, tie) <= hi become 32-byte records
+//                         staged in shared memory and flushed with one
+//                         global reservation per CTA round
+//   3 sel_split_kernel    one CTA: the records' size must reach the excess
+//                         (checked exactly; otherwise the host re-runs from
+//                         2 taking every slot); 4096 sampled records' 32-bit
+//                         windows (the bits from the records' first varying
+//                         bit) radix-sorted give <= 1024 bucket splitters and
+//                         a lookup table over their top 12 bits
+//   4 sel_bucket_kernel   bucket of each record (table lookup + a short
+//                         search in smem) + per-bucket count / size
+//   5 sel_scan_kernel     bucket offsets; the bucket where the size prefix
+//                         reaches the excess (later buckets are skipped)
+//   6 sel_scatter_kernel  records -> bucket order (one global reservation
+//                         per (CTA, bucket))
+//   7 sel_sort_kernel     one CTA per bucket (persistent): the 32 bits from
+//                         the bucket's first varying bit are block-radix-
+//                         sorted (cub::BlockRadixSort as a building block
+//                         inside this kernel); ids land at their final
+//                         positions, and the cut bucket finds the last
+//                         victim with a block scan of the sizes
+//   8 sel_big_kernel      buckets whose windows tie, or above the cap: the
+//                         full varying bits (<= 192) radix-sorted in chunks,
+//                         chunks merged along merge paths
+//
+// Keys are unique -- the third word is the slot when slots are in id order
+// (ids appended ascending) and the id otherwise -- so the order is total
+// and the output deterministic even though records are appended in
+// reservation order.
+#pragma once
+
+#include <cub/block/block_radix_sort.cuh>
+
+#include "common.cuh"
+#include "evict.cuh"
+
+namespace sine {
+
+struct SelRec {
+    uint64_t k0, k1, k2;  // (primary, created_at, slot-or-id) order keys
+    int64_t size;
+};
+
+struct SelCtl {
+    uint64_t hi[3];
+    int32_t all;       // take every live slot (host: small stores / retry; sample: bound >= total)
+    int32_t retry;     // records below hi do not reach the excess: re-run with all = 1
+    int32_t nb;        // buckets
+    int32_t cutb;      // bucket holding the last victim
+    int32_t nbig;      // buckets above the cap
+    int32_t pad;
+    unsigned long long count;  // records
+    unsigned long long wtake;  // their size
+    unsigned long long rand[3], ror[3];  // AND / OR of the record keys (host presets ~0 / 0)
+    int64_t wbase;     // size of the buckets before cutb
+    int64_t V;         // victims
+};
+
+constexpr int kSelSample = 4096;       // sel_sample_kernel: 1024 threads x 4
+constexpr int kSelSplitSample = 4096;  // sel_split_kernel: 1024 threads x 4
+constexpr int kSelMaxBuckets = 1024;
+constexpr int kSelSortThreads = 512;
+constexpr int kSelCap = 8 * kSelSortThreads;      // records one CTA window-sorts
+constexpr int kSelFullCap = 8 * kSelSortThreads;  // records one CTA full-key-sorts
+constexpr int kSelStage = 2048;               // collect: records staged per CTA
+constexpr int kSelRadixBits = 6;
+
+__device__ __forceinline__ bool key_less(uint64_t a0, uint64_t a1, uint64_t a2, uint64_t b0, uint64_t b1,
+                                         uint64_t b2) {
+    return a0 != b0 ? a0 < b0 : (a1 != b1 ? a1 < b1 : a2 < b2);
+}
+__device__ __forceinline__ bool rec_less(const SelRec& a, const SelRec& b) {
+    return key_less(a.k0, a.k1, a.k2, b.k0, b.k1, b.k2);
+}
+__device__ __forceinline__ int64_t rec_id(const SelRec& r, int slot_tie, const int64_t* ids) {
+    return slot_tie ? ids[r.k2] : static_cast<int64_t>(r.k2 ^ 0x8000000000000000ull);
+}
+__device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t i64max(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// Exclusive block scan of one int64 per thread.
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wtot, int64_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int64_t x = lane < nw ? wtot[lane] : 0;
+        int64_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        if (lane < nw) wtot[lane] = xi - x;
+        if (lane == 31) *total = xi;
+    }
+    __syncthreads();
+    const int64_t r = wtot[warp] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+// Block AND / OR of three words (sa, so: 3 shared words each, preset).
+__device__ __forceinline__ void block_and_or3(uint64_t a[3], uint64_t o[3], unsigned long long* sa,
+                                              unsigned long long* so) {
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            a[w] &= __shfl_xor_sync(0xffffffffu, a[w], d);
+            o[w] |= __shfl_xor_sync(0xffffffffu, o[w], d);
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+            atomicAnd(sa + w, static_cast<unsigned long long>(a[w]));
+            atomicOr(so + w, static_cast<unsigned long long>(o[w]));
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 3; ++w) a[w] = sa[w], o[w] = so[w];
+}
+
+// 64 bits of the 192-bit key starting at its first bit that varies over a
+// set (given the set's AND / OR): order-preserving up to ties for the set.
+__device__ __forceinline__ uint64_t key_window(uint64_t k0, uint64_t k1, uint64_t k2, const uint64_t a[3],
+                                               const uint64_t o[3]) {
+    const uint64_t k[3] = {k0, k1, k2};
+    int p = 192;
+#pragma unroll
+    for (int w = 2; w >= 0; --w)
+        if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
+    if (p >= 192) return 0;
+    const int w = p >> 6, off = p & 63;
+    uint64_t v = k[w] << off;
+    if (off && w < 2) v |= k[w + 1] >> (64 - off);
+    return v;
+}
+
+__device__ __forceinline__ void slot_keys(const EvictCols& c, int64_t s, int policy, double now, int slot_tie,
+                                          uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+    k0 = primary_key(c, s, policy, now);
+    k1 = f64_key(c.created[s]);
+    k2 = slot_tie ? static_cast<uint64_t>(s) : i64_key(c.ids[s]);
+}
+
+// ---------------------------------------------------------------- 1 sample
+// 8 bits of a 192-bit key at big-endian bit q (q + 8 <= 192).
+__device__ __forceinline__ uint32_t key_digit8(const uint64_t k[3], int q) {
+    const int w = q >> 6, off = q & 63;
+    uint64_t v = k[w] << off;
+    if (off > 56) v |= k[w + 1] >> (64 - off);
+    return static_cast<uint32_t>(v >> 56);
+}
+
+// Weighted radix select over the full keys of 4096 strided samples (8-bit
+// digits from the first varying bit; a sample stays alive while it matches
+// every chosen digit) until one sample is left: the one where the
+// cumulative size reaches the target.  hi = its full key.
+__global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int policy, double now, int64_t nlive,
+                                                         int64_t excess, int slot_tie, SelCtl* ctl) {
+    __shared__ uint32_t hl[256], hh[256], hc[256];
+    __shared__ int64_t wtot[32];
+    __shared__ int64_t wsum;
+    __shared__ unsigned long long sa[3], so[3];
+    __shared__ int nvalid, digit, left;
+    __shared__ int64_t below;
+    constexpr int per = kSelSample / 1024;
+    if (threadIdx.x < 3) sa[threadIdx.x] = ~0ull, so[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) nvalid = 0;
+    __syncthreads();
+    const int64_t ns = c.nslots;
+    uint64_t k[per][3];
+    int64_t W[per];
+    bool alive[per];
+    uint64_t a[3] = {~0ull, ~0ull, ~0ull}, o[3] = {0, 0, 0};
+    int nv_local = 0;
+    int64_t wloc = 0;
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+        const int i = per * threadIdx.x + j;
+        const int64_t s = ((2 * static_cast<int64_t>(i) + 1) * ns) / (2 * kSelSample);
+        alive[j] = valid_bit(c.valid, s);
+        W[j] = 0;
+        k[j][0] = k[j][1] = k[j][2] = 0;
+        if (alive[j]) {
+            slot_keys(c, s, policy, now, slot_tie, k[j][0], k[j][1], k[j][2]);
+            W[j] = c.size[s];
+            wloc += W[j];
+            ++nv_local;
+#pragma unroll
+            for (int w = 0; w < 3; ++w) a[w] &= k[j][w], o[w] |= k[j][w];
+        }
+    }
+    if (nv_local) atomicAdd(&nvalid, nv_local);
+    block_and_or3(a, o, sa, so);
+    block_excl_scan(wloc, wtot, &wsum);
+    const int nv = nvalid;
+    const int64_t ws = wsum;
+    // weighted quantile of the excess + a 6-sigma sampling margin
+    double g = 2.0;
+    if (nv > 0 && ws > 0) {
+        const double west = static_cast<double>(ws) * static_cast<double>(nlive) / nv;
+        const double f = fmin(1.0, static_cast<double>(excess) / west);
+        g = f + 6.0 * sqrt(fmax(f * (1.0 - f), 1.0 / nv) / nv) + 4.0 / nv;
+    }
+    if (g >= 1.0) {
+        if (threadIdx.x == 0) ctl->all = 1;
+        return;
+    }
+    int p = 192;  // first bit varying over the samples
+#pragma unroll
+    for (int w = 2; w >= 0; --w)
+        if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
+    int64_t rem = static_cast<int64_t>(ceil(g * static_cast<double>(ws)));
+    int nleft = nv;
+    for (int q0 = p; q0 < 192 && nleft > 1;) {
+        const int q = q0 < 184 ? q0 : 184;  // the last digit may overlap fixed bits
+        if (threadIdx.x < 256) hl[threadIdx.x] = hh[threadIdx.x] = hc[threadIdx.x] = 0;
+        __syncthreads();
+        uint32_t dg[per];
+#pragma unroll
+        for (int j = 0; j < per; ++j) {
+            dg[j] = key_digit8(k[j], q);
+            if (alive[j]) {
+                smem_add64(&hl[dg[j]], &hh[dg[j]], static_cast<uint64_t>(W[j]));
+                atomicAdd(&hc[dg[j]], 1u);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // warp 0: bins 8l .. 8l + 7
+            int64_t v[8], t = 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int bn = 8 * threadIdx.x + r;
+                v[r] = static_cast<int64_t>((static_cast<uint64_t>(hh[bn]) << 32) | hl[bn]);
+                t += v[r];
+            }
+            int64_t inc = t;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, inc, off);
+                if (threadIdx.x >= off) inc += y;
+            }
+            int64_t run = inc - t;
+            int found = 256;
+            int64_t bel = 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if (found == 256 && run + v[r] >= rem) found = 8 * threadIdx.x + r, bel = run;
+                run += v[r];
+            }
+            // rem <= the alive weight is invariant, so some bin reaches it;
+            // otherwise (cannot happen) every slot becomes a record
+            const uint32_t m = __ballot_sync(0xffffffffu, found < 256);
+            const int src = m ? __ffs(m) - 1 : 0;
+            const int fd = __shfl_sync(0xffffffffu, found, src);
+            const int64_t fb = __shfl_sync(0xffffffffu, bel, src);
+            if (threadIdx.x == 0) {
+                digit = m ? fd : -1;
+                below = m ? fb : 0;
+                left = m ? static_cast<int>(hc[fd]) : 0;
+            }
+        }
+        __syncthreads();
+        const int d = digit;
+#pragma unroll
+        for (int j = 0; j < per; ++j) alive[j] = alive[j] && static_cast<int>(dg[j]) == d;
+        rem -= below;
+        nleft = left;
+        // next digit: the first bit that still varies over the alive samples
+        if (threadIdx.x < 3) sa[threadIdx.x] = ~0ull, so[threadIdx.x] = 0ull;
+        __syncthreads();
+        uint64_t aa[3] = {~0ull, ~0ull, ~0ull}, oo[3] = {0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < per; ++j)
+            if (alive[j])
+#pragma unroll
+                for (int w = 0; w < 3; ++w) aa[w] &= k[j][w], oo[w] |= k[j][w];
+        block_and_or3(aa, oo, sa, so);
+        int pn = 192;
+#pragma unroll
+        for (int w = 2; w >= 0; --w)
+            if (aa[w] ^ oo[w]) pn = 64 * w + __clzll(aa[w] ^ oo[w]);
+        q0 = pn > q + 8 ? pn : q + 8;
+        __syncthreads();
+    }
+    // the surviving sample (keys are unique); `all` when none survived
+    __shared__ int winner;
+    if (threadIdx.x == 0) winner = -1;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < per; ++j)
+        if (alive[j]) winner = per * threadIdx.x + j;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < per; ++j)
+        if (per * static_cast<int>(threadIdx.x) + j == winner) {
+            ctl->hi[0] = k[j][0], ctl->hi[1] = k[j][1], ctl->hi[2] = k[j][2];
+        }
+    if (threadIdx.x == 0 && winner < 0) ctl->all = 1;
+}
+
+// --------------------------------------------------------------- 2 collect
+// Each warp stages its records in its own smem slice and flushes them with
+// one global reservation when the slice could overflow (no block barriers
+// in the streaming loop).
+constexpr int kSelWarpStage = 128;                 // records per warp slice
+constexpr int kSelCollectThreads = 256;
+constexpr int kSelCollectU = 1;                    // slot pairs per lane per warp tile
+constexpr int kSelCollectSmem = (kSelCollectThreads / 32) * kSelWarpStage * static_cast<int>(sizeof(SelRec));
+
+__device__ __forceinline__ void warp_flush(SelRec* st, int& n, SelCtl* ctl, SelRec* rec) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long b = 0;
+    if (lane == 0 && n) b = atomicAdd(&ctl->count, static_cast<unsigned long long>(n));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) rec[b + i] = st[i];
+    __syncwarp();
+    n = 0;
+}
+
+// Warp tile t covers pairs [t * 32 * U, +32 * U): 16-byte column loads, U per lane
+// and column in flight; then, in one batch, the created_at / id loads of the
+// slots whose primary key is at or below the bound's (one extra latency per
+// tile, not one per slot).
+__global__ void __launch_bounds__(kSelCollectThreads, 4) sel_collect_kernel(const EvictCols c, int policy, double now,
+                                                                          int slot_tie, SelCtl* ctl, SelRec* rec) {
+    extern __shared__ uint64_t sel_smem[];
+    constexpr int U = kSelCollectU;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    SelRec* st = reinterpret_cast<SelRec*>(sel_smem) + warp * kSelWarpStage;
+    int nst = 0;
+    const int all = ctl->all;
+    const uint64_t hi[3] = {ctl->hi[0], ctl->hi[1], ctl->hi[2]};
+    const int64_t npairs = c.nslots >> 1;
+    const int64_t ntiles = (npairs + 1 + 32 * U - 1) / (32 * U);  // + 1: the odd tail slot
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kSelCollectThreads / 32);
+    unsigned long long wl = 0;
+    uint64_t ra[3] = {~0ull, ~0ull, ~0ull}, ro[3] = {0, 0, 0};
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(kSelCollectThreads / 32) + warp; t < ntiles; t += nwarps) {
+        uint64_t key[U][2];
+        int64_t sz[U][2];
+        bool act[U][2];
+        int64_t s0[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = t * 32 * U + u * 32 + lane;
+            s0[u] = 2 * p;
+            const bool in = p < npairs;
+            const uint32_t vw = in ? __ldg(c.valid + (s0[u] >> 5)) : 0u;
+            act[u][0] = (vw >> (s0[u] & 31)) & 1u;
+            act[u][1] = (vw >> ((s0[u] + 1) & 31)) & 1u;
+            const longlong2 z = in ? __ldg(reinterpret_cast<const longlong2*>(c.size) + p) : make_longlong2(0, 0);
+            sz[u][0] = z.x, sz[u][1] = z.y;
+            if (policy == 0) {
+                const double2 zero = make_double2(0.0, 0.0);
+                const double2 lf = in ? __ldg(reinterpret_cast<const double2*>(c.lf) + p) : zero;
+                const double2 lc = in ? __ldg(reinterpret_cast<const double2*>(c.lc) + p) : zero;
+                const double2 ll = in ? __ldg(reinterpret_cast<const double2*>(c.ll) + p) : zero;
+                const double2 ls = in ? __ldg(reinterpret_cast<const double2*>(c.ls) + p) : zero;
+                const double2 ex = in ? __ldg(reinterpret_cast<const double2*>(c.expiration) + p) : zero;
+                // cal_score (engine.py:33-48): exact order, no FMA contraction
+                double v0 = 0.0, v1 = 0.0;
+                if (z.x != 0 && !(__dsub_rn(ex.x, now) <= 0.0))
+                    v0 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(lf.x, lc.x), ll.x), ls.x), static_cast<double>(z.x));
+                if (z.y != 0 && !(__dsub_rn(ex.y, now) <= 0.0))
+                    v1 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(lf.y, lc.y), ll.y), ls.y), static_cast<double>(z.y));
+                key[u][0] = f64_key(v0), key[u][1] = f64_key(v1);
+            } else if (policy == 1) {
+                const double2 la = in ? __ldg(reinterpret_cast<const double2*>(c.last_access) + p)
+                                      : make_double2(0.0, 0.0);
+                key[u][0] = f64_key(la.x), key[u][1] = f64_key(la.y);
+            } else {
+                const longlong2 fq = in ? __ldg(reinterpret_cast<const longlong2*>(c.freq) + p) : make_longlong2(0, 0);
+                key[u][0] = i64_key(fq.x), key[u][1] = i64_key(fq.y);
+            }
+            if (p == npairs && (c.nslots & 1)) {  // the odd tail slot
+                const int64_t s = c.nslots - 1;
+                s0[u] = s;
+                act[u][0] = valid_bit(c.valid, s);
+                act[u][1] = false;
+                sz[u][0] = act[u][0] ? c.size[s] : 0;
+                key[u][0] = act[u][0] ? primary_key(c, s, policy, now) : 0ull;
+            }
+        }
+        // candidates: primary key at or below the bound's (or every slot)
+        uint64_t k1[U][2], k2[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                act[u][e] = act[u][e] && (all || key[u][e] <= hi[0]);
+                const int64_t s = s0[u] + e;
+                k1[u][e] = act[u][e] ? f64_key(__ldg(c.created + s)) : 0ull;
+                k2[u][e] = act[u][e] ? (slot_tie ? static_cast<uint64_t>(s) : i64_key(__ldg(c.ids + s))) : 0ull;
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                bool take = act[u][e];
+                if (take && !all && key[u][e] == hi[0])
+                    take = k1[u][e] != hi[1] ? k1[u][e] < hi[1] : k2[u][e] <= hi[2];
+                const uint32_t m = __ballot_sync(0xffffffffu, take);
+                if (!m) continue;
+                if (nst + __popc(m) > kSelWarpStage) warp_flush(st, nst, ctl, rec);
+                if (take) {
+                    wl += static_cast<unsigned long long>(sz[u][e]);
+                    SelRec r;
+                    r.k0 = key[u][e];
+                    r.k1 = k1[u][e];
+                    r.k2 = k2[u][e];
+                    r.size = sz[u][e];
+                    ra[0] &= r.k0, ra[1] &= r.k1, ra[2] &= r.k2;
+                    ro[0] |= r.k0, ro[1] |= r.k1, ro[2] |= r.k2;
+                    st[nst + __popc(m & ((1u << lane) - 1u))] = r;
+                }
+                nst += __popc(m);
+            }
+        }
+    }
+    warp_flush(st, nst, ctl, rec);
+    // per-warp reductions straight to the control block
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            ra[w] &= __shfl_xor_sync(0xffffffffu, ra[w], d);
+            ro[w] |= __shfl_xor_sync(0xffffffffu, ro[w], d);
+        }
+    }
+    if (lane == 0 && wl) {
+        atomicAdd(&ctl->wtake, wl);
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+            atomicAnd(&ctl->rand[w], static_cast<unsigned long long>(ra[w]));
+            atomicOr(&ctl->ror[w], static_cast<unsigned long long>(ro[w]));
+        }
+    }
+}
+
+// 32-bit window of a record relative to the records' AND / OR: a prefix of
+// the full key over the record set, so window order never contradicts it.
+__device__ __forceinline__ uint32_t rec_win32(const SelRec& r, const uint64_t a[3], const uint64_t o[3]) {
+    return static_cast<uint32_t>(key_window(r.k0, r.k1, r.k2, a, o) >> 32);
+}
+
+__device__ __forceinline__ void ctl_and_or(const SelCtl* ctl, uint64_t a[3], uint64_t o[3]) {
+#pragma unroll
+    for (int w = 0; w < 3; ++w) a[w] = ctl->rand[w], o[w] = ctl->ror[w];
+}
+
+// ----------------------------------------------------------------- 3 split
+// 4096 sampled records' windows radix-sorted; every os-th is a splitter
+// (32-bit values: bucket b holds the windows in (spl[b-1], spl[b]]), plus a
+// table over the top 12 window bits: tab[t] = splitters whose top 12 bits
+// are below t, so a record's bucket is tab[t] + a search among the few
+// splitters sharing its top bits.
+using SplitSort = cub::BlockRadixSort<uint32_t, 1024, kSelSplitSample / 1024, cub::NullType, 4>;
+
+__global__ void __launch_bounds__(1024) sel_split_kernel(int64_t excess, SelCtl* ctl, const SelRec* rec,
+                                                        uint32_t* spl, uint32_t* tab, int cap) {
+    __shared__ typename SplitSort::TempStorage ts;
+    __shared__ uint32_t S[kSelMaxBuckets];
+    if (!ctl->all && static_cast<int64_t>(ctl->wtake) < excess) {
+        if (threadIdx.x == 0) ctl->retry = 1;
+        return;
+    }
+    const int64_t M = static_cast<int64_t>(ctl->count);
+    if (M <= cap) {  // one bucket
+        if (threadIdx.x == 0) ctl->nb = 1;
+        return;
+    }
+    uint64_t a[3], o[3];
+    ctl_and_or(ctl, a, o);
+    constexpr int per = kSelSplitSample / 1024;
+    uint32_t keys[per];
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+        const int i = per * threadIdx.x + j;
+        keys[j] = rec_win32(rec[((2 * static_cast<int64_t>(i) + 1) * M) / (2 * kSelSplitSample)], a, o);
+    }
+    SplitSort(ts).Sort(keys);
+    // buckets of ~cap/3 records on average (the sampling spread stays below cap)
+    int nb = 2;
+    while (nb < kSelMaxBuckets && nb < kSelSplitSample / 4 && static_cast<int64_t>(nb) * (cap / 3) < M) nb <<= 1;
+    const int os = kSelSplitSample / nb;
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+        const int r = per * threadIdx.x + j + 1;  // 1-based rank
+        if (r % os == 0 && r < kSelSplitSample) S[r / os - 1] = keys[j];
+    }
+    __syncthreads();
+    const int ns = nb - 1;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) spl[j] = S[j];
+    for (int t = threadIdx.x; t <= 4096; t += blockDim.x) {
+        int lo = 0, hi = ns;  // splitters with top-12 bits < t
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (static_cast<int>(S[mid] >> 20) < t)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        tab[t] = static_cast<uint32_t>(lo);
+    }
+    if (threadIdx.x == 0) ctl->nb = nb;
+}
+
+// ------------------------------------------------------ 4 bucket, 6 scatter
+constexpr int kSelBucketSmem = kSelMaxBuckets * 4 + 4100 * 4 + kSelMaxBuckets * 12;
+
+__device__ __forceinline__ int find_bucket(uint32_t w, const uint32_t* S, const uint32_t* T) {
+    const int t = static_cast<int>(w >> 20);
+    int lo = static_cast<int>(T[t]), hi = static_cast<int>(T[t + 1]);
+    while (lo < hi) {  // splitters below w among those sharing its top bits
+        const int mid = (lo + hi) >> 1;
+        if (S[mid] < w)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Both kernels give CTA x the same contiguous record range.
+__device__ __forceinline__ void cta_range(int64_t M, int64_t& b, int64_t& e) {
+    const int64_t per = (M + gridDim.x - 1) / gridDim.x;
+    b = i64min(M, per * blockIdx.x);
+    e = i64min(M, b + per);
+}
+
+__global__ void __launch_bounds__(1024) sel_bucket_kernel(const SelCtl* ctl, const SelRec* rec, const uint32_t* spl,
+                                                         const uint32_t* tab, uint16_t* bid,
+                                                         unsigned long long* bcnt, unsigned long long* bw) {
+    extern __shared__ uint64_t sel_smem[];
+    if (ctl->retry) return;
+    const int nb = ctl->nb, ns = nb - 1;
+    uint32_t* S = reinterpret_cast<uint32_t*>(sel_smem);
+    uint32_t* T = S + kSelMaxBuckets;
+    uint32_t* sc = T + 4100;
+    uint32_t* swl = sc + kSelMaxBuckets;
+    uint32_t* swh = swl + kSelMaxBuckets;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) S[j] = spl[j];
+    for (int j = threadIdx.x; j <= 4096; j += blockDim.x) T[j] = ns ? tab[j] : 0u;
+    if (threadIdx.x == 0) T[4097] = ns;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) sc[j] = swl[j] = swh[j] = 0;
+    __syncthreads();
+    uint64_t a[3], o[3];
+    ctl_and_or(ctl, a, o);
+    int64_t b, e;
+    cta_range(static_cast<int64_t>(ctl->count), b, e);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const SelRec r = rec[i];
+        const int k = ns ? find_bucket(rec_win32(r, a, o), S, T) : 0;
+        bid[i] = static_cast<uint16_t>(k);
+        atomicAdd(&sc[k], 1u);
+        smem_add64(&swl[k], &swh[k], static_cast<uint64_t>(r.size));
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+        if (sc[j]) {
+            atomicAdd(bcnt + j, static_cast<unsigned long long>(sc[j]));
+            atomicAdd(bw + j, (static_cast<unsigned long long>(swh[j]) << 32) | swl[j]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) sel_scatter_kernel(const SelCtl* ctl, const SelRec* rec, const uint16_t* bid,
+                                                          const int64_t* boff, uint32_t* bcur, SelRec* rec2) {
+    __shared__ uint32_t lc[kSelMaxBuckets], lb[kSelMaxBuckets];
+    if (ctl->retry) return;
+    const int nb = ctl->nb, cutb = ctl->cutb;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) lc[j] = 0;
+    __syncthreads();
+    int64_t b, e;
+    cta_range(static_cast<int64_t>(ctl->count), b, e);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const int k = bid[i];
+        if (k <= cutb) atomicAdd(&lc[k], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j <= cutb; j += blockDim.x) {
+        lb[j] = lc[j] ? atomicAdd(bcur + j, lc[j]) : 0u;
+        lc[j] = 0;
+    }
+    __syncthreads();
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const int k = bid[i];
+        if (k > cutb) continue;
+        rec2[boff[k] + lb[k] + atomicAdd(&lc[k], 1u)] = rec[i];
+    }
+}
+
+// ------------------------------------------------------------------ 5 scan
+__global__ void __launch_bounds__(1024) sel_scan_kernel(SelCtl* ctl, int64_t excess, const unsigned long long* bcnt,
+                                                       const unsigned long long* bw, int64_t* boff, uint32_t* bcur) {
+    __shared__ int64_t wtot[32];
+    __shared__ int64_t total;
+    __shared__ int cut;
+    if (ctl->retry) return;
+    const int nb = ctl->nb;
+    constexpr int per = kSelMaxBuckets / 1024;
+    const int b0 = per * threadIdx.x;
+    int64_t c[per], w[per], lc = 0, lw = 0;
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+        c[j] = b0 + j < nb ? static_cast<int64_t>(bcnt[b0 + j]) : 0;
+        w[j] = b0 + j < nb ? static_cast<int64_t>(bw[b0 + j]) : 0;
+        lc += c[j], lw += w[j];
+    }
+    if (threadIdx.x == 0) cut = nb - 1;
+    int64_t oc = block_excl_scan(lc, wtot, &total);
+    int64_t ow = block_excl_scan(lw, wtot, &total);
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+        if (b0 + j < nb) {
+            boff[b0 + j] = oc;
+            bcur[b0 + j] = 0;
+            if (ow + w[j] >= excess) atomicMin(&cut, b0 + j);
+        }
+        oc += c[j], ow += w[j];
+    }
+    __syncthreads();
+    int64_t pw = 0;
+#pragma unroll
+    for (int j = 0; j < per; ++j)
+        if (b0 + j < cut) pw += w[j];
+    block_excl_scan(pw, wtot, &total);
+    if (threadIdx.x == 0) {
+        ctl->cutb = cut;
+        ctl->wbase = total;  // size of the buckets before the cut bucket
+    }
+}
+
+// ------------------------------------------------------- 7 bucket sorting
+// Packed key: per word only the low bits that vary over the bucket, the
+// three fields concatenated (word 0 most significant).  <= 128 bits (the
+// common case: a constant or narrow primary key) sorts as two words,
+// otherwise as three.
+struct Key2 {
+    uint64_t w1, w0;  // most .. least significant
+};
+struct Key3 {
+    uint64_t w2, w1, w0;
+};
+struct Key2Decomposer {
+    __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&> operator()(Key2& k) const { return {k.w1, k.w0}; }
+};
+struct Key3Decomposer {
+    __host__ __device__ ::cuda::std::tuple<uint64_t&, uint64_t&, uint64_t&> operator()(Key3& k) const {
+        return {k.w2, k.w1, k.w0};
+    }
+};
+
+// (w2, w1, w0) |= v << sh for v < 2^64, sh in [0, 192)
+__device__ __forceinline__ void or_shl(uint64_t& w2, uint64_t& w1, uint64_t& w0, uint64_t v, int sh) {
+    const int q = sh >> 6, r = sh & 63;
+    const uint64_t lo = v << r, hi = r ? (v >> (64 - r)) : 0ull;
+    if (q == 0) {
+        w0 |= lo;
+        w1 |= hi;
+    } else if (q == 1) {
+        w1 |= lo;
+        w2 |= hi;
+    } else {
+        w2 |= lo;
+    }
+}
+
+template <typename K, int IPT>
+using BucketSort = cub::BlockRadixSort<K, kSelSortThreads, IPT, uint16_t, kSelRadixBits>;
+
+union BucketSortStorage {
+    typename BucketSort<Key2, 2>::TempStorage a2;
+    typename BucketSort<Key2, 4>::TempStorage a4;
+    typename BucketSort<Key2, 8>::TempStorage a8;
+    typename BucketSort<Key3, 2>::TempStorage b2;
+    typename BucketSort<Key3, 4>::TempStorage b4;
+    typename BucketSort<Key3, 8>::TempStorage b8;
+};
+
+struct BucketShared {
+    BucketSortStorage sort;
+    unsigned long long sa[3], so[3];
+    int64_t wtot[32];
+    int64_t total;
+    int first;
+};
+
+constexpr int kSelSortSmem = static_cast<int>(sizeof(BucketShared));
+
+template <typename K, int IPT>
+__device__ __forceinline__ typename BucketSort<K, IPT>::TempStorage& sort_storage(BucketShared& sh) {
+    return *reinterpret_cast<typename BucketSort<K, IPT>::TempStorage*>(&sh.sort);
+}
+
+template <typename K, int IPT>
+__device__ __forceinline__ void bucket_sort_k(const SelRec* src, int n, const int span[3], int total,
+                                              BucketShared& sh, uint16_t (&idx)[IPT]) {
+    K keys[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const int i = threadIdx.x * IPT + j;
+        idx[j] = i < n ? static_cast<uint16_t>(i) : static_cast<uint16_t>(0xffff);
+        uint64_t w2 = 0, w1 = 0, w0 = 0;
+        if (i < n) {
+            const SelRec r = src[i];  // second read: L1 / L2
+            const uint64_t f[3] = {r.k0, r.k1, r.k2};
+            int at = total;
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                at -= span[w];
+                if (span[w]) or_shl(w2, w1, w0, span[w] == 64 ? f[w] : (f[w] & ((1ull << span[w]) - 1)), at);
+            }
+        } else {
+            w2 = w1 = w0 = ~0ull;  // after every real key (stable on ties)
+        }
+        if constexpr (sizeof(K) == 16)
+            keys[j] = K{w1, w0};
+        else
+            keys[j] = K{w2, w1, w0};
+    }
+    if constexpr (sizeof(K) == 16)
+        BucketSort<K, IPT>(sort_storage<K, IPT>(sh)).Sort(keys, idx, Key2Decomposer{}, 0, total);
+    else
+        BucketSort<K, IPT>(sort_storage<K, IPT>(sh)).Sort(keys, idx, Key3Decomposer{}, 0, total);
+}
+
+// Sorts src[0, n) (n <= 512 * IPT) by full key; thread t's items j hold the
+// ranks t * IPT + j as indices into src (0xffff: padding).
+template <int IPT>
+__device__ __forceinline__ void bucket_sort(const SelRec* src, int n, BucketShared& sh, uint16_t (&idx)[IPT]) {
+    uint64_t a[3] = {~0ull, ~0ull, ~0ull}, o[3] = {0, 0, 0};
+    if (threadIdx.x < 3) sh.sa[threadIdx.x] = ~0ull, sh.so[threadIdx.x] = 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const int i = threadIdx.x * IPT + j;
+        if (i < n) {
+            const SelRec r = src[i];
+            a[0] &= r.k0, a[1] &= r.k1, a[2] &= r.k2;
+            o[0] |= r.k0, o[1] |= r.k1, o[2] |= r.k2;
+        }
+    }
+    block_and_or3(a, o, sh.sa, sh.so);
+    int span[3], total = 0;
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+        const uint64_t d = a[w] ^ o[w];
+        span[w] = d ? 64 - __clzll(d) : 0;
+        total += span[w];
+    }
+    if (total == 0) {  // one record (keys are unique)
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const int i = threadIdx.x * IPT + j;
+            idx[j] = i < n ? static_cast<uint16_t>(i) : static_cast<uint16_t>(0xffff);
+        }
+    } else if (total <= 128) {
+        bucket_sort_k<Key2, IPT>(src, n, span, total, sh, idx);
+    } else {
+        bucket_sort_k<Key3, IPT>(src, n, span, total, sh, idx);
+    }
+}
+
+// Victim ids of sorted records at their final positions [base, base + n)
+// (get(idx[j]) = the record of rank t * IPT + j).  With `cut`, also the
+// first rank where the size sum from `wbase` reaches the excess: sets V and
+// returns true when found; sh.total = the size of these n records.
+template <int IPT, typename GetRec, typename Sh>
+__device__ __forceinline__ bool bucket_emit(GetRec get, const uint16_t (&idx)[IPT], int n, int64_t base, bool cut,
+                                            int64_t wbase, int64_t excess, int slot_tie, const int64_t* ids,
+                                            int64_t* out, SelCtl* ctl, Sh& sh) {
+    int64_t sz[IPT];
+    int64_t loc = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const int rk = threadIdx.x * IPT + j;
+        sz[j] = 0;
+        if (rk < n) {
+            const SelRec r = get(idx[j]);
+            out[base + rk] = rec_id(r, slot_tie, ids);
+            loc += (sz[j] = r.size);
+        }
+    }
+    if (!cut) return false;
+    if (threadIdx.x == 0) sh.first = n;
+    int64_t run = wbase + block_excl_scan(loc, sh.wtot, &sh.total);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const int rk = threadIdx.x * IPT + j;
+        if (rk < n) {
+            run += sz[j];
+            if (run >= excess) {
+                atomicMin(&sh.first, rk);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    const int first = sh.first;
+    if (threadIdx.x == 0) ctl->V = base + (first < n ? first + 1 : n);
+    __syncthreads();
+    return first < n;
+}
+
+// ------------------------------------------------ 7 bucket sort (window)
+// Per bucket: the top 20 of the 32 bits from the bucket's first varying bit
+// are block-radix-sorted (5 passes of 4 bits); records whose 20-bit windows
+// tie form short runs that one thread orders by full key (insertion sort).
+// Runs longer than kSelRunMax (heavy ties: e.g. equal primary keys and
+// equal created_at) send the bucket to the full-key kernel (sel_big_kernel).
+constexpr int kSelWinBits = 20;
+constexpr int kSelRunMax = 64;
+
+template <int IPT>
+using WinSort = cub::BlockRadixSort<uint32_t, kSelSortThreads, IPT, uint16_t, 4>;
+
+union WinSortStorage {
+    typename WinSort<2>::TempStorage s2;
+    typename WinSort<4>::TempStorage s4;
+    typename WinSort<8>::TempStorage s8;
+};
+
+struct WinShared {
+    WinSortStorage sort;
+    uint32_t skey[kSelCap];
+    uint16_t sidx[kSelCap];
+    unsigned long long sa[3], so[3];
+    int64_t wtot[32];
+    int64_t total;
+    int first;
+    int tie;
+};
+
+constexpr int kSelWinSmem = static_cast<int>(sizeof(WinShared));
+
+template <int IPT>
+__device__ __forceinline__ bool win_sort_emit(const SelRec* src, int n, int64_t base, bool cut, int64_t wbase,
+                                              int64_t excess, int slot_tie, const int64_t* ids, int64_t* out,
+                                              SelCtl* ctl, WinShared& sh) {
+    uint64_t a[3] = {~0ull, ~0ull, ~0ull}, o[3] = {0, 0, 0};
+    if (threadIdx.x < 3) sh.sa[threadIdx.x] = ~0ull, sh.so[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) sh.tie = 0;
+    __syncthreads();
+    uint32_t keys[IPT];
+    uint16_t idx[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const int i = threadIdx.x * IPT + j;
+        if (i < n) {
+            const SelRec r = src[i];
+            a[0] &= r.k0, a[1] &= r.k1, a[2] &= r.k2;
+            o[0] |= r.k0, o[1] |= r.k1, o[2] |= r.k2;
+        }
+    }
+    block_and_or3(a, o, sh.sa, sh.so);
+    int span = 0;  // bits from the first varying bit to the last
+    {
+        int p = 192, q = -1;
+#pragma unroll
+        for (int w = 2; w >= 0; --w)
+            if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
+#pragma unroll
+        for (int w = 0; w < 3; ++w)
+            if (a[w] ^ o[w]) q = 64 * w + 64 - __ffsll(static_cast<long long>(a[w] ^ o[w]));
+        span = q >= p ? q - p + 1 : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const int i = threadIdx.x * IPT + j;
+        idx[j] = i < n ? static_cast<uint16_t>(i) : static_cast<uint16_t>(0xffff);
+        keys[j] = 0xffffffffu;
+        if (i < n) {
+            const SelRec r = src[i];  // second read: L1 / L2
+            keys[j] = static_cast<uint32_t>(key_window(r.k0, r.k1, r.k2, a, o) >> 32);
+        }
+    }
+    // bits below the span are constant; below the top 20, ties are resolved
+    // by full key afterwards
+    const int lo_bit = span >= kSelWinBits ? 32 - kSelWinBits : 32 - span;
+    if constexpr (IPT == 2)
+        WinSort<2>(sh.sort.s2).Sort(keys, idx, lo_bit, 32);
+    else if constexpr (IPT == 4)
+        WinSort<4>(sh.sort.s4).Sort(keys, idx, lo_bit, 32);
+    else
+        WinSort<8>(sh.sort.s8).Sort(keys, idx, lo_bit, 32);
+    if (span > kSelWinBits) {  // windows may tie: order each run of equal windows by full key
+        const uint32_t msk = ~((1u << lo_bit) - 1u);
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const int r = threadIdx.x * IPT + j;
+            if (r < n) sh.skey[r] = keys[j] & msk, sh.sidx[r] = idx[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const int r = threadIdx.x * IPT + j;
+            if (r + 1 < n && (r == 0 || sh.skey[r - 1] != sh.skey[r]) && sh.skey[r + 1] == sh.skey[r]) {
+                int e = r + 2;
+                while (e < n && sh.skey[e] == sh.skey[r] && e - r <= kSelRunMax) ++e;
+                if (e - r > kSelRunMax) {
+                    sh.tie = 1;
+                } else {
+                    for (int x = r + 1; x < e; ++x) {  // insertion sort by full key
+                        const uint16_t v = sh.sidx[x];
+                        const SelRec rv = src[v];
+                        int y = x - 1;
+                        while (y >= r && rec_less(rv, src[sh.sidx[y]])) {
+                            sh.sidx[y + 1] = sh.sidx[y];
+                            --y;
+                        }
+                        sh.sidx[y + 1] = v;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (sh.tie) return false;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const int r = threadIdx.x * IPT + j;
+            if (r < n) idx[j] = sh.sidx[r];
+        }
+    }
+    bucket_emit<IPT>([&](int i) { return src[i]; }, idx, n, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+    return true;
+}
+
+__global__ void __launch_bounds__(kSelSortThreads, 2) sel_sort_kernel(SelCtl* ctl, int64_t excess, int slot_tie,
+                                                                     const int64_t* ids, const SelRec* rec2,
+                                                                     const int64_t* boff,
+                                                                     const unsigned long long* bcnt, int32_t* big,
+                                                                     int64_t* out, int cap) {
+    extern __shared__ uint64_t sel_smem[];
+    WinShared& sh = *reinterpret_cast<WinShared*>(sel_smem);
+    if (ctl->retry) return;
+    const int cutb = ctl->cutb;
+    const int64_t wbase = ctl->wbase;
+    for (int b = blockIdx.x; b <= cutb; b += gridDim.x) {
+        const int64_t n = static_cast<int64_t>(bcnt[b]);
+        const int64_t base = boff[b];
+        if (n == 0) {
+            if (b == cutb && threadIdx.x == 0) ctl->V = base;
+            continue;
+        }
+        bool ok = false;
+        if (n <= cap) {
+            const SelRec* src = rec2 + base;
+            const int m = static_cast<int>(n);
+            const bool cut = b == cutb;
+            if (m <= 2 * kSelSortThreads)
+                ok = win_sort_emit<2>(src, m, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+            else if (m <= 4 * kSelSortThreads)
+                ok = win_sort_emit<4>(src, m, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+            else
+                ok = win_sort_emit<8>(src, m, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+        }
+        if (!ok && threadIdx.x == 0) big[atomicAdd(&ctl->nbig, 1)] = b;
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------- 8 big sort
+// One CTA per bucket the window sort could not finish (above the cap, or
+// tied windows): chunks radix-sorted on the full key into `tmp`,
+// then pairwise merges along merge paths (ping-pong between tmp and rec2),
+// then the same emission over the sorted run in chunks.
+__global__ void __launch_bounds__(kSelSortThreads) sel_big_kernel(SelCtl* ctl, int64_t excess, int slot_tie,
+                                                                 const int64_t* ids, SelRec* rec2, SelRec* tmp,
+                                                                 const int64_t* boff,
+                                                                 const unsigned long long* bcnt,
+                                                                 const int32_t* big, int64_t* out, int cap) {
+    extern __shared__ uint64_t sel_smem[];
+    BucketShared& sh = *reinterpret_cast<BucketShared*>(sel_smem);
+    if (ctl->retry) return;
+    const int nbig = ctl->nbig;
+    const int cutb = ctl->cutb;
+    for (int e = blockIdx.x; e < nbig; e += gridDim.x) {
+        const int b = big[e];
+        const int64_t n = static_cast<int64_t>(bcnt[b]);
+        const int64_t base = boff[b];
+        SelRec* a = rec2 + base;
+        SelRec* t = tmp + base;
+        const int chunk = cap < kSelFullCap ? cap : kSelFullCap;
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            const int m = static_cast<int>(i64min(chunk, n - c0));
+            uint16_t idx[8];
+            bucket_sort<8>(a + c0, m, sh, idx);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int rk = threadIdx.x * 8 + j;
+                if (rk < m) t[c0 + rk] = a[c0 + idx[j]];
+            }
+            __syncthreads();
+        }
+        SelRec* src = t;
+        SelRec* dst = a;
+        for (int64_t L = chunk; L < n; L <<= 1) {
+            for (int64_t i = 0; i < n; i += 2 * L) {
+                const SelRec* A = src + i;
+                const int64_t na = i64min(L, n - i);
+                const SelRec* B = A + na;
+                const int64_t nbb = i64max(0, i64min(L, n - i - na));
+                const int64_t tot = na + nbb;
+                const int64_t per = (tot + blockDim.x - 1) / blockDim.x;
+                const int64_t d0 = i64min(tot, per * threadIdx.x);
+                const int64_t d1 = i64min(tot, d0 + per);
+                int64_t lo = i64max(0, d0 - nbb), hi = i64min(d0, na);
+                while (lo < hi) {  // merge path: first a with A[a] after B[d0 - 1 - a]
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (rec_less(A[mid], B[d0 - 1 - mid]))
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                int64_t ia = lo, ib = d0 - lo;
+                for (int64_t d = d0; d < d1; ++d) {
+                    const bool take_a = ib >= nbb || (ia < na && rec_less(A[ia], B[ib]));
+                    dst[i + d] = take_a ? A[ia++] : B[ib++];
+                }
+            }
+            __syncthreads();
+            SelRec* x = src;
+            src = dst;
+            dst = x;
+        }
+        int64_t wb = ctl->wbase;
+        for (int64_t c0 = 0; c0 < n; c0 += kSelFullCap) {
+            const int m = static_cast<int>(i64min(kSelFullCap, n - c0));
+            uint16_t idx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) idx[j] = static_cast<uint16_t>(threadIdx.x * 8 + j);
+            const SelRec* chunk = src + c0;
+            const bool found = bucket_emit<8>([&](int i) { return chunk[i]; }, idx, m, base + c0, b == cutb, wb,
+                                              excess, slot_tie, ids, out, ctl, sh);
+            if (b == cutb) {
+                if (found) break;
+                wb += sh.total;
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace sine

@@ -44,10 +44,14 @@ def main():
     t0 = time.perf_counter()
     Nat.check(idx._lib.sine_expired(idx.handle, now, 1, p, n, ctypes.byref(cnt)))
     print("expired", cnt.value, f"{(time.perf_counter() - t0) * 1e3:.2f} ms", flush=True)
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        Nat.check(idx._lib.sine_select_victims(idx.handle, 0, now, excess, p, n, ctypes.byref(cnt)))
-        print("victims", cnt.value, f"{(time.perf_counter() - t0) * 1e3:.2f} ms", flush=True)
+    idx.set_timing(True)
+    policies = [int(x) for x in os.environ.get("EVICT_POLICIES", "0").split(",")]
+    for pol in policies:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            Nat.check(idx._lib.sine_select_victims(idx.handle, pol, now, excess, p, n, ctypes.byref(cnt)))
+            print("policy", pol, "victims", cnt.value, f"{(time.perf_counter() - t0) * 1e3:.3f} ms e2e",
+                  f"{idx.last_timing()[2]:.3f} ms device", flush=True)
 
 
 if __name__ == "__main__":
