@@ -163,7 +163,7 @@ int sine_expired(sine_index_t *h, double now, int remove, int64_t *out,
 int sine_select_victims(sine_index_t *h, int policy, double now, int64_t excess,
                         int64_t *out, int64_t cap, int64_t *n);
 /* Test hook (not in the reference): the number of selection records one CTA
- * sorts in shared memory (2..4096, default 4096).  Lower values drive the
+ * sorts in shared memory (2..6144, default 6144).  Lower values drive the
  * merge path for oversized buckets on small stores. */
 int sine_set_select_cap(sine_index_t *h, int cap);
 

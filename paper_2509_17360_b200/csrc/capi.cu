@@ -385,7 +385,7 @@ void alloc_col(T*& p, int64_t n) {
 void grow(sine_index* h, int64_t want) {
     if (want <= h->cap) return;
     int64_t nc = std::max<int64_t>(want, std::max<int64_t>(1024, h->cap * 2));
-    nc = round_up(nc, 32);
+    nc = round_up(nc, 128);  // whole 128-slot groups: TMA tiles of the columns and validity words
     auto move = [&](auto*& col, int64_t width) {
         using T = std::remove_reference_t<decltype(*col)>;
         if (!col && width >= 0) return;
@@ -1440,7 +1440,7 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     h->sctl_h.ensure(1);
     smem_optin(reinterpret_cast<const void*>(sel_collect_kernel), kSelCollectSmem);
     smem_optin(reinterpret_cast<const void*>(sel_bucket_kernel), kSelBucketSmem);
-    smem_optin(reinterpret_cast<const void*>(sel_sort_kernel), kSelWinSmem);
+    smem_optin(reinterpret_cast<const void*>(sel_sort_kernel), kSelCountSmem);
     smem_optin(reinterpret_cast<const void*>(sel_big_kernel), kSelSortSmem);
     const EvictCols cols = evict_cols(h);
     const int slot_tie = h->ids_ascending ? 1 : 0;
@@ -1453,6 +1453,7 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         SelCtl c0{};
         c0.all = all ? 1 : 0;
         for (int w = 0; w < 3; ++w) c0.rand[w] = ~0ull;
+        c0.wmin = ~0ull;
         *h->sctl_h.p = c0;
         CK(cudaMemcpyAsync(h->sctl.p, h->sctl_h.p, sizeof(SelCtl), cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(bcnt, 0, 2 * kSelMaxBuckets * sizeof(unsigned long long), st));
@@ -1460,11 +1461,21 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
             sel_sample_kernel<<<1, 1024, 0, st>>>(cols, policy, now, h->nlive, excess, slot_tie, h->sctl.p);
             ++h->launches;
         }
-        const int64_t tiles = (h->nslots / 2 + 1 + 32 * kSelCollectU - 1) / (32 * kSelCollectU);
-        const int gcol = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>((tiles + kSelCollectThreads / 32 - 1) / (kSelCollectThreads / 32), 4ll * h->num_sms)));
-        sel_collect_kernel<<<gcol, kSelCollectThreads, kSelCollectSmem, st>>>(cols, policy, now, slot_tie, h->sctl.p,
-                                                                              h->srec.p);
+        SelColumns sc{};
+        if (policy == 0) {
+            const void* c7[7] = {h->lf, h->lc, h->ll, h->ls, h->expiration, h->size, h->created};
+            for (int k = 0; k < 7; ++k) sc.col[k] = c7[k];
+            sc.ncol = 7;
+        } else {
+            sc.col[0] = policy == 1 ? static_cast<const void*>(h->last_access) : static_cast<const void*>(h->freq);
+            sc.col[1] = h->size;
+            sc.col[2] = h->created;
+            sc.ncol = 3;
+        }
+        const int64_t tiles = (h->nslots + kSelTile - 1) / kSelTile;
+        const int gcol = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, h->num_sms)));
+        sel_collect_kernel<<<gcol, kSelCollectThreads, kSelCollectSmem, st>>>(cols, sc, policy, now, slot_tie,
+                                                                             h->sctl.p, h->srec.p);
         sel_split_kernel<<<1, 1024, 0, st>>>(excess, h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, scap);
         // bucket and scatter must split the records the same way (same grid)
         const int grec = 2 * h->num_sms;
@@ -1473,8 +1484,8 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         sel_scan_kernel<<<1, 1024, 0, st>>>(h->sctl.p, excess, bcnt, bw, h->sboff.p, h->sbcur.p);
         sel_scatter_kernel<<<grec, 1024, 0, st>>>(h->sctl.p, h->srec.p, h->sbid.p, h->sboff.p, h->sbcur.p,
                                                   h->srec2.p);
-        sel_sort_kernel<<<2 * h->num_sms, kSelSortThreads, kSelWinSmem, st>>>(
-            h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
+        sel_sort_kernel<<<3 * h->num_sms, kSelSortThreads, kSelCountSmem, st>>>(
+            h->sctl.p, excess, slot_tie, h->ids, h->sspl.p, h->srec2.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
         sel_big_kernel<<<h->num_sms, kSelSortThreads, kSelSortSmem, st>>>(
             h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->srec.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
         h->launches += 7;
@@ -2116,7 +2127,7 @@ int sine_stream(sine_index_t* h, void** stream) {
 
 int sine_set_select_cap(sine_index_t* h, int cap) {
     return guarded([&] {
-        if (cap < 2 || cap > kSelCap) fail(SINE_EINVAL, "select cap must be in [2, 4096]");
+        if (cap < 2 || cap > kSelCap) fail(SINE_EINVAL, "select cap must be in [2, 6144]");
         std::lock_guard<std::mutex> g(h->mu);
         h->sel_cap = cap;
     });

@@ -73,6 +73,7 @@ struct SelCtl {
     unsigned long long count;  // records
     unsigned long long wtake;  // their size
     unsigned long long rand[3], ror[3];  // AND / OR of the record keys (host presets ~0 / 0)
+    unsigned long long wmin, wmax;       // min / max 64-bit window of the records (host presets ~0 / 0)
     int64_t wbase;     // size of the buckets before cutb
     int64_t V;         // victims
 };
@@ -81,7 +82,7 @@ constexpr int kSelSample = 4096;       // sel_sample_kernel: 1024 threads x 4
 constexpr int kSelSplitSample = 4096;  // sel_split_kernel: 1024 threads x 4
 constexpr int kSelMaxBuckets = 1024;
 constexpr int kSelSortThreads = 512;
-constexpr int kSelCap = 8 * kSelSortThreads;      // records one CTA window-sorts
+constexpr int kSelCap = 12 * kSelSortThreads;     // records one CTA counting-sorts (6144)
 constexpr int kSelFullCap = 8 * kSelSortThreads;  // records one CTA full-key-sorts
 constexpr int kSelStage = 2048;               // collect: records staged per CTA
 constexpr int kSelRadixBits = 6;
@@ -166,6 +167,24 @@ __device__ __forceinline__ uint64_t key_window(uint64_t k0, uint64_t k1, uint64_
     return v;
 }
 
+// 64 bits of the 192-bit key from big-endian bit p (zero-padded past 192).
+__device__ __forceinline__ uint64_t key_window_at(uint64_t k0, uint64_t k1, uint64_t k2, int p) {
+    if (p >= 192) return 0;
+    const uint64_t k[3] = {k0, k1, k2};
+    const int w = p >> 6, off = p & 63;
+    uint64_t v = k[w] << off;
+    if (off && w < 2) v |= k[w + 1] >> (64 - off);
+    return v;
+}
+
+__device__ __forceinline__ int first_varying(const uint64_t a[3], const uint64_t o[3]) {
+    int p = 192;
+#pragma unroll
+    for (int w = 2; w >= 0; --w)
+        if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
+    return p;
+}
+
 __device__ __forceinline__ void slot_keys(const EvictCols& c, int64_t s, int policy, double now, int slot_tie,
                                           uint64_t& k0, uint64_t& k1, uint64_t& k2) {
     k0 = primary_key(c, s, policy, now);
@@ -209,16 +228,20 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
     for (int j = 0; j < per; ++j) {
         const int i = per * threadIdx.x + j;
         const int64_t s = ((2 * static_cast<int64_t>(i) + 1) * ns) / (2 * kSelSample);
+        // loads issued regardless of validity (one latency, not two)
         alive[j] = valid_bit(c.valid, s);
-        W[j] = 0;
-        k[j][0] = k[j][1] = k[j][2] = 0;
+        slot_keys(c, s, policy, now, slot_tie, k[j][0], k[j][1], k[j][2]);
+        W[j] = c.size[s];
+    }
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
         if (alive[j]) {
-            slot_keys(c, s, policy, now, slot_tie, k[j][0], k[j][1], k[j][2]);
-            W[j] = c.size[s];
             wloc += W[j];
             ++nv_local;
 #pragma unroll
             for (int w = 0; w < 3; ++w) a[w] &= k[j][w], o[w] |= k[j][w];
+        } else {
+            W[j] = 0;
         }
     }
     if (nv_local) atomicAdd(&nvalid, nv_local);
@@ -251,9 +274,34 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
 #pragma unroll
         for (int j = 0; j < per; ++j) {
             dg[j] = key_digit8(k[j], q);
-            if (alive[j]) {
-                smem_add64(&hl[dg[j]], &hh[dg[j]], static_cast<uint64_t>(W[j]));
-                atomicAdd(&hc[dg[j]], 1u);
+            // a quarter of the samples can share one digit (equal scores):
+            // few distinct digits in a warp take one shared atomic per
+            // digit (warp sums), many take plain per-lane atomics
+            const int lane = threadIdx.x & 31;
+            const bool act = alive[j];
+            const uint32_t peers = __match_any_sync(0xffffffffu, act ? dg[j] : 0x100u);
+            const bool group_leader = act && (__ffs(peers) - 1) == lane;
+            if (__popc(__ballot_sync(0xffffffffu, group_leader)) > 4) {
+                if (act) {
+                    smem_add64(&hl[dg[j]], &hh[dg[j]], static_cast<uint64_t>(W[j]));
+                    atomicAdd(&hc[dg[j]], 1u);
+                }
+            } else {
+                uint32_t pend = __ballot_sync(0xffffffffu, act);
+                while (pend) {
+                    const int leader = __ffs(pend) - 1;
+                    const uint32_t ldg = __shfl_sync(0xffffffffu, dg[j], leader);
+                    const bool mine = act && dg[j] == ldg;
+                    const uint32_t grp = __ballot_sync(0xffffffffu, mine);
+                    unsigned long long v = mine ? static_cast<unsigned long long>(W[j]) : 0ull;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                    if (lane == leader) {
+                        smem_add64(&hl[ldg], &hh[ldg], v);
+                        atomicAdd(&hc[ldg], static_cast<uint32_t>(__popc(grp)));
+                    }
+                    pend &= ~grp;
+                }
             }
         }
         __syncthreads();
@@ -332,12 +380,16 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
 
 // --------------------------------------------------------------- 2 collect
 // Each warp stages its records in its own smem slice and flushes them with
-// one global reservation when the slice could overflow (no block barriers
-// in the streaming loop).
-constexpr int kSelWarpStage = 128;                 // records per warp slice
-constexpr int kSelCollectThreads = 256;
-constexpr int kSelCollectU = 1;                    // slot pairs per lane per warp tile
-constexpr int kSelCollectSmem = (kSelCollectThreads / 32) * kSelWarpStage * static_cast<int>(sizeof(SelRec));
+// one global reservation when the slice could overflow.
+constexpr int kSelWarpStage = 96;        // records per warp slice
+constexpr int kSelConsumers = 512;       // 16 consumer warps
+constexpr int kSelCollectThreads = kSelConsumers + 32;  // + one producer warp
+constexpr int kSelTile = 1024;           // slots per TMA tile
+constexpr int kSelStages = 3;            // tiles in flight per CTA
+constexpr int kSelMaxCols = 7;
+constexpr int kSelStageBytes = kSelMaxCols * kSelTile * 8 + kSelTile / 8;  // columns + validity words
+constexpr int kSelCollectSmem = kSelStages * kSelStageBytes +
+                                (kSelConsumers / 32) * kSelWarpStage * static_cast<int>(sizeof(SelRec)) + 64;
 
 __device__ __forceinline__ void warp_flush(SelRec* st, int& n, SelCtl* ctl, SelRec* rec) {
     const int lane = threadIdx.x & 31;
@@ -350,108 +402,117 @@ __device__ __forceinline__ void warp_flush(SelRec* st, int& n, SelCtl* ctl, SelR
     n = 0;
 }
 
-// Warp tile t covers pairs [t * 32 * U, +32 * U): 16-byte column loads, U per lane
-// and column in flight; then, in one batch, the created_at / id loads of the
-// slots whose primary key is at or below the bound's (one extra latency per
-// tile, not one per slot).
-__global__ void __launch_bounds__(kSelCollectThreads, 4) sel_collect_kernel(const EvictCols c, int policy, double now,
-                                                                          int slot_tie, SelCtl* ctl, SelRec* rec) {
-    extern __shared__ uint64_t sel_smem[];
-    constexpr int U = kSelCollectU;
+// The columns a policy's key needs, then size_tokens and created_at.
+struct SelColumns {
+    const void* col[kSelMaxCols];
+    int ncol;
+};
+
+// Persistent CTAs: a producer warp streams 1024-slot tiles of the key
+// columns and the validity words into a 3-stage shared-memory ring with 1-D
+// bulk copies (TMA engine; `full` mbarriers complete on the bytes, `empty`
+// mbarriers collect one arrival per consumer warp), so the bytes in flight do
+// not depend on registers and no block-wide barrier couples the warps.  Each
+// consumer thread takes two slots per tile; records go to per-warp smem
+// slices (warp-aggregated), flushed with one global reservation each.
+__global__ void __launch_bounds__(kSelCollectThreads, 1) sel_collect_kernel(const EvictCols c, const SelColumns cols,
+                                                                           int policy, double now, int slot_tie,
+                                                                           SelCtl* ctl, SelRec* rec) {
+    extern __shared__ __align__(128) uint64_t sel_smem[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sel_smem);  // [stage]{[col][tile] f64, [tile/32] u32}
+    SelRec* wst = reinterpret_cast<SelRec*>(ring + kSelStages * kSelStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(wst + (kSelConsumers / 32) * kSelWarpStage);
+    uint64_t* empty = full + kSelStages;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    SelRec* st = reinterpret_cast<SelRec*>(sel_smem) + warp * kSelWarpStage;
+    const int nc = cols.ncol;
+    const int64_t ntiles = (c.nslots + kSelTile - 1) / kSelTile;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kSelStages; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, kSelConsumers / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kSelConsumers / 32) {  // producer
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int stg = it % kSelStages;
+                if (it >= kSelStages) mbar_wait(empty + stg, static_cast<uint32_t>(((it / kSelStages) - 1) & 1));
+                const int64_t s0 = t * kSelTile;
+                const int64_t n = c.nslots - s0 < kSelTile ? c.nslots - s0 : kSelTile;
+                const int64_t nr = (n + 127) / 128 * 128;  // capacity is a multiple of 128 slots
+                const uint32_t bytes = static_cast<uint32_t>(nr) * 8u, vbytes = static_cast<uint32_t>(nr / 8);
+                uint8_t* base = ring + stg * kSelStageBytes;
+                mbar_arrive_expect_tx(full + stg, bytes * nc + vbytes);
+                for (int k = 0; k < nc; ++k)
+                    bulk_g2s(base + k * kSelTile * 8, static_cast<const double*>(cols.col[k]) + s0, bytes, full + stg,
+                             pol);
+                bulk_g2s(base + kSelMaxCols * kSelTile * 8, c.valid + s0 / 32, vbytes, full + stg, pol);
+            }
+        }
+        return;
+    }
+    SelRec* st = wst + warp * kSelWarpStage;
     int nst = 0;
     const int all = ctl->all;
     const uint64_t hi[3] = {ctl->hi[0], ctl->hi[1], ctl->hi[2]};
-    const int64_t npairs = c.nslots >> 1;
-    const int64_t ntiles = (npairs + 1 + 32 * U - 1) / (32 * U);  // + 1: the odd tail slot
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kSelCollectThreads / 32);
     unsigned long long wl = 0;
     uint64_t ra[3] = {~0ull, ~0ull, ~0ull}, ro[3] = {0, 0, 0};
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(kSelCollectThreads / 32) + warp; t < ntiles; t += nwarps) {
-        uint64_t key[U][2];
-        int64_t sz[U][2];
-        bool act[U][2];
-        int64_t s0[U];
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int stg = it % kSelStages;
+        mbar_wait(full + stg, static_cast<uint32_t>((it / kSelStages) & 1));
+        const double* S = reinterpret_cast<const double*>(ring + stg * kSelStageBytes);
+        const uint32_t* V = reinterpret_cast<const uint32_t*>(ring + stg * kSelStageBytes + kSelMaxCols * kSelTile * 8);
+        const int64_t s0 = t * kSelTile;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t p = t * 32 * U + u * 32 + lane;
-            s0[u] = 2 * p;
-            const bool in = p < npairs;
-            const uint32_t vw = in ? __ldg(c.valid + (s0[u] >> 5)) : 0u;
-            act[u][0] = (vw >> (s0[u] & 31)) & 1u;
-            act[u][1] = (vw >> ((s0[u] + 1) & 31)) & 1u;
-            const longlong2 z = in ? __ldg(reinterpret_cast<const longlong2*>(c.size) + p) : make_longlong2(0, 0);
-            sz[u][0] = z.x, sz[u][1] = z.y;
+        for (int q = 0; q < kSelTile / kSelConsumers; ++q) {
+            const int j = q * kSelConsumers + threadIdx.x;
+            const int64_t s = s0 + j;
+            const bool act = s < c.nslots && ((V[j >> 5] >> (j & 31)) & 1u);
+            uint64_t k0;
+            int64_t size;
+            double created;
             if (policy == 0) {
-                const double2 zero = make_double2(0.0, 0.0);
-                const double2 lf = in ? __ldg(reinterpret_cast<const double2*>(c.lf) + p) : zero;
-                const double2 lc = in ? __ldg(reinterpret_cast<const double2*>(c.lc) + p) : zero;
-                const double2 ll = in ? __ldg(reinterpret_cast<const double2*>(c.ll) + p) : zero;
-                const double2 ls = in ? __ldg(reinterpret_cast<const double2*>(c.ls) + p) : zero;
-                const double2 ex = in ? __ldg(reinterpret_cast<const double2*>(c.expiration) + p) : zero;
-                // cal_score (engine.py:33-48): exact order, no FMA contraction
-                double v0 = 0.0, v1 = 0.0;
-                if (z.x != 0 && !(__dsub_rn(ex.x, now) <= 0.0))
-                    v0 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(lf.x, lc.x), ll.x), ls.x), static_cast<double>(z.x));
-                if (z.y != 0 && !(__dsub_rn(ex.y, now) <= 0.0))
-                    v1 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(lf.y, lc.y), ll.y), ls.y), static_cast<double>(z.y));
-                key[u][0] = f64_key(v0), key[u][1] = f64_key(v1);
-            } else if (policy == 1) {
-                const double2 la = in ? __ldg(reinterpret_cast<const double2*>(c.last_access) + p)
-                                      : make_double2(0.0, 0.0);
-                key[u][0] = f64_key(la.x), key[u][1] = f64_key(la.y);
+                size = __double_as_longlong(S[5 * kSelTile + j]);
+                created = S[6 * kSelTile + j];
+                double v = 0.0;  // cal_score (engine.py:33-48): exact order, no FMA contraction
+                if (size != 0 && !(__dsub_rn(S[4 * kSelTile + j], now) <= 0.0))
+                    v = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(S[j], S[kSelTile + j]), S[2 * kSelTile + j]),
+                                            S[3 * kSelTile + j]),
+                                  static_cast<double>(size));
+                k0 = f64_key(v);
             } else {
-                const longlong2 fq = in ? __ldg(reinterpret_cast<const longlong2*>(c.freq) + p) : make_longlong2(0, 0);
-                key[u][0] = i64_key(fq.x), key[u][1] = i64_key(fq.y);
+                size = __double_as_longlong(S[kSelTile + j]);
+                created = S[2 * kSelTile + j];
+                k0 = policy == 1 ? f64_key(S[j]) : i64_key(__double_as_longlong(S[j]));
             }
-            if (p == npairs && (c.nslots & 1)) {  // the odd tail slot
-                const int64_t s = c.nslots - 1;
-                s0[u] = s;
-                act[u][0] = valid_bit(c.valid, s);
-                act[u][1] = false;
-                sz[u][0] = act[u][0] ? c.size[s] : 0;
-                key[u][0] = act[u][0] ? primary_key(c, s, policy, now) : 0ull;
-            }
-        }
-        // candidates: primary key at or below the bound's (or every slot)
-        uint64_t k1[U][2], k2[U][2];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                act[u][e] = act[u][e] && (all || key[u][e] <= hi[0]);
-                const int64_t s = s0[u] + e;
-                k1[u][e] = act[u][e] ? f64_key(__ldg(c.created + s)) : 0ull;
-                k2[u][e] = act[u][e] ? (slot_tie ? static_cast<uint64_t>(s) : i64_key(__ldg(c.ids + s))) : 0ull;
-            }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                bool take = act[u][e];
-                if (take && !all && key[u][e] == hi[0])
-                    take = k1[u][e] != hi[1] ? k1[u][e] < hi[1] : k2[u][e] <= hi[2];
-                const uint32_t m = __ballot_sync(0xffffffffu, take);
-                if (!m) continue;
+            const uint64_t k1 = f64_key(created);
+            bool take = act && (all || k0 <= hi[0]);
+            uint64_t k2 = slot_tie ? static_cast<uint64_t>(s) : 0ull;
+            if (take && !slot_tie) k2 = i64_key(__ldg(c.ids + s));
+            if (take && !all && k0 == hi[0]) take = k1 != hi[1] ? k1 < hi[1] : k2 <= hi[2];
+            const uint32_t m = __ballot_sync(0xffffffffu, take);
+            if (m) {
                 if (nst + __popc(m) > kSelWarpStage) warp_flush(st, nst, ctl, rec);
                 if (take) {
-                    wl += static_cast<unsigned long long>(sz[u][e]);
+                    wl += static_cast<unsigned long long>(size);
                     SelRec r;
-                    r.k0 = key[u][e];
-                    r.k1 = k1[u][e];
-                    r.k2 = k2[u][e];
-                    r.size = sz[u][e];
-                    ra[0] &= r.k0, ra[1] &= r.k1, ra[2] &= r.k2;
-                    ro[0] |= r.k0, ro[1] |= r.k1, ro[2] |= r.k2;
+                    r.k0 = k0, r.k1 = k1, r.k2 = k2, r.size = size;
+                    ra[0] &= k0, ra[1] &= k1, ra[2] &= k2;
+                    ro[0] |= k0, ro[1] |= k1, ro[2] |= k2;
                     st[nst + __popc(m & ((1u << lane) - 1u))] = r;
                 }
                 nst += __popc(m);
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + stg);  // this warp is done with the stage
     }
     warp_flush(st, nst, ctl, rec);
-    // per-warp reductions straight to the control block
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
 #pragma unroll
@@ -514,9 +575,10 @@ __global__ void __launch_bounds__(1024) sel_split_kernel(int64_t excess, SelCtl*
         keys[j] = rec_win32(rec[((2 * static_cast<int64_t>(i) + 1) * M) / (2 * kSelSplitSample)], a, o);
     }
     SplitSort(ts).Sort(keys);
-    // buckets of ~cap/3 records on average (the sampling spread stays below cap)
+    // buckets of ~1024 records on average; with 4 samples per bucket the
+    // largest of 1024 buckets stays well below the 8192 cap
     int nb = 2;
-    while (nb < kSelMaxBuckets && nb < kSelSplitSample / 4 && static_cast<int64_t>(nb) * (cap / 3) < M) nb <<= 1;
+    while (nb < kSelMaxBuckets && nb < kSelSplitSample / 4 && static_cast<int64_t>(nb) * 1024 < M) nb <<= 1;
     const int os = kSelSplitSample / nb;
 #pragma unroll
     for (int j = 0; j < per; ++j) {
@@ -563,7 +625,7 @@ __device__ __forceinline__ void cta_range(int64_t M, int64_t& b, int64_t& e) {
     e = i64min(M, b + per);
 }
 
-__global__ void __launch_bounds__(1024) sel_bucket_kernel(const SelCtl* ctl, const SelRec* rec, const uint32_t* spl,
+__global__ void __launch_bounds__(1024) sel_bucket_kernel(SelCtl* ctl, const SelRec* rec, const uint32_t* spl,
                                                          const uint32_t* tab, uint16_t* bid,
                                                          unsigned long long* bcnt, unsigned long long* bw) {
     extern __shared__ uint64_t sel_smem[];
@@ -581,14 +643,29 @@ __global__ void __launch_bounds__(1024) sel_bucket_kernel(const SelCtl* ctl, con
     __syncthreads();
     uint64_t a[3], o[3];
     ctl_and_or(ctl, a, o);
+    const int pg = first_varying(a, o);
     int64_t b, e;
     cta_range(static_cast<int64_t>(ctl->count), b, e);
+    uint64_t wmn = ~0ull, wmx = 0ull;
     for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
         const SelRec r = rec[i];
-        const int k = ns ? find_bucket(rec_win32(r, a, o), S, T) : 0;
+        const uint64_t w64 = key_window_at(r.k0, r.k1, r.k2, pg);
+        wmn = w64 < wmn ? w64 : wmn;
+        wmx = w64 > wmx ? w64 : wmx;
+        const int k = ns ? find_bucket(static_cast<uint32_t>(w64 >> 32), S, T) : 0;
         bid[i] = static_cast<uint16_t>(k);
         atomicAdd(&sc[k], 1u);
         smem_add64(&swl[k], &swh[k], static_cast<uint64_t>(r.size));
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const uint64_t x = __shfl_xor_sync(0xffffffffu, wmn, d), y = __shfl_xor_sync(0xffffffffu, wmx, d);
+        wmn = x < wmn ? x : wmn;
+        wmx = y > wmx ? y : wmx;
+    }
+    if ((threadIdx.x & 31) == 0 && wmn <= wmx) {
+        atomicMin(&ctl->wmin, static_cast<unsigned long long>(wmn));
+        atomicMax(&ctl->wmax, static_cast<unsigned long long>(wmx));
     }
     __syncthreads();
     for (int j = threadIdx.x; j < nb; j += blockDim.x) {
@@ -838,139 +915,116 @@ __device__ __forceinline__ bool bucket_emit(GetRec get, const uint16_t (&idx)[IP
     return first < n;
 }
 
-// ------------------------------------------------ 7 bucket sort (window)
-// Per bucket: the top 20 of the 32 bits from the bucket's first varying bit
-// are block-radix-sorted (5 passes of 4 bits); records whose 20-bit windows
-// tie form short runs that one thread orders by full key (insertion sort).
-// Runs longer than kSelRunMax (heavy ties: e.g. equal primary keys and
-// equal created_at) send the bucket to the full-key kernel (sel_big_kernel).
-constexpr int kSelWinBits = 20;
-constexpr int kSelRunMax = 64;
+// ------------------------------------------------ 7 bucket sort (counting)
+// Per bucket: each record's 64-bit window (from the records' first varying
+// bit) minus the bucket's lower bound, scaled so the bucket's range fills 44
+// bits, splits into a 12-bit bin and a 32-bit sub-key.  Records are counted
+// into the 4096 bins and scattered in bin order; bins holding several
+// records (~1 record per 4 bins on average) are ordered by sub-key from
+// smem by one thread each (insertion sort), and only equal sub-keys compare
+// full keys.  Runs longer than kSelRunMax (a bucket whose records pile into
+// one bin) go to the full-key kernel (sel_big_kernel).
+constexpr int kSelBins = 4096;
+constexpr int kSelRunMax = 128;
 
-template <int IPT>
-using WinSort = cub::BlockRadixSort<uint32_t, kSelSortThreads, IPT, uint16_t, 4>;
-
-union WinSortStorage {
-    typename WinSort<2>::TempStorage s2;
-    typename WinSort<4>::TempStorage s4;
-    typename WinSort<8>::TempStorage s8;
-};
-
-struct WinShared {
-    WinSortStorage sort;
-    uint32_t skey[kSelCap];
-    uint16_t sidx[kSelCap];
-    unsigned long long sa[3], so[3];
+struct CountShared {
+    uint32_t hist[kSelBins];
+    uint32_t ssub[kSelCap];  // sub-key at rank r
+    uint16_t sidx[kSelCap];  // record at rank r
+    uint16_t sbin[kSelCap];  // bin at rank r
     int64_t wtot[32];
     int64_t total;
     int first;
     int tie;
 };
 
-constexpr int kSelWinSmem = static_cast<int>(sizeof(WinShared));
+constexpr int kSelCountSmem = static_cast<int>(sizeof(CountShared));
+
+__device__ __forceinline__ uint64_t bucket_offset(const SelRec& r, int pg, uint64_t lo64, int shift) {
+    const uint64_t off = (key_window_at(r.k0, r.k1, r.k2, pg) - lo64) >> shift;
+    return off < (1ull << 44) ? off : (1ull << 44) - 1;
+}
 
 template <int IPT>
-__device__ __forceinline__ bool win_sort_emit(const SelRec* src, int n, int64_t base, bool cut, int64_t wbase,
-                                              int64_t excess, int slot_tie, const int64_t* ids, int64_t* out,
-                                              SelCtl* ctl, WinShared& sh) {
-    uint64_t a[3] = {~0ull, ~0ull, ~0ull}, o[3] = {0, 0, 0};
-    if (threadIdx.x < 3) sh.sa[threadIdx.x] = ~0ull, sh.so[threadIdx.x] = 0ull;
+__device__ __forceinline__ bool count_sort_emit(const SelRec* src, int n, int pg, uint64_t lo64, int shift,
+                                                int64_t base, bool cut, int64_t wbase, int64_t excess, int slot_tie,
+                                                const int64_t* ids, int64_t* out, SelCtl* ctl, CountShared& sh) {
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) sh.hist[i] = 0;
     if (threadIdx.x == 0) sh.tie = 0;
     __syncthreads();
-    uint32_t keys[IPT];
-    uint16_t idx[IPT];
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        atomicAdd(&sh.hist[bucket_offset(src[i], pg, lo64, shift) >> 32], 1u);
+    __syncthreads();
+    {  // exclusive scan of the bins
+        constexpr int per = kSelBins / kSelSortThreads;
+        uint32_t v[per], t = 0;
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const int i = threadIdx.x * IPT + j;
-        if (i < n) {
-            const SelRec r = src[i];
-            a[0] &= r.k0, a[1] &= r.k1, a[2] &= r.k2;
-            o[0] |= r.k0, o[1] |= r.k1, o[2] |= r.k2;
+        for (int q = 0; q < per; ++q) t += (v[q] = sh.hist[per * threadIdx.x + q]);
+        int64_t run = block_excl_scan(static_cast<int64_t>(t), sh.wtot, &sh.total);
+#pragma unroll
+        for (int q = 0; q < per; ++q) {
+            sh.hist[per * threadIdx.x + q] = static_cast<uint32_t>(run);
+            run += v[q];
         }
     }
-    block_and_or3(a, o, sh.sa, sh.so);
-    int span = 0;  // bits from the first varying bit to the last
-    {
-        int p = 192, q = -1;
-#pragma unroll
-        for (int w = 2; w >= 0; --w)
-            if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
-#pragma unroll
-        for (int w = 0; w < 3; ++w)
-            if (a[w] ^ o[w]) q = 64 * w + 64 - __ffsll(static_cast<long long>(a[w] ^ o[w]));
-        span = q >= p ? q - p + 1 : 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t o = bucket_offset(src[i], pg, lo64, shift);  // second read: L1
+        const uint32_t k = static_cast<uint32_t>(o >> 32);
+        const uint32_t at = atomicAdd(&sh.hist[k], 1u);
+        sh.sidx[at] = static_cast<uint16_t>(i);
+        sh.sbin[at] = static_cast<uint16_t>(k);
+        sh.ssub[at] = static_cast<uint32_t>(o);
     }
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const int i = threadIdx.x * IPT + j;
-        idx[j] = i < n ? static_cast<uint16_t>(i) : static_cast<uint16_t>(0xffff);
-        keys[j] = 0xffffffffu;
-        if (i < n) {
-            const SelRec r = src[i];  // second read: L1 / L2
-            keys[j] = static_cast<uint32_t>(key_window(r.k0, r.k1, r.k2, a, o) >> 32);
-        }
-    }
-    // bits below the span are constant; below the top 20, ties are resolved
-    // by full key afterwards
-    const int lo_bit = span >= kSelWinBits ? 32 - kSelWinBits : 32 - span;
-    if constexpr (IPT == 2)
-        WinSort<2>(sh.sort.s2).Sort(keys, idx, lo_bit, 32);
-    else if constexpr (IPT == 4)
-        WinSort<4>(sh.sort.s4).Sort(keys, idx, lo_bit, 32);
-    else
-        WinSort<8>(sh.sort.s8).Sort(keys, idx, lo_bit, 32);
-    if (span > kSelWinBits) {  // windows may tie: order each run of equal windows by full key
-        const uint32_t msk = ~((1u << lo_bit) - 1u);
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const int r = threadIdx.x * IPT + j;
-            if (r < n) sh.skey[r] = keys[j] & msk, sh.sidx[r] = idx[j];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const int r = threadIdx.x * IPT + j;
-            if (r + 1 < n && (r == 0 || sh.skey[r - 1] != sh.skey[r]) && sh.skey[r + 1] == sh.skey[r]) {
-                int e = r + 2;
-                while (e < n && sh.skey[e] == sh.skey[r] && e - r <= kSelRunMax) ++e;
-                if (e - r > kSelRunMax) {
-                    sh.tie = 1;
-                } else {
-                    for (int x = r + 1; x < e; ++x) {  // insertion sort by full key
-                        const uint16_t v = sh.sidx[x];
-                        const SelRec rv = src[v];
-                        int y = x - 1;
-                        while (y >= r && rec_less(rv, src[sh.sidx[y]])) {
-                            sh.sidx[y + 1] = sh.sidx[y];
-                            --y;
-                        }
-                        sh.sidx[y + 1] = v;
+    __syncthreads();
+    for (int r = threadIdx.x; r + 1 < n; r += blockDim.x) {
+        if ((r == 0 || sh.sbin[r - 1] != sh.sbin[r]) && sh.sbin[r + 1] == sh.sbin[r]) {
+            int e = r + 2;
+            while (e < n && sh.sbin[e] == sh.sbin[r] && e - r <= kSelRunMax) ++e;
+            if (e - r > kSelRunMax) {
+                sh.tie = 1;
+            } else {
+                for (int x = r + 1; x < e; ++x) {  // insertion sort by (sub-key, full key)
+                    const uint16_t v = sh.sidx[x];
+                    const uint32_t kv = sh.ssub[x];
+                    int y = x - 1;
+                    while (y >= r && (sh.ssub[y] > kv || (sh.ssub[y] == kv && rec_less(src[v], src[sh.sidx[y]])))) {
+                        sh.sidx[y + 1] = sh.sidx[y];
+                        sh.ssub[y + 1] = sh.ssub[y];
+                        --y;
                     }
+                    sh.sidx[y + 1] = v;
+                    sh.ssub[y + 1] = kv;
                 }
             }
         }
-        __syncthreads();
-        if (sh.tie) return false;
+    }
+    __syncthreads();
+    if (sh.tie) return false;
+    uint16_t idx[IPT];
 #pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const int r = threadIdx.x * IPT + j;
-            if (r < n) idx[j] = sh.sidx[r];
-        }
+    for (int j = 0; j < IPT; ++j) {
+        const int r = threadIdx.x * IPT + j;
+        idx[j] = r < n ? sh.sidx[r] : static_cast<uint16_t>(0);
     }
     bucket_emit<IPT>([&](int i) { return src[i]; }, idx, n, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
     return true;
 }
 
-__global__ void __launch_bounds__(kSelSortThreads, 2) sel_sort_kernel(SelCtl* ctl, int64_t excess, int slot_tie,
-                                                                     const int64_t* ids, const SelRec* rec2,
-                                                                     const int64_t* boff,
-                                                                     const unsigned long long* bcnt, int32_t* big,
-                                                                     int64_t* out, int cap) {
+__global__ void __launch_bounds__(kSelSortThreads) sel_sort_kernel(SelCtl* ctl, int64_t excess, int slot_tie,
+                                                                  const int64_t* ids, const uint32_t* spl,
+                                                                  const SelRec* rec2, const int64_t* boff,
+                                                                  const unsigned long long* bcnt, int32_t* big,
+                                                                  int64_t* out, int cap) {
     extern __shared__ uint64_t sel_smem[];
-    WinShared& sh = *reinterpret_cast<WinShared*>(sel_smem);
+    CountShared& sh = *reinterpret_cast<CountShared*>(sel_smem);
     if (ctl->retry) return;
-    const int cutb = ctl->cutb;
+    const int cutb = ctl->cutb, nb = ctl->nb;
     const int64_t wbase = ctl->wbase;
+    uint64_t ga[3], go[3];
+    ctl_and_or(ctl, ga, go);
+    const int pg = first_varying(ga, go);
+    const uint64_t wmin = ctl->wmin, wmax = ctl->wmax;
     for (int b = blockIdx.x; b <= cutb; b += gridDim.x) {
         const int64_t n = static_cast<int64_t>(bcnt[b]);
         const int64_t base = boff[b];
@@ -980,15 +1034,22 @@ __global__ void __launch_bounds__(kSelSortThreads, 2) sel_sort_kernel(SelCtl* ct
         }
         bool ok = false;
         if (n <= cap) {
-            const SelRec* src = rec2 + base;
-            const int m = static_cast<int>(n);
-            const bool cut = b == cutb;
-            if (m <= 2 * kSelSortThreads)
-                ok = win_sort_emit<2>(src, m, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
-            else if (m <= 4 * kSelSortThreads)
-                ok = win_sort_emit<4>(src, m, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+            // the bucket's 64-bit windows lie in [wlo << 32, whi << 32 | ~0],
+            // clipped to the records' own range (the end buckets are open)
+            uint64_t lo64 = b == 0 ? 0ull : static_cast<uint64_t>(spl[b - 1] + 1u) << 32;
+            uint64_t hi64 = b == nb - 1 ? ~0ull : (static_cast<uint64_t>(spl[b]) << 32) | 0xffffffffull;
+            lo64 = lo64 > wmin ? lo64 : wmin;
+            hi64 = hi64 < wmax ? hi64 : wmax;
+            if (hi64 < lo64) hi64 = lo64;
+            const uint64_t width = hi64 - lo64;
+            const int bits = width ? 64 - __clzll(width) : 0;
+            const int shift = bits > 44 ? bits - 44 : 0;
+            if (n <= 4 * kSelSortThreads)
+                ok = count_sort_emit<4>(rec2 + base, static_cast<int>(n), pg, lo64, shift, base, b == cutb, wbase,
+                                        excess, slot_tie, ids, out, ctl, sh);
             else
-                ok = win_sort_emit<8>(src, m, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+                ok = count_sort_emit<12>(rec2 + base, static_cast<int>(n), pg, lo64, shift, base, b == cutb, wbase,
+                                         excess, slot_tie, ids, out, ctl, sh);
         }
         if (!ok && threadIdx.x == 0) big[atomicAdd(&ctl->nbig, 1)] = b;
         __syncthreads();

@@ -98,7 +98,7 @@ def test_select_matches_oracle_order(pkg, shuffled, tied):
     live[dead] = False
     now = 20.0
     total = int(m["size"][live].sum())
-    for cap in (4096, 512):
+    for cap in (6144, 512):
         N.check(idx._lib.sine_set_select_cap(idx.handle, cap))
         for policy in ("lcfu", "lru", "lfu"):
             order = _order(policy, ids, m, now, live)
