@@ -522,6 +522,7 @@ def run_ours(args):
         del idx
         torch.cuda.empty_cache()
         eviction = measure_eviction(args.evict_rows, hbm_peak)
+        eviction["engine"] = measure_engine_eviction()
     config_c = None
     if world == 1 and not args.no_config_c:
         import gc
@@ -894,6 +895,75 @@ def measure_eviction(n, hbm_peak, cpu_sample=300_000):
                          "frac": (n * bytes_per_se / (dev_ms / 1e3) / 1e9 / hbm_peak) if dev_ms else None},
             "cpu_baseline": {"value": m / cpu_s, "unit": "SEs/s", "cores": 1, "kind": "port",
                              "sample": f"{m} SEs: oracle evict_until_fits (Python cal_score + tuple sort)"}}
+
+
+def measure_engine_eviction(n=1_000_000, ref_sample=200_000):
+    """Config D through the public engine API: `CacheEngine.evict_until_fits`
+    on n resident SEs at capacity = 0.9 x live usage -- the device TTL purge
+    and victim select + tombstone, plus the reference's host dict
+    bookkeeping for every removed id.  Parity: the removed list equals the
+    oracle's.  CPU baseline: the reference `CacheEngine.evict_until_fits`
+    (oracle/_ref/semcache) on the first ref_sample SEs, its engine and index
+    populated by direct attribute assignment."""
+    import paper_2509_17360_b200 as P
+    from paper_2509_17360_b200 import model as M
+    from oracle import sine_oracle as O
+
+    meta = evict_metadata(n, seed=5)
+    now = 1.0e4
+    shared = M.EmbeddingVector((1.0, 0.0, 0.0, 0.0))
+    els = _make_elements(M, n, meta, shared)
+    eng = P.CacheEngine(P.CacheConfig(capacity_tokens=10 ** 15), _DictEmbedder(4), _TextJudge())
+    rows = np.zeros((n, 4))
+    rows[:, 0] = 1.0
+    ids = eng.bulk_admit(els, embeddings=rows)
+    live = (meta["expiration"] - now) > 0.0
+    cap = int(0.9 * int(meta["size"][live].sum()))
+    eng.config.capacity_tokens = cap
+    t0 = time.perf_counter()
+    removed = eng.evict_until_fits(now)
+    eng_s = time.perf_counter() - t0
+    want = O.evict_until_fits_np(np.asarray(ids), meta["freq"], meta["cost"], meta["lat"], meta["staticity"],
+                                 meta["size"], meta["created"], meta["expiration"], now, cap)
+    parity = bool(np.array_equal(np.asarray(removed), want))
+    n_left = len(eng)
+    del eng, els
+    out = {"workload": f"config D through CacheEngine.evict_until_fits: {n} SEs (1/7 short TTL), capacity = "
+                       f"0.9 x live usage, now={now}",
+           "removed": len(removed), "left": n_left, "ms": eng_s * 1e3, "ses_per_s": n / eng_s,
+           "parity_vs_oracle": parity,
+           "note": "includes the reference's host bookkeeping (element / key / last-access dicts) per removed id"}
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "semcache")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import semcache.engine as RE
+        import semcache.index as RI
+        import semcache.model as RM
+        m = min(ref_sample, n)
+        rmeta = {k: v[:m] for k, v in meta.items()}
+        remb = RM.EmbeddingVector((1.0, 0.0, 0.0, 0.0))
+        rels = _make_elements(RM, m, rmeta, remb)
+        reng = RE.CacheEngine(RM.CacheConfig(capacity_tokens=10 ** 15), _DictEmbedder(4), _TextJudge())
+        idx = RI.ExactCosineIndex(4)
+        idx._ids = list(range(1, m + 1))
+        idx._pos = {i: i - 1 for i in range(1, m + 1)}
+        idx._vecs = rows[:m].copy()
+        reng._index = idx
+        reng._elements = {i + 1: el for i, el in enumerate(rels)}
+        reng._by_key = {(el.key.text, el.key.tool): i + 1 for i, el in enumerate(rels)}
+        reng._last_access = {i + 1: el.created_at for i, el in enumerate(rels)}
+        reng._usage = int(rmeta["size"].sum())
+        reng._next_id = m + 1
+        rlive = (rmeta["expiration"] - now) > 0.0
+        reng.config.capacity_tokens = int(0.9 * int(rmeta["size"][rlive].sum()))
+        t0 = time.perf_counter()
+        rremoved = reng.evict_until_fits(now)
+        ref_s = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": m / ref_s, "unit": "SEs/s", "cores": 1, "kind": "reference",
+                               "sample": f"{m} SEs: semcache.engine.CacheEngine.evict_until_fits (oracle/_ref), "
+                                         f"{len(rremoved)} removed, {ref_s * 1e3:.0f} ms"}
+    return out
 
 
 # ------------------------------------------------- config E: mixed trace

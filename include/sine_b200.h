@@ -162,6 +162,11 @@ int sine_expired(sine_index_t *h, double now, int remove, int64_t *out,
  * size_tokens sum reaches `excess`, in order.  Not removed. */
 int sine_select_victims(sine_index_t *h, int policy, double now, int64_t excess,
                         int64_t *out, int64_t cap, int64_t *n);
+/* sine_select_victims + tombstoning the victims in the same call (the
+ * engine's pop loops at engine.py:321-327, :353-359, which remove what they
+ * select). */
+int sine_evict(sine_index_t *h, int policy, double now, int64_t excess,
+               int64_t *out, int64_t cap, int64_t *n);
 /* Test hook (not in the reference): the number of selection records one CTA
  * sorts in shared memory (2..6144, default 6144).  Lower values drive the
  * merge path for oversized buckets on small stores. */

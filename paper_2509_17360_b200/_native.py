@@ -67,6 +67,8 @@ _SIGS = {
                                     ctypes.c_int64, _i64p]),
     "sine_select_victims": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
                                            _i64p, ctypes.c_int64, _i64p]),
+    "sine_evict": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
+                                           _i64p, ctypes.c_int64, _i64p]),
     "sine_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "sine_set_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "sine_set_select_cap": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

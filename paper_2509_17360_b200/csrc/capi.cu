@@ -169,6 +169,11 @@ struct sine_index {
     // sequence of inserts and removals.
     std::vector<int64_t> order_slot;  // position -> slot
     std::vector<int64_t> order_pos;   // slot -> position (-1 once removed)
+    // pending order ops, replayed only when the order is read (ids(),
+    // snapshots, compaction): s >= 0 removes slot s (swap-last), s < 0
+    // appends slot ~s.  Removal bursts (TTL purge, eviction) then cost one
+    // log entry per row.
+    std::vector<int64_t> order_log;
 
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
@@ -221,6 +226,7 @@ struct sine_index {
     DevBuf<uint32_t> sbcur;
     DevBuf<int32_t> sbig;
     DevBuf<SelCtl> sctl;
+    DevBuf<int64_t> sslot;  // victim slots (sine_evict on slot-ordered stores)
     int sel_cap = kSelCap;  // records sorted in smem per CTA (sine_set_select_cap lowers it in tests)
     HostBuf<SelCtl> sctl_h;
     DevBuf<__nv_bfloat16> qbf;          // umma path: bf16 queries
@@ -497,6 +503,10 @@ void copy_meta(sine_index* h, int64_t s0, int64_t n, const sine_meta_cols_t* m) 
     cp(h->expiration, m->expiration_time), cp(h->last_access, m->last_access);
 }
 
+void order_append(sine_index* h, int64_t slot);
+void order_removed(sine_index* h, int64_t slot);
+void order_flush(sine_index* h);
+
 void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bool rows_on_device,
             const sine_meta_cols_t* meta) {
     grow(h, h->nslots + n);
@@ -517,8 +527,7 @@ void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bo
     CK(cudaGetLastError());
     const bool was_ascending = h->ids_ascending;
     for (int64_t i = 0; i < n; ++i) {
-        h->order_pos.push_back(static_cast<int64_t>(h->order_slot.size()));
-        h->order_slot.push_back(s0 + i);
+        order_append(h, s0 + i);
         h->ids_h.push_back(ids[i]);
         h->live_h.push_back(1);
         if (ids[i] <= h->max_id) h->ids_ascending = false;
@@ -537,6 +546,7 @@ void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bo
 }
 
 void compact(sine_index* h) {
+    order_flush(h);
     std::vector<int64_t> from;
     from.reserve(h->nlive);
     for (int64_t s = 0; s < h->nslots; ++s)
@@ -1418,8 +1428,11 @@ EvictCols evict_cols(const sine_index* h) {
 // Victims are written straight into the caller's buffer (pinned or pageable).
 // Sample select (select.cuh): one pass over the store, then only the
 // records below the sampled bound are bucketed and sorted.
+void remove_slots(sine_index* h, const std::vector<int64_t>& slots, const int64_t* dslots);
+
+// remove: also tombstone the victims (sine_evict).
 void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, int64_t* out, int64_t cap,
-                         int64_t* nout) {
+                         int64_t* nout, bool remove = false) {
     *nout = 0;
     if (!(h->flags & SINE_STORE_META)) fail(SINE_EINVAL, "index has no LCFU metadata (SINE_STORE_META)");
     if (excess <= 0 || h->nlive == 0) return;
@@ -1430,6 +1443,8 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     h->srec2.ensure(nl);
     h->sbid.ensure(nl);
     h->vids.ensure(nl);
+    if (remove && h->ids_ascending) h->sslot.ensure(nl);
+    int64_t* oslot = remove && h->ids_ascending ? h->sslot.p : nullptr;
     h->sspl.ensure(kSelMaxBuckets);
     h->stab.ensure(4100);
     h->sbcnt.ensure(2 * kSelMaxBuckets);
@@ -1478,16 +1493,17 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
                                                                              h->sctl.p, h->srec.p);
         sel_split_kernel<<<1, 1024, 0, st>>>(excess, h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, scap);
         // bucket and scatter must split the records the same way (same grid)
-        const int grec = 2 * h->num_sms;
+        const int grec = h->num_sms;
         sel_bucket_kernel<<<grec, 1024, kSelBucketSmem, st>>>(h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, h->sbid.p,
                                                               bcnt, bw);
         sel_scan_kernel<<<1, 1024, 0, st>>>(h->sctl.p, excess, bcnt, bw, h->sboff.p, h->sbcur.p);
         sel_scatter_kernel<<<grec, 1024, 0, st>>>(h->sctl.p, h->srec.p, h->sbid.p, h->sboff.p, h->sbcur.p,
                                                   h->srec2.p);
         sel_sort_kernel<<<3 * h->num_sms, kSelSortThreads, kSelCountSmem, st>>>(
-            h->sctl.p, excess, slot_tie, h->ids, h->sspl.p, h->srec2.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
+            h->sctl.p, excess, slot_tie, h->ids, h->sspl.p, h->srec2.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap, oslot);
         sel_big_kernel<<<h->num_sms, kSelSortThreads, kSelSortSmem, st>>>(
-            h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->srec.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap);
+            h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->srec.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap,
+            oslot);
         h->launches += 7;
         CK(cudaGetLastError());
         record(h, 4, st);
@@ -1499,9 +1515,19 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     const int64_t V = h->sctl_h.p->V;
     if (V > cap) fail(SINE_EINVAL, "output buffer too small for the victim list");
     CK(cudaMemcpyAsync(out, h->vids.p, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> slots;
+    if (remove && V > 0) {
+        slots.resize(V);
+        if (oslot) CK(cudaMemcpyAsync(slots.data(), oslot, V * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
     *nout = V;
     if (h->timing) CK(cudaEventElapsedTime(&h->t_evict, h->ev[3], h->ev[4]));
+    if (remove && V > 0) {
+        if (!oslot)
+            for (int64_t i = 0; i < V; ++i) slots[i] = find_slot(h, out[i]);
+        remove_slots(h, slots, oslot);
+    }
 }
 
 bool certify_in_flight(const sine_index* h) {
@@ -1540,6 +1566,37 @@ void maybe_compact(sine_index* h) {
 
 // ExactCosineIndex.remove's bookkeeping (index.py:80-92): the last id moves
 // into the removed id's position.
+void order_remove(sine_index* h, int64_t slot);
+
+void order_flush(sine_index* h) {
+    for (const int64_t op : h->order_log) {
+        if (op >= 0) {
+            order_remove(h, op);
+        } else {
+            const int64_t s = ~op;
+            if (static_cast<int64_t>(h->order_pos.size()) <= s) h->order_pos.resize(s + 1, -1);
+            h->order_pos[s] = static_cast<int64_t>(h->order_slot.size());
+            h->order_slot.push_back(s);
+        }
+    }
+    h->order_log.clear();
+}
+
+void order_append(sine_index* h, int64_t slot) {
+    if (h->order_log.empty()) {
+        if (static_cast<int64_t>(h->order_pos.size()) <= slot) h->order_pos.resize(slot + 1, -1);
+        h->order_pos[slot] = static_cast<int64_t>(h->order_slot.size());
+        h->order_slot.push_back(slot);
+    } else {
+        h->order_log.push_back(~slot);
+    }
+}
+
+void order_removed(sine_index* h, int64_t slot) {
+    h->order_log.push_back(slot);
+    if (static_cast<int64_t>(h->order_log.size()) > 2 * (h->nslots + 1024)) order_flush(h);
+}
+
 void order_remove(sine_index* h, int64_t slot) {
     const int64_t p = h->order_pos[slot];
     const int64_t last = h->order_slot.back();
@@ -1552,13 +1609,17 @@ void order_remove(sine_index* h, int64_t slot) {
 }
 
 // slots removed in the given order (the caller's removal sequence)
-void remove_slots(sine_index* h, const std::vector<int64_t>& slots) {
+// Tombstone `slots` (device copy `dslots` when the caller already has one).
+void remove_slots(sine_index* h, const std::vector<int64_t>& slots, const int64_t* dslots = nullptr) {
     if (slots.empty()) return;
     DevBuf<int64_t> d;
-    d.ensure(slots.size());
     snapshot_bitmap_for_tickets(h);
-    CK(cudaMemcpyAsync(d.p, slots.data(), slots.size() * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
-    set_bits_kernel<<<grid_for(slots.size(), 256, h->num_sms), 256, 0, h->stream>>>(h->valid, d.p, slots.size(), 0);
+    if (!dslots) {
+        d.ensure(slots.size());
+        CK(cudaMemcpyAsync(d.p, slots.data(), slots.size() * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+        dslots = d.p;
+    }
+    set_bits_kernel<<<grid_for(slots.size(), 256, h->num_sms), 256, 0, h->stream>>>(h->valid, dslots, slots.size(), 0);
     ++h->launches;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
@@ -1566,7 +1627,7 @@ void remove_slots(sine_index* h, const std::vector<int64_t>& slots) {
     for (int64_t s : slots) {
         if (!h->ids_ascending) h->pos.erase(h->ids_h[s]);
         h->live_h[s] = 0;
-        order_remove(h, s);
+        order_removed(h, s);
     }
     h->nlive -= static_cast<int64_t>(slots.size());
     maybe_compact(h);
@@ -1720,6 +1781,7 @@ int sine_size(sine_index_t* h, int64_t* live, int64_t* slots) {
 int sine_ids(sine_index_t* h, int64_t* out, int64_t cap, int64_t* n) {
     return guarded([&] {
         std::lock_guard<std::mutex> g(h->mu);
+        order_flush(h);
         const int64_t m = static_cast<int64_t>(h->order_slot.size());
         for (int64_t j = 0; j < std::min(m, cap); ++j) out[j] = h->ids_h[h->order_slot[j]];
         *n = m;
@@ -1746,6 +1808,7 @@ int sine_snapshot(sine_index_t* h, int64_t cap, int64_t* ids, double* rows, int6
         std::lock_guard<std::mutex> g(h->mu);
         CK(cudaSetDevice(h->device));
         ws_acquire(h, h->stream);
+        order_flush(h);
         const int64_t m = static_cast<int64_t>(h->order_slot.size());
         *n = m;
         if (m > cap) fail(SINE_EINVAL, "snapshot buffers hold " + std::to_string(cap) + " rows, need " +
@@ -2102,7 +2165,7 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
             for (int32_t sl : by_id) {
                 if (!h->ids_ascending) h->pos.erase(h->ids_h[sl]);
                 h->live_h[sl] = 0;
-                order_remove(h, sl);
+                order_removed(h, sl);
             }
             h->nlive -= total;
             maybe_compact(h);
@@ -2123,6 +2186,16 @@ int sine_select_victims(sine_index_t* h, int policy, double now, int64_t excess,
 
 int sine_stream(sine_index_t* h, void** stream) {
     return guarded([&] { *stream = h->stream; });
+}
+
+int sine_evict(sine_index_t* h, int policy, double now, int64_t excess, int64_t* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        if (policy < 0 || policy > 2) fail(SINE_EINVAL, "unknown eviction policy");
+        std::lock_guard<std::mutex> g(h->mu);
+        CK(cudaSetDevice(h->device));
+        ws_acquire(h, h->stream);
+        select_victims_impl(h, policy, now, excess, out, cap, n, true);
+    });
 }
 
 int sine_set_select_cap(sine_index_t* h, int cap) {

@@ -881,7 +881,7 @@ __device__ __forceinline__ void bucket_sort(const SelRec* src, int n, BucketShar
 template <int IPT, typename GetRec, typename Sh>
 __device__ __forceinline__ bool bucket_emit(GetRec get, const uint16_t (&idx)[IPT], int n, int64_t base, bool cut,
                                             int64_t wbase, int64_t excess, int slot_tie, const int64_t* ids,
-                                            int64_t* out, SelCtl* ctl, Sh& sh) {
+                                            int64_t* out, SelCtl* ctl, Sh& sh, int64_t* oslot = nullptr) {
     int64_t sz[IPT];
     int64_t loc = 0;
 #pragma unroll
@@ -891,6 +891,7 @@ __device__ __forceinline__ bool bucket_emit(GetRec get, const uint16_t (&idx)[IP
         if (rk < n) {
             const SelRec r = get(idx[j]);
             out[base + rk] = rec_id(r, slot_tie, ids);
+            if (oslot) oslot[base + rk] = static_cast<int64_t>(r.k2);  // slot-ordered stores only
             loc += (sz[j] = r.size);
         }
     }
@@ -948,7 +949,8 @@ __device__ __forceinline__ uint64_t bucket_offset(const SelRec& r, int pg, uint6
 template <int IPT>
 __device__ __forceinline__ bool count_sort_emit(const SelRec* src, int n, int pg, uint64_t lo64, int shift,
                                                 int64_t base, bool cut, int64_t wbase, int64_t excess, int slot_tie,
-                                                const int64_t* ids, int64_t* out, SelCtl* ctl, CountShared& sh) {
+                                                const int64_t* ids, int64_t* out, SelCtl* ctl, CountShared& sh,
+                                                int64_t* oslot) {
     for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) sh.hist[i] = 0;
     if (threadIdx.x == 0) sh.tie = 0;
     __syncthreads();
@@ -1007,7 +1009,8 @@ __device__ __forceinline__ bool count_sort_emit(const SelRec* src, int n, int pg
         const int r = threadIdx.x * IPT + j;
         idx[j] = r < n ? sh.sidx[r] : static_cast<uint16_t>(0);
     }
-    bucket_emit<IPT>([&](int i) { return src[i]; }, idx, n, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh);
+    bucket_emit<IPT>([&](int i) { return src[i]; }, idx, n, base, cut, wbase, excess, slot_tie, ids, out, ctl, sh,
+                     oslot);
     return true;
 }
 
@@ -1015,7 +1018,7 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_sort_kernel(SelCtl* ctl, 
                                                                   const int64_t* ids, const uint32_t* spl,
                                                                   const SelRec* rec2, const int64_t* boff,
                                                                   const unsigned long long* bcnt, int32_t* big,
-                                                                  int64_t* out, int cap) {
+                                                                  int64_t* out, int cap, int64_t* oslot) {
     extern __shared__ uint64_t sel_smem[];
     CountShared& sh = *reinterpret_cast<CountShared*>(sel_smem);
     if (ctl->retry) return;
@@ -1046,10 +1049,10 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_sort_kernel(SelCtl* ctl, 
             const int shift = bits > 44 ? bits - 44 : 0;
             if (n <= 4 * kSelSortThreads)
                 ok = count_sort_emit<4>(rec2 + base, static_cast<int>(n), pg, lo64, shift, base, b == cutb, wbase,
-                                        excess, slot_tie, ids, out, ctl, sh);
+                                        excess, slot_tie, ids, out, ctl, sh, oslot);
             else
                 ok = count_sort_emit<12>(rec2 + base, static_cast<int>(n), pg, lo64, shift, base, b == cutb, wbase,
-                                         excess, slot_tie, ids, out, ctl, sh);
+                                         excess, slot_tie, ids, out, ctl, sh, oslot);
         }
         if (!ok && threadIdx.x == 0) big[atomicAdd(&ctl->nbig, 1)] = b;
         __syncthreads();
@@ -1065,7 +1068,8 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_big_kernel(SelCtl* ctl, i
                                                                  const int64_t* ids, SelRec* rec2, SelRec* tmp,
                                                                  const int64_t* boff,
                                                                  const unsigned long long* bcnt,
-                                                                 const int32_t* big, int64_t* out, int cap) {
+                                                                 const int32_t* big, int64_t* out, int cap,
+                                                                 int64_t* oslot) {
     extern __shared__ uint64_t sel_smem[];
     BucketShared& sh = *reinterpret_cast<BucketShared*>(sel_smem);
     if (ctl->retry) return;
@@ -1128,7 +1132,7 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_big_kernel(SelCtl* ctl, i
             for (int j = 0; j < 8; ++j) idx[j] = static_cast<uint16_t>(threadIdx.x * 8 + j);
             const SelRec* chunk = src + c0;
             const bool found = bucket_emit<8>([&](int i) { return chunk[i]; }, idx, m, base + c0, b == cutb, wb,
-                                              excess, slot_tie, ids, out, ctl, sh);
+                                              excess, slot_tie, ids, out, ctl, sh, oslot);
             if (b == cutb) {
                 if (found) break;
                 wb += sh.total;
