@@ -382,12 +382,13 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
 // Each warp stages its records in its own smem slice and flushes them with
 // one global reservation when the slice could overflow.
 constexpr int kSelWarpStage = 96;        // records per warp slice
-constexpr int kSelConsumers = 512;       // 16 consumer warps
+constexpr int kSelConsumers = 768;       // 24 consumer warps, one slot each per tile
 constexpr int kSelCollectThreads = kSelConsumers + 32;  // + one producer warp
-constexpr int kSelTile = 1024;           // slots per TMA tile
+constexpr int kSelTile = 768;            // slots per TMA tile (96-byte validity rows stay 16-B aligned)
 constexpr int kSelStages = 3;            // tiles in flight per CTA
 constexpr int kSelMaxCols = 7;
 constexpr int kSelStageBytes = kSelMaxCols * kSelTile * 8 + kSelTile / 8;  // columns + validity words
+static_assert(kSelTile % kSelConsumers == 0 && kSelTile % 128 == 0, "tile shape");
 constexpr int kSelCollectSmem = kSelStages * kSelStageBytes +
                                 (kSelConsumers / 32) * kSelWarpStage * static_cast<int>(sizeof(SelRec)) + 64;
 
@@ -408,12 +409,12 @@ struct SelColumns {
     int ncol;
 };
 
-// Persistent CTAs: a producer warp streams 1024-slot tiles of the key
+// Persistent CTAs: a producer warp streams 768-slot tiles of the key
 // columns and the validity words into a 3-stage shared-memory ring with 1-D
 // bulk copies (TMA engine; `full` mbarriers complete on the bytes, `empty`
 // mbarriers collect one arrival per consumer warp), so the bytes in flight do
 // not depend on registers and no block-wide barrier couples the warps.  Each
-// consumer thread takes two slots per tile; records go to per-warp smem
+// consumer thread takes one slot per tile; records go to per-warp smem
 // slices (warp-aggregated), flushed with one global reservation each.
 __global__ void __launch_bounds__(kSelCollectThreads, 1) sel_collect_kernel(const EvictCols c, const SelColumns cols,
                                                                            int policy, double now, int slot_tie,
