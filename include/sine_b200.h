@@ -183,6 +183,19 @@ int sine_kernel_launches(sine_index_t *h, int64_t *n);
  * buffers overflowed and were re-run on the list-keeping kernels.  Not in
  * the reference (diagnostic for the batched path, like sine_uncertified). */
 int sine_gemm_overflows(sine_index_t *h, int64_t *n);
+/* Single-process multi-GPU stage-1 (replaces one ExactCosineIndex with P
+ * row shards for the reference's single-process engine, engine.py:103-109):
+ * shards[p] lives on devices[p] (a device may repeat); each query runs on
+ * every shard concurrently (one worker thread per shard, certified exact
+ * top-k each), the [B][k] blocks are peer-copied to devices[0] and merged
+ * by (similarity desc, id asc).  The group does not own the shards. */
+typedef struct sine_group sine_group_t;
+int sine_group_create(sine_index_t *const *shards, const int *devices, int n, int64_t dim,
+                      sine_group_t **out);
+int sine_group_destroy(sine_group_t *g);
+int sine_group_query(sine_group_t *g, int64_t B, const double *q, int k, double min_sim,
+                     uint32_t mode, int64_t *out_ids, double *out_sims, int32_t *out_counts);
+
 /* Row-sharded stage-1 (one process per GPU): merge the P per-rank exact
  * top-k lists of B queries -- the all-gather output on the device, rank r's
  * [B][k] ids / sims at r * rank_stride elements (0 = B * k), id -1 =

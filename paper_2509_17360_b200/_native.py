@@ -43,6 +43,11 @@ _SIGS = {
     "sine_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int64,
                                    ctypes.POINTER(ctypes.c_void_p)]),
     "sine_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "sine_group_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                         ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "sine_group_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "sine_group_query": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _f64p, ctypes.c_int, ctypes.c_double,
+                                        ctypes.c_uint32, _i64p, _f64p, _i32p]),
     "sine_reserve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     "sine_insert": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _i64p, _f64p,
                                    ctypes.POINTER(MetaCols), ctypes.c_uint32]),

@@ -1663,6 +1663,10 @@ void gather_rows_host(sine_index* h, int64_t n, const int64_t* slots, double* ou
 extern "C" {
 
 const char* sine_last_error(void) { return g_err.c_str(); }
+
+// not in the public header: other translation units (group.cu) report
+// their failures through the same thread-local message
+void sine_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
 int sine_version(void) { return 1; }
 
 int sine_device_count(int* n) {

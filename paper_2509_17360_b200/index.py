@@ -31,6 +31,14 @@ from .errors import ValidationError
 _NORM_TOL = 1e-6
 
 
+# Device limits (documented in INTEGRATION.md): the top-k keeps k + 16
+# candidates per query in shared memory (k <= 128), and the streaming scan
+# holds one query in registers.
+MAX_K = 128
+MAX_DIM_F32 = 2048
+MAX_DIM_BF16 = 4096
+
+
 @dataclass(frozen=True)
 class Candidate:
     """(id, similarity) -- mirrors reference index.py:26-29."""
@@ -80,15 +88,20 @@ class GpuCosineIndex:
             raise ValidationError("dimension must be >= 1")
         if scan not in ("fp32", "bf16"):
             raise ValidationError(f"scan must be 'fp32' or 'bf16', got {scan!r}")
+        if store_f32 is None:  # bf16 + re-rank keeps fp32 rows: the certificate's exact fallback
+            store_f32 = scan == "fp32" or rerank
+        if store_bf16 is None:
+            store_bf16 = scan == "bf16"
+        # the streaming scan (also the certificates' exact fallback) keeps a
+        # query in registers: up to 2048 fp32 / 4096 bf16 components
+        if (store_f32 and dimension > MAX_DIM_F32) or (store_bf16 and not store_f32 and dimension > MAX_DIM_BF16):
+            raise ValidationError(f"dimension {dimension} exceeds the device scan limit "
+                                  f"({MAX_DIM_F32} with fp32 rows, {MAX_DIM_BF16} bf16-only)")
         self.dimension = dimension
         self.seed = seed
         self.device = device
         self.scan = scan
         self.rerank = rerank
-        if store_f32 is None:  # bf16 + re-rank keeps fp32 rows: the certificate's exact fallback
-            store_f32 = scan == "fp32" or rerank
-        if store_bf16 is None:
-            store_bf16 = scan == "bf16"
         flags = (N.STORE_F32 if store_f32 else 0) | (N.STORE_BF16 if store_bf16 else 0) | \
             (N.STORE_META if metadata else 0)
         self._lib = N.load_library()
@@ -488,6 +501,21 @@ class PendingQuery:
 
     def wait(self):
         if self._result is None:
-            N.check(self._index._lib.sine_query_wait(self._index.handle, self._ticket))
+            try:
+                N.check(self._index._lib.sine_query_wait(self._index.handle, self._ticket))
+            finally:
+                self._ticket = None  # the library freed the ticket (or it was never valid)
             self._result = (self._ids.array.copy(), self._sims.array.copy(), self._counts.array.copy())
         return self._result
+
+    def close(self) -> None:
+        """Release the ticket of a batch whose results are not needed (its
+        pinned buffers stay alive until the device is done with them)."""
+        if self._result is None and getattr(self, "_ticket", None) is not None:
+            try:
+                self.wait()
+            except Exception:  # noqa: BLE001 - best effort: the ticket is freed either way
+                pass
+
+    def __del__(self):
+        self.close()
