@@ -850,13 +850,17 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.slot_ids = h->ids_ascending ? 1 : 0;
         p.gbound = h->gbound.p;  // zeroed by res_prep_queries
         p.tile_stride = 1;
-        // a single query over fp32 rows: FFMA on the staged tiles instead of
-        // N = 16 MMAs that are 15/16 padding.  Same box, config B, B = 1:
-        // fp32 2166-2177 vs 1851-1862 lookups/s (kernel 0.451 vs 0.521 ms);
-        // bf16 rows lose (3611 vs 3760: twice the FMAs per byte), so they
-        // keep the MMAs.  SINE_NO_FFMA=1 keeps the MMAs, for A/B timing.
+        // a single query over fp32 rows: FFMA2 on the staged tiles instead
+        // of N = 16 MMAs that are 15/16 padding.  Same box, config B, B = 1:
+        // 2166-2177 vs 1851-1862 lookups/s (kernel 0.451 vs 0.521 ms).  bf16
+        // rows carry twice the elements per byte and the four epilogue warps
+        // also keep the top-k lists: even with packed FFMA2 and the query
+        // widened once in smem they lose (3418 vs 3709 at tau 0.9, 2660 vs
+        // 3404 at tau -1), so they keep the MMAs unless SINE_FFMA_BF16=1.
+        // SINE_NO_FFMA=1 keeps the MMAs for fp32 rows too (A/B timing).
         static const bool ffma_on = getenv("SINE_NO_FFMA") == nullptr;
-        p.ffma = ffma_on && tf32 && CS == 1 && nq == 1 && NQ == 16 ? 1 : 0;
+        static const bool ffma_bf16 = getenv("SINE_FFMA_BF16") != nullptr;
+        p.ffma = ffma_on && (tf32 || ffma_bf16) && CS == 1 && nq == 1 && NQ == 16 ? 1 : 0;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;

@@ -423,7 +423,7 @@ constexpr int kSparse = 128;     // (query, row) pairs per tile handed to the sp
 constexpr int kSparseRows = 32;  // tiles with more passing rows take the dense (bitonic) rounds
 
 struct ResSmem {
-    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, sparse_off, total;
+    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, sparse_off, fq_off, total;
 };
 
 // Nq_res: queries resident in this CTA's shared memory (== Nq except for the
@@ -454,6 +454,9 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     off = (off + 15) / 16 * 16;
     L.sparse_off = off;  // counter + kSparse (query, slot, key) entries
     off += 16 + static_cast<size_t>(kSparse) * 16;
+    off = (off + 15) / 16 * 16;
+    L.fq_off = off;  // FFMA mode: the single query in fp32, one 128-B K block -> kUmmaKB / 2 floats (bf16 rows)
+    off += static_cast<size_t>(kblocks) * (kUmmaKB / 2) * 4;
     L.total = off + 1024;
     return L;
 }
@@ -576,6 +579,15 @@ __device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool v) {
         : "r"(v ? 1u : 0u), "r"(id), "r"(nthreads)
         : "memory");
     return r != 0;
+}
+
+// Packed fp32 pair {lo, hi} in one 64-bit register and the sm_100 FFMA2:
+// acc.lo += a.lo * b.lo, acc.hi += a.hi * b.hi (round-to-nearest each).
+__device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) {
+    return static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+}
+__device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t a, uint64_t b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
 }
 
 #define SINE_TMEM_LD16(taddr, r)                                                                              \
@@ -793,7 +805,18 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         int i = 0;
         int fs = 0;  // FFMA mode: this thread's view of the stage ring
         uint32_t fph = 0;
-        if (p.ffma) mbar_wait(qfull, 0);
+        float* fq = reinterpret_cast<float*>(smem + L.fq_off);
+        if (p.ffma) {
+            mbar_wait(qfull, 0);
+            if (!p.tf32) {  // query row 0 of each bf16 K block is unswizzled: widen it once
+                for (int e = tid; e < nkb * (kUmmaKB / 2); e += 128) {
+                    const int kb = e / (kUmmaKB / 2), c = e % (kUmmaKB / 2);
+                    const uint16_t v = reinterpret_cast<const uint16_t*>(sq + static_cast<size_t>(kb) * NQ * kUmmaKB)[c];
+                    fq[e] = __uint_as_float(static_cast<uint32_t>(v) << 16);
+                }
+                named_bar_sync(2, 128);
+            }
+        }
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
             const int64_t slot = static_cast<int64_t>(t) * p.tile_stride * kUmmaN + tid;
@@ -808,32 +831,40 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             named_bar_sync(2, 128);
             float sc[NQ];
             if (p.ffma) {
-                // one query: 768 FMAs per row per tile on the CUDA cores, read
-                // from the 128B-swizzled stages (16-B chunk c of row r sits at
-                // chunk c ^ (r & 7)); query row 0 of each K block is unswizzled
-                float a0 = 0.0f, a1 = 0.0f;
+                // one query: the dot products on the CUDA cores with packed
+                // FFMA2 (two fp32 lanes per instruction), read from the
+                // 128B-swizzled stages (16-B chunk c of row r sits at chunk
+                // c ^ (r & 7)); bf16 rows widen with a shift / mask per pair
+                // against the query pre-converted to fp32 in smem
+                uint64_t acc2[2] = {0ull, 0ull};  // {lo, hi} fp32 pairs
                 const int sw = tid & 7;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(full + fs, fph);
                     const uint8_t* rowp = sa + static_cast<size_t>(fs) * kUmmaN * kUmmaKB + tid * kUmmaKB;
-                    const uint8_t* qp = sq + static_cast<size_t>(kb) * NQ * kUmmaKB;
+                    if (p.tf32) {
+                        const uint8_t* qp = sq + static_cast<size_t>(kb) * NQ * kUmmaKB;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
-                        const uint4 qv = *reinterpret_cast<const uint4*>(qp + (c << 4));
-                        if (p.tf32) {
-                            a0 = fmaf(__uint_as_float(xv.x), __uint_as_float(qv.x), a0);
-                            a1 = fmaf(__uint_as_float(xv.y), __uint_as_float(qv.y), a1);
-                            a0 = fmaf(__uint_as_float(xv.z), __uint_as_float(qv.z), a0);
-                            a1 = fmaf(__uint_as_float(xv.w), __uint_as_float(qv.w), a1);
-                        } else {
-                            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                        for (int c = 0; c < 8; ++c) {
+                            const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+                            const uint4 qv = *reinterpret_cast<const uint4*>(qp + (c << 4));
+                            ffma2(acc2[0], pack2(xv.x, xv.y), pack2(qv.x, qv.y));
+                            ffma2(acc2[1], pack2(xv.z, xv.w), pack2(qv.z, qv.w));
+                        }
+                    } else {
+                        const float4* qf = reinterpret_cast<const float4*>(fq + kb * (kUmmaKB / 2));
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                a0 = fmaf(__uint_as_float(xw[u] << 16), __uint_as_float(qw[u] << 16), a0);
-                                a1 = fmaf(__uint_as_float(xw[u] & 0xffff0000u), __uint_as_float(qw[u] & 0xffff0000u),
-                                          a1);
-                            }
+                        for (int c = 0; c < 8; ++c) {
+                            const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+                            const float4 q0 = qf[2 * c], q1 = qf[2 * c + 1];
+                            // bf16 pair w -> fp32 (w << 16, w & 0xffff0000)
+                            ffma2(acc2[0], pack2(xv.x << 16, xv.x & 0xffff0000u),
+                                  pack2(__float_as_uint(q0.x), __float_as_uint(q0.y)));
+                            ffma2(acc2[1], pack2(xv.y << 16, xv.y & 0xffff0000u),
+                                  pack2(__float_as_uint(q0.z), __float_as_uint(q0.w)));
+                            ffma2(acc2[0], pack2(xv.z << 16, xv.z & 0xffff0000u),
+                                  pack2(__float_as_uint(q1.x), __float_as_uint(q1.y)));
+                            ffma2(acc2[1], pack2(xv.w << 16, xv.w & 0xffff0000u),
+                                  pack2(__float_as_uint(q1.z), __float_as_uint(q1.w)));
                         }
                     }
                     __syncwarp();
@@ -843,7 +874,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                         fph ^= 1;
                     }
                 }
-                sc[0] = (a0 + a1) + 0.0f;
+                const float s0 = __uint_as_float(static_cast<uint32_t>(acc2[0])) +
+                                 __uint_as_float(static_cast<uint32_t>(acc2[1]));
+                const float s1 = __uint_as_float(static_cast<uint32_t>(acc2[0] >> 32)) +
+                                 __uint_as_float(static_cast<uint32_t>(acc2[1] >> 32));
+                sc[0] = (s0 + s1) + 0.0f;
 #pragma unroll
                 for (int j = 1; j < NQ; ++j) sc[j] = 0.0f;
             } else {
