@@ -858,9 +858,13 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         // widened once in smem they lose (3418 vs 3709 at tau 0.9, 2660 vs
         // 3404 at tau -1), so they keep the MMAs unless SINE_FFMA_BF16=1.
         // SINE_NO_FFMA=1 keeps the MMAs for fp32 rows too (A/B timing).
+        // fp32 rows use scalar FFMA in four chains: packed FFMA2 measured
+        // slower on the same box (headline kernel 0.479 vs 0.449 ms, 2040 vs
+        // 2189 lookups/s), so it is opt-in (SINE_FFMA2=1).
         static const bool ffma_on = getenv("SINE_NO_FFMA") == nullptr;
         static const bool ffma_bf16 = getenv("SINE_FFMA_BF16") != nullptr;
-        p.ffma = ffma_on && (tf32 || ffma_bf16) && CS == 1 && nq == 1 && NQ == 16 ? 1 : 0;
+        static const bool ffma2 = getenv("SINE_FFMA2") != nullptr;
+        p.ffma = ffma_on && (tf32 || ffma_bf16) && CS == 1 && nq == 1 && NQ == 16 ? (tf32 && !ffma2 ? 1 : 2) : 0;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;

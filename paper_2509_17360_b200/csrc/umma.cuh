@@ -407,8 +407,9 @@ struct ResParams {
     int slot_ids;     // slot order == id order (ties resolved without loads)
     uint32_t* gbound;  // [nq] chip-wide admission bound per query (f32 keys)
     int tile_stride;   // 1 = every tile; >1 = sample pass over every tile_stride-th tile
-    int ffma;          // 1 = single query: the epilogue warps take the dot products with FFMA
-                       //     straight from the TMA-staged tiles (no MMAs)
+    int ffma;          // single query: the epilogue warps take the dot products on the CUDA
+                       //     cores straight from the TMA-staged tiles (no MMAs): 1 = scalar
+                       //     FFMA (fp32 rows), 2 = packed FFMA2
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -836,12 +837,24 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 // 128B-swizzled stages (16-B chunk c of row r sits at chunk
                 // c ^ (r & 7)); bf16 rows widen with a shift / mask per pair
                 // against the query pre-converted to fp32 in smem
-                uint64_t acc2[2] = {0ull, 0ull};  // {lo, hi} fp32 pairs
+                uint64_t acc2[2] = {0ull, 0ull};  // {lo, hi} fp32 pairs (FFMA2)
+                float fa[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // scalar chains (p.ffma == 1)
                 const int sw = tid & 7;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(full + fs, fph);
                     const uint8_t* rowp = sa + static_cast<size_t>(fs) * kUmmaN * kUmmaKB + tid * kUmmaKB;
-                    if (p.tf32) {
+                    if (p.tf32 && p.ffma == 1) {  // scalar FFMA, four independent chains
+                        const uint8_t* qp = sq + static_cast<size_t>(kb) * NQ * kUmmaKB;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+                            const uint4 qv = *reinterpret_cast<const uint4*>(qp + (c << 4));
+                            fa[0] = fmaf(__uint_as_float(xv.x), __uint_as_float(qv.x), fa[0]);
+                            fa[1] = fmaf(__uint_as_float(xv.y), __uint_as_float(qv.y), fa[1]);
+                            fa[2] = fmaf(__uint_as_float(xv.z), __uint_as_float(qv.z), fa[2]);
+                            fa[3] = fmaf(__uint_as_float(xv.w), __uint_as_float(qv.w), fa[3]);
+                        }
+                    } else if (p.tf32) {
                         const uint8_t* qp = sq + static_cast<size_t>(kb) * NQ * kUmmaKB;
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
@@ -875,9 +888,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                     }
                 }
                 const float s0 = __uint_as_float(static_cast<uint32_t>(acc2[0])) +
-                                 __uint_as_float(static_cast<uint32_t>(acc2[1]));
+                                 __uint_as_float(static_cast<uint32_t>(acc2[1])) + (fa[0] + fa[2]);
                 const float s1 = __uint_as_float(static_cast<uint32_t>(acc2[0] >> 32)) +
-                                 __uint_as_float(static_cast<uint32_t>(acc2[1] >> 32));
+                                 __uint_as_float(static_cast<uint32_t>(acc2[1] >> 32)) + (fa[1] + fa[3]);
                 sc[0] = (s0 + s1) + 0.0f;
 #pragma unroll
                 for (int j = 1; j < NQ; ++j) sc[j] = 0.0f;
