@@ -525,8 +525,10 @@ def run_ours(args):
     if world == 1 and not args.no_trace:
         trace = measure_trace(rows)
     persistence = None
+    host_master = None
     if world == 1 and not args.no_trace:
         persistence = measure_persistence(rows)
+        host_master = measure_host_master(rows, idx, torch)
     embedder = None
     if world == 1 and not args.no_trace:
         embedder = measure_embedder()
@@ -567,7 +569,7 @@ def run_ours(args):
                 "gpu_launches": int(launches), "uncertified_rerun_in_timed_region": uncertified,
                 "parity": parity, "parity_sampled": None if parity is None else parity["parity_sampled"],
                 "regimes": regimes, "eviction": eviction, "trace": trace, "config_c": config_c,
-                "persistence": persistence, "embedder": embedder}
+                "persistence": persistence, "embedder": embedder, "host_master": host_master}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -643,6 +645,38 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                             "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
                             "tflops": flops / (ms / 1e3) / 1e12,
                             "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak})
+    return out
+
+
+def measure_host_master(rows, idx, torch):
+    """The fp64 master rows in pinned, device-mapped host memory
+    (host_master=True): what the re-rank's k' row reads over the host link
+    cost, against the HBM master of the headline index, same box.  Merge
+    kernel time per launch (CUDA events on the library stream) and the
+    per-batch time through the host API."""
+    from paper_2509_17360_b200 import GpuCosineIndex
+
+    n, d = rows.shape
+    hm = GpuCosineIndex(d, scan="fp32", store_f32=True, store_bf16=True, capacity=n, host_master=True)
+    hm.insert_batch(np.arange(n), rows, _checked=True)
+    out = {"workload": f"config B {n} x {d}, k={K}, tau={TAU}: fp64 master rows in HBM vs host-mapped "
+                       f"(HBM saved: {n * d * 8 / 1e9:.1f} GB)", "cases": []}
+    for b in (1, 64, 4096):
+        q = make_queries(rows, b, seed=300 + b)
+        row = {"batch": b}
+        for name, ix in (("hbm_master", idx), ("host_master", hm)):
+            ix.query_batch(q, K, TAU)
+            ix.set_timing(True)
+            ix.timing_totals(1, reset=True)
+            t0 = time.perf_counter()
+            for _ in range(5):
+                ix.query_batch(q, K, TAU)
+            dt = (time.perf_counter() - t0) / 5
+            mm, mn = ix.timing_totals(1, reset=True)
+            ix.set_timing(False)
+            row[name] = {"ms_per_batch": dt * 1e3, "merge_ms_per_launch": mm / max(mn, 1)}
+        out["cases"].append(row)
+    hm.close()
     return out
 
 

@@ -49,6 +49,10 @@ extern "C" {
 #define SINE_STORE_F32   0x1u  /* keep fp32 scan rows  (exact mode)          */
 #define SINE_STORE_BF16  0x2u  /* keep bf16 scan rows  (fast mode)           */
 #define SINE_STORE_META  0x4u  /* keep LCFU metadata columns (engine mode)   */
+#define SINE_STORE_F64_HOST 0x8u /* fp64 master rows in pinned host memory mapped
+                                    into the device address space instead of HBM:
+                                    the re-rank reads only k' rows per query over
+                                    the host link; frees 8 B/dim/row of HBM     */
 
 /* ---- sine_query modes ------------------------------------------------------ */
 #define SINE_SCAN_F32      0x0u  /* fp32 rows, fp32 accumulation             */

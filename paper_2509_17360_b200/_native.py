@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 
 SINE_OK, SINE_EINVAL, SINE_ECUDA, SINE_ENCCL, SINE_ENOMEM, SINE_ENOTFOUND, SINE_EDUP, SINE_ENORM = range(8)
 
-STORE_F32, STORE_BF16, STORE_META = 0x1, 0x2, 0x4
+STORE_F32, STORE_BF16, STORE_META, STORE_F64_HOST = 0x1, 0x2, 0x4, 0x8
 SCAN_F32, SCAN_BF16, RERANK_F64, NO_NORM_CHECK, SCAN_CUDA_CORE, SCAN_UMMA_V1, CERTIFY, SCAN_CLUSTER, SCAN_PAIR = \
     0x0, 0x1, 0x10, 0x100, 0x200, 0x400, 0x800, 0x1000, 0x2000
 SCAN_GEMM, SCAN_NO_GEMM = 0x4000, 0x8000

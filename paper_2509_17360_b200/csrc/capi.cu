@@ -6,6 +6,8 @@
 //   rows32 [cap][stride32] fp32     scan rows, exact mode   (128-B padded)
 //   rows16 [cap][stride16] bf16     scan rows, fast mode    (128-B padded)
 //   rows64 [cap][dim]      fp64     master copy: fp64 re-rank + snapshots
+//                                   (pinned, device-mapped host memory with
+//                                   SINE_STORE_F64_HOST)
 //   ids    [cap] int64,  valid bitmap [cap/32] uint32
 //   LCFU columns (engine mode): log_freq/log_cost/log_lat/log_stat,
 //     created_at, expiration_time, last_access (fp64), frequency,
@@ -185,6 +187,7 @@ struct sine_index {
     cudaStream_t ws_stream = nullptr;  // last stream that enqueued store/workspace work
     cudaEvent_t ws_ev = nullptr;       // recorded after that work when it was a caller stream
     bool timing = false;
+    uint32_t ev_mask = 0;  // ev[i] recorded since the last read
     // accumulated per-kernel device time (CUDA events on the launch stream)
     struct Timed {
         cudaEvent_t a = nullptr, b = nullptr;
@@ -388,6 +391,25 @@ void alloc_col(T*& p, int64_t n) {
     CK(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(T)));
 }
 
+// The fp64 master rows: HBM, or pinned host memory mapped into the device
+// address space (SINE_STORE_F64_HOST; UVA: one pointer for host and device).
+double* alloc_master(const sine_index* h, int64_t elems) {
+    double* p = nullptr;
+    if (h->flags & SINE_STORE_F64_HOST) {
+        CK(cudaHostAlloc(&p, std::max<int64_t>(elems, 1) * sizeof(double), cudaHostAllocMapped | cudaHostAllocPortable));
+    } else {
+        CK(cudaMalloc(&p, std::max<int64_t>(elems, 1) * sizeof(double)));
+    }
+    return p;
+}
+void free_master(const sine_index* h, double* p) {
+    if (!p) return;
+    if (h->flags & SINE_STORE_F64_HOST)
+        cudaFreeHost(p);
+    else
+        cudaFree(p);
+}
+
 void grow(sine_index* h, int64_t want) {
     if (want <= h->cap) return;
     int64_t nc = std::max<int64_t>(want, std::max<int64_t>(1024, h->cap * 2));
@@ -406,7 +428,7 @@ void grow(sine_index* h, int64_t want) {
     if (h->cap == 0) {
         if (h->flags & SINE_STORE_F32) alloc_col(h->rows32, nc * h->stride32);
         if (h->flags & SINE_STORE_BF16) alloc_col(h->rows16, nc * h->stride16);
-        alloc_col(h->rows64, nc * h->dim);
+        h->rows64 = alloc_master(h, nc * h->dim);
         alloc_col(h->ids, nc);
         alloc_col(h->valid, nc / 32);
         CK(cudaMemsetAsync(h->valid, 0, nc / 32 * sizeof(uint32_t), h->stream));
@@ -418,7 +440,14 @@ void grow(sine_index* h, int64_t want) {
     } else {
         move(h->rows32, h->stride32);
         move(h->rows16, h->stride16);
-        move(h->rows64, h->dim);
+        {
+            double* nw = alloc_master(h, nc * h->dim);
+            if (h->nslots)
+                CK(cudaMemcpyAsync(nw, h->rows64, h->nslots * h->dim * sizeof(double), cudaMemcpyDefault, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            free_master(h, h->rows64);
+            h->rows64 = nw;
+        }
         move(h->ids, 1);
         {
             uint32_t* nv = nullptr;
@@ -512,7 +541,8 @@ void append(sine_index* h, int64_t n, const int64_t* ids, const double* rows, bo
     grow(h, h->nslots + n);
     const int64_t s0 = h->nslots;
     const cudaMemcpyKind kind = rows_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CK(cudaMemcpyAsync(h->rows64 + s0 * h->dim, rows, n * h->dim * sizeof(double), kind, h->stream));
+    CK(cudaMemcpyAsync(h->rows64 + s0 * h->dim, rows, n * h->dim * sizeof(double),
+                       (h->flags & SINE_STORE_F64_HOST) ? cudaMemcpyDefault : kind, h->stream));
     const int64_t width = std::max(h->rows32 ? h->stride32 : 0, h->rows16 ? h->stride16 : 0);
     if (width) {
         convert_rows_kernel<<<grid_for(n * width, 256, h->num_sms), 256, 0, h->stream>>>(
@@ -570,7 +600,13 @@ void compact(sine_index* h) {
     };
     redo(h->rows32, h->stride32);
     redo(h->rows16, h->stride16);
-    redo(h->rows64, h->dim);
+    if (h->flags & SINE_STORE_F64_HOST) {  // host-resident master rows: compact on the host
+        CK(cudaStreamSynchronize(h->stream));
+        for (int64_t i = 0; i < n; ++i)
+            if (from[i] != i) std::memmove(h->rows64 + i * h->dim, h->rows64 + from[i] * h->dim, h->dim * sizeof(double));
+    } else {
+        redo(h->rows64, h->dim);
+    }
     redo(h->ids, 1);
     redo(h->lf, 1), redo(h->lc, 1), redo(h->ll, 1), redo(h->ls, 1);
     redo(h->created, 1), redo(h->expiration, 1), redo(h->last_access, 1);
@@ -653,7 +689,20 @@ void launch_scan_nq(int NQ, const ScanParams& p, int grid, int threads, size_t s
 }
 
 void record(sine_index* h, int i, cudaStream_t st) {
-    if (h->timing) CK(cudaEventRecord(h->ev[i], st));
+    if (h->timing) {
+        CK(cudaEventRecord(h->ev[i], st));
+        h->ev_mask |= 1u << i;
+    }
+}
+
+// last_timing's scan / merge split: only the CUDA-core path records the
+// three events; the tensor-core paths report through timing_totals
+void scan_merge_times(sine_index* h) {
+    if ((h->ev_mask & 7u) == 7u) {
+        CK(cudaEventElapsedTime(&h->t_scan, h->ev[0], h->ev[1]));
+        CK(cudaEventElapsedTime(&h->t_merge, h->ev[1], h->ev[2]));
+    }
+    h->ev_mask &= ~7u;
 }
 
 // kind 0 = scan kernel, 1 = merge kernel, 2 = tensor-core scan
@@ -1709,7 +1758,8 @@ int sine_destroy(sine_index_t* h) {
         cudaSetDevice(h->device);
         if (h->ws_stream != h->stream) cudaEventSynchronize(h->ws_ev);  // caller-stream queries drain first
         cudaStreamSynchronize(h->stream);
-        for (void* p : {(void*)h->rows32, (void*)h->rows16, (void*)h->rows64, (void*)h->ids, (void*)h->valid,
+        free_master(h, h->rows64);
+        for (void* p : {(void*)h->rows32, (void*)h->rows16, (void*)h->ids, (void*)h->valid,
                         (void*)h->lf, (void*)h->lc, (void*)h->ll, (void*)h->ls, (void*)h->created,
                         (void*)h->expiration, (void*)h->last_access, (void*)h->freq, (void*)h->size})
             if (p) cudaFree(p);
@@ -1876,10 +1926,7 @@ int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_si
             std::memcpy(out_ids, h->ids_zc.p, B * k * sizeof(int64_t));
             std::memcpy(out_sims, h->sims_zc.p, B * k * sizeof(double));
             std::memcpy(out_counts, h->cnt_zc.p, B * sizeof(int32_t));
-            if (h->timing) {
-                CK(cudaEventElapsedTime(&h->t_scan, h->ev[0], h->ev[1]));
-                CK(cudaEventElapsedTime(&h->t_merge, h->ev[1], h->ev[2]));
-            }
+            if (h->timing) scan_merge_times(h);
             return;
         }
         query_device_impl(h, B, h->q64.p, k, min_sim, mode, h->o_ids.p, h->o_sims.p, h->o_cnt.p, h->stream);
@@ -1905,10 +1952,7 @@ int sine_query(sine_index_t* h, int64_t B, const double* q, int k, double min_si
                 CK(cudaStreamSynchronize(h->stream));
             }
         }
-        if (h->timing) {
-            CK(cudaEventElapsedTime(&h->t_scan, h->ev[0], h->ev[1]));
-            CK(cudaEventElapsedTime(&h->t_merge, h->ev[1], h->ev[2]));
-        }
+        if (h->timing) scan_merge_times(h);
     });
 }
 

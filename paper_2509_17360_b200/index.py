@@ -83,7 +83,11 @@ class GpuCosineIndex:
 
     def __init__(self, dimension: int, seed: int = 1, *, device: int = 0, scan: str = "fp32",
                  rerank: bool = True, store_bf16: bool | None = None, store_f32: bool | None = None,
-                 metadata: bool = False, capacity: int = 0):
+                 metadata: bool = False, capacity: int = 0, host_master: bool = False):
+        """host_master: keep the fp64 master rows (re-rank + snapshots) in
+        pinned, device-mapped host memory instead of HBM (SINE_STORE_F64_HOST):
+        8 B per dimension per row less HBM; the re-rank reads its k' rows
+        per query over the host link."""
         if dimension < 1:
             raise ValidationError("dimension must be >= 1")
         if scan not in ("fp32", "bf16"):
@@ -103,7 +107,7 @@ class GpuCosineIndex:
         self.scan = scan
         self.rerank = rerank
         flags = (N.STORE_F32 if store_f32 else 0) | (N.STORE_BF16 if store_bf16 else 0) | \
-            (N.STORE_META if metadata else 0)
+            (N.STORE_META if metadata else 0) | (N.STORE_F64_HOST if host_master else 0)
         self._lib = N.load_library()
         h = ctypes.c_void_p()
         N.check(self._lib.sine_create(device, dimension, flags, int(capacity), ctypes.byref(h)))
