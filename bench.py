@@ -1186,7 +1186,11 @@ def measure_trace(rows, n_ops=2000, cpu_ops=24):
             emb = _DictEmbedder(d)
             els = _make_elements(M, n, meta, shared)
             usage = int(meta["size"].sum())
-            eng = P.CacheEngine(P.CacheConfig(capacity_tokens=usage), emb, _TextJudge(), scan=scan)
+            # the store reserves room for the trace's admissions up front (a
+            # deployment sizes its store; growing a 1M x 768 store mid-trace
+            # reallocates ~10 GB of columns inside the timed region)
+            ix = P.GpuCosineIndex(d, seed=1, scan=scan, metadata=True, capacity=n + n_ops + 1024)
+            eng = P.CacheEngine(P.CacheConfig(capacity_tokens=usage), emb, _TextJudge(), index=ix)
             eng.bulk_admit(els, rows, now=0.0)
             run_trace(eng, ops[:50], emb, M, 1.0, batched)  # warm-up
             t0 = time.perf_counter()
