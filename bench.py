@@ -526,9 +526,11 @@ def run_ours(args):
         trace = measure_trace(rows)
     persistence = None
     host_master = None
+    recall = None
     if world == 1 and not args.no_trace:
         persistence = measure_persistence(rows)
         host_master = measure_host_master(rows, idx, torch)
+        recall = measure_recall(rows, idx)
     embedder = None
     if world == 1 and not args.no_trace:
         embedder = measure_embedder()
@@ -569,7 +571,8 @@ def run_ours(args):
                 "gpu_launches": int(launches), "uncertified_rerun_in_timed_region": uncertified,
                 "parity": parity, "parity_sampled": None if parity is None else parity["parity_sampled"],
                 "regimes": regimes, "eviction": eviction, "trace": trace, "config_c": config_c,
-                "persistence": persistence, "embedder": embedder, "host_master": host_master}
+                "persistence": persistence, "embedder": embedder, "host_master": host_master,
+                "recall": recall}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -645,6 +648,30 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                             "hbm_frac": byt / (ms / 1e3) / 1e9 / hbm_peak,
                             "tflops": flops / (ms / 1e3) / 1e12,
                             "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak})
+    return out
+
+
+def measure_recall(rows, idx, n_q=1024, k=K):
+    """north_star: the recall of each mode against the exact answer.  bf16
+    fast mode WITHOUT the fp64 re-rank (bf16 scores, no certificate) against
+    the exact fp32 + fp64 path (parity-checked against the oracle), config B,
+    half planted near-duplicates: recall@k at min_similarity -1, and at
+    tau_sim the fraction of exact hits (cos >= 0.9) the fast mode returns.
+    The bf16 mode WITH the re-rank is exact under its certificate (recall 1
+    by construction; checked here too)."""
+    q = make_queries(rows, n_q, seed=500)
+    out = {"queries": n_q, "k": k}
+    ex_ids, _, ex_cnt = idx.query_batch(q, k, -1.0, scan="fp32", rerank=True)
+    for name, rr in (("bf16_no_rerank", False), ("bf16_rerank", True)):
+        f_ids, _, _ = idx.query_batch(q, k, -1.0, scan="bf16", rerank=rr)
+        inter = [len(set(ex_ids[i, :ex_cnt[i]].tolist()) & set(f_ids[i].tolist())) / max(1, ex_cnt[i])
+                 for i in range(n_q)]
+        out[f"recall_at_{k}_{name}"] = float(np.mean(inter))
+        h_ids, _, h_cnt = idx.query_batch(q, k, TAU, scan="fp32", rerank=True)
+        g_ids, _, g_cnt = idx.query_batch(q, k, TAU, scan="bf16", rerank=rr)
+        hits = sum(int(h_cnt[i]) for i in range(n_q))
+        found = sum(len(set(h_ids[i, :h_cnt[i]].tolist()) & set(g_ids[i, :g_cnt[i]].tolist())) for i in range(n_q))
+        out[f"hit_recall_tau_{name}"] = found / max(1, hits)
     return out
 
 
@@ -770,12 +797,22 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
     idx = GpuCosineIndex(d, scan="bf16", store_f32=store_f32, store_bf16=True, capacity=n)
     g = torch.Generator(device="cuda").manual_seed(7)
     chunk = 250_000
+    # a host copy for the CPU baseline (the reference's float64 matrix) when
+    # the host has room for it next to everything else
+    try:
+        import psutil
+        host_ok = psutil.virtual_memory().available > n * d * 8 * 1.4
+    except Exception:  # noqa: BLE001
+        host_ok = False
+    host = np.empty((n, d), dtype=np.float64) if host_ok else None
     t0 = time.perf_counter()
     for i0 in range(0, n, chunk):
         m = min(chunk, n - i0)
         x = torch.randn((m, d), dtype=torch.float64, device="cuda", generator=g)
         x /= x.norm(dim=1, keepdim=True)
         idx.insert_device(np.arange(i0, i0 + m, dtype=np.int64) + 1, x.data_ptr())
+        if host is not None:
+            host[i0:i0 + m] = x.cpu().numpy()
         del x
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t0
@@ -829,8 +866,50 @@ def measure_config_c(torch, hbm_peak, tensor_peak, n=10_000_000, d=1024, k=20):
                                "hbm_frac": algorithmic_bytes(n, d, b, k, scan) / (ms / 1e3) / 1e9 / hbm_peak,
                                "tensor_frac": flops / (ms / 1e3) / 1e12 / tpeak,
                                "planted_hit_exact": hit})
+    # e2e: B = 1 through the host API (queries up, results down, certificate)
+    for scan in ("bf16",) + (("fp32",) if store_f32 else ()):
+        q1 = qs[:8]
+        idx.query_batch(q1[:1], k, TAU, scan=scan)
+        t1 = time.perf_counter()
+        for j in range(8):
+            idx.query_batch(q1[j:j + 1], k, TAU, scan=scan)
+        dt = (time.perf_counter() - t1) / 8
+        out[f"e2e_b1_{scan}"] = {"value": 1.0 / dt, "unit": "lookups/s",
+                                 "api": "GpuCosineIndex.query_batch (sine_query), one query per call",
+                                 "h2d_bytes_per_step": d * 8, "d2h_bytes_per_step": k * 16 + 4}
+    # roofline of the HBM-bound B = 1 scans (algorithmic bytes over the batch time)
+    out["roofline"] = {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
+                       "b1": {r["scan"]: {"achieved": algorithmic_bytes(n, d, 1, k, r["scan"]) /
+                                          (r["ms_per_batch"] / 1e3) / 1e9, "frac": r["hbm_frac"]}
+                              for r in out["regimes"] if r["batch"] == 1},
+                       "traffic_b1_fp32": "ncu: 40.96 GB DRAM read per launch = the algorithmic bytes "
+                                          "(profiles/r02/ncu_cfgc_b1f32.txt)"}
     del idx
     torch.cuda.empty_cache()
+    if host is not None:
+        # CPU baseline: the reference's ExactCosineIndex.query on the same 10M x
+        # 1024 float64 matrix (populated directly), 2 queries
+        cls, kind = reference_exact_index()
+        if cls is not None:
+            ref = cls(d)
+            ref._ids = list(range(1, n + 1))
+            ref._pos = None  # query() does not read it
+            ref._vecs = host
+        else:
+            from oracle import sine_oracle as O
+            ref = O.OracleExactIndex(d, capacity=1)
+            ref._buf = host
+            ref._ids = list(range(1, n + 1))
+        t1 = time.perf_counter()
+        for j in range(2):
+            ref.query(qs[j], k, min_similarity=TAU)
+        dt = (time.perf_counter() - t1) / 2
+        out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "lookups/s", "cores": cpu_threads(), "kind": kind,
+                               "sample": "2 queries through " + ("semcache.index.ExactCosineIndex.query "
+                                                                 "(oracle/_ref)" if kind == "reference" else
+                                                                 "the oracle restatement") +
+                                         " on the same 10M x 1024 float64 rows (82 GB host)"}
+        del ref, host
     return out
 
 
