@@ -313,14 +313,19 @@ def run_ours(args):
             idx.query_device_cert(b, q_dev[s].data_ptr(), K, TAU, ids_log[s].data_ptr(), sims_log[s].data_ptr(),
                                   cnt_log[s].data_ptr(), cert_log[s].data_ptr(), stream)
 
-        def fix_uncertified(s0, s1):
-            bad = (cert_log[s0:s1] == 0).nonzero().tolist()  # one device->host read per pass
-            for s_, j_ in bad:
-                s_ += s0
-                idx.query_device(1, q_dev[s_, j_].data_ptr(), K, TAU, ids_log[s_, j_].data_ptr(),
-                                 sims_log[s_, j_].data_ptr(), cnt_log[s_, j_:j_ + 1].data_ptr(), stream,
+        def fix_uncertified(s0, s1):  # one device->host read per pass; the re-runs as one batch
+            bad = (cert_log[s0:s1] == 0).nonzero()
+            nbad = int(bad.shape[0])
+            if nbad:
+                si, ji = bad[:, 0] + s0, bad[:, 1]
+                qb = q_dev[si, ji].contiguous()
+                ib = torch.empty((nbad, K), dtype=torch.int64, device=q_dev.device)
+                sb = torch.empty((nbad, K), dtype=torch.float64, device=q_dev.device)
+                cb = torch.empty((nbad,), dtype=torch.int32, device=q_dev.device)
+                idx.query_device(nbad, qb.data_ptr(), K, TAU, ib.data_ptr(), sb.data_ptr(), cb.data_ptr(), stream,
                                  certify=True)
-            return len(bad)
+                ids_log[si, ji], sims_log[si, ji], cnt_log[si, ji] = ib, sb, cb
+            return nbad
 
     def barrier():
         torch.cuda.synchronize()
@@ -610,12 +615,18 @@ def measure_regimes(idx, rows, torch, hbm_peak, tensor_peak):
                     scan=scan, cuda_core=path == "cuda_core", umma_v1=path == "umma_v1", pair=path == "pair",
                     gemm=False if path == "pair" else None)
 
-                def fix():
-                    bad = (cert == 0).nonzero().flatten().tolist()
-                    for j in bad:
-                        idx.query_device(1, q[j].data_ptr(), K, tau, ids[j].data_ptr(), sims[j].data_ptr(),
-                                         cnt[j:j + 1].data_ptr(), stream, certify=True)
-                    return len(bad)
+                def fix():  # the uncertified queries re-run exactly, as one batch (one more pass)
+                    bad = (cert == 0).nonzero().flatten()
+                    nbad = int(bad.numel())
+                    if nbad:
+                        qb = q[bad].contiguous()
+                        ib = torch.empty((nbad, K), dtype=torch.int64, device="cuda")
+                        sb = torch.empty((nbad, K), dtype=torch.float64, device="cuda")
+                        cb = torch.empty((nbad,), dtype=torch.int32, device="cuda")
+                        idx.query_device(nbad, qb.data_ptr(), K, tau, ib.data_ptr(), sb.data_ptr(), cb.data_ptr(),
+                                         stream, certify=True)
+                        ids[bad], sims[bad], cnt[bad] = ib, sb, cb
+                    return nbad
 
                 run()
                 uncert = fix()
