@@ -1442,19 +1442,36 @@ int64_t certify_and_fix(sine_index* h, int64_t B, const double* q_dev, int k, do
     }
     const bool exact_path_used = !bf16 && (mode & SINE_SCAN_CUDA_CORE);
     if (exact_path_used) return 0;
-    int64_t fixed = 0;
-    DevBuf<double> one_q;
-    one_q.ensure(h->dim);
-    for (int64_t b = 0; b < B; ++b) {
-        if (cert[b]) continue;
-        CK(cudaMemcpyAsync(one_q.p, q_dev + b * h->dim, h->dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        const uint32_t m2 = SINE_SCAN_F32 | SINE_RERANK_F64 | SINE_SCAN_CUDA_CORE;
-        query_device_impl(h, 1, one_q.p, k, min_sim, m2, ids_dev + b * k, sims_dev + b * k, counts_dev + b, st);
-        ++fixed;
+    // the failing queries re-run on the exact fp32 CUDA-core scan as ONE
+    // batch (one more pass over the rows, not one per query), then their
+    // results are copied back into place
+    std::vector<int64_t> bad;
+    for (int64_t b = 0; b < B; ++b)
+        if (!cert[b]) bad.push_back(b);
+    const int64_t R = static_cast<int64_t>(bad.size());
+    if (R == 0) return 0;
+    DevBuf<double> rq;
+    DevBuf<int64_t> rid;
+    DevBuf<double> rsim;
+    DevBuf<int32_t> rcnt;
+    rq.ensure(R * h->dim);
+    rid.ensure(R * k);
+    rsim.ensure(R * k);
+    rcnt.ensure(R);
+    for (int64_t r = 0; r < R; ++r)
+        CK(cudaMemcpyAsync(rq.p + r * h->dim, q_dev + bad[r] * h->dim, h->dim * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+    const uint32_t m2 = SINE_SCAN_F32 | SINE_RERANK_F64 | SINE_SCAN_CUDA_CORE;
+    query_device_impl(h, R, rq.p, k, min_sim, m2, rid.p, rsim.p, rcnt.p, st);
+    for (int64_t r = 0; r < R; ++r) {
+        const int64_t b = bad[r];
+        // (the destinations may be mapped host staging: cudaMemcpyDefault)
+        CK(cudaMemcpyAsync(ids_dev + b * k, rid.p + r * k, k * sizeof(int64_t), cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(sims_dev + b * k, rsim.p + r * k, k * sizeof(double), cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(counts_dev + b, rcnt.p + r, sizeof(int32_t), cudaMemcpyDefault, st));
     }
-    if (fixed) CK(cudaStreamSynchronize(st));
-    one_q.release();
-    return fixed;
+    CK(cudaStreamSynchronize(st));
+    return R;
 }
 
 void check_queries_host(const sine_index* h, int64_t B, const double* q) {
