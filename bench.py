@@ -230,7 +230,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: standard-normal rows normalised in float64 (seed 1); queries half planted "
                     "near-duplicates (cos 0.88-0.99), half random",
-            "config": dict(workload_config(args, world, args.rows // world), sampled_lookups_per_step=per_step),
+            "config": workload_config(args, world, args.rows // world),  # the GPU arm's dict, key for key
             "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": cores, "kind": kind,
                              "sample": f"{n} lookups ({per_step} of each step's batch): {what}, numpy float64 "
                                        f"GEMV + lexsort, {cores} BLAS threads"},

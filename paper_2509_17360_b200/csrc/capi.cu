@@ -2217,8 +2217,8 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out, h->vids.p, total * 8, cudaMemcpyDeviceToHost, h->stream));
         int32_t* slots = nullptr;  // pinned staging: the host tables drop these slots
+        h->cnt_h.ensure(total);    // sized by listing calls too: a later purge finds it ready
         if (remove) {
-            h->cnt_h.ensure(total);
             slots = h->cnt_h.p;
             CK(cudaMemcpyAsync(slots, h->vslots.p, total * 4, cudaMemcpyDeviceToHost, h->stream));
         }
@@ -2231,15 +2231,21 @@ int sine_expired(sine_index_t* h, double now, int remove, int64_t* out, int64_t 
             ++h->launches;
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(h->stream));
-            std::vector<int32_t> by_id(slots, slots + total);  // the reference removes sorted(expired)
-            if (!h->ids_ascending)
+            // the reference removes sorted(expired): with slots in id order the
+            // slot list already is that order (no copy, no sort)
+            std::vector<int32_t> by_id;
+            const int32_t* order = slots;
+            if (!h->ids_ascending) {
+                by_id.assign(slots, slots + total);
                 std::sort(by_id.begin(), by_id.end(),
                           [&](int32_t a, int32_t b) { return h->ids_h[a] < h->ids_h[b]; });
-            for (int32_t sl : by_id) {
-                if (!h->ids_ascending) h->pos.erase(h->ids_h[sl]);
-                h->live_h[sl] = 0;
-                order_removed(h, sl);
+                order = by_id.data();
+                for (int64_t i = 0; i < total; ++i) h->pos.erase(h->ids_h[order[i]]);
             }
+            uint8_t* live = h->live_h.data();
+            for (int64_t i = 0; i < total; ++i) live[order[i]] = 0;
+            h->order_log.reserve(h->order_log.size() + total);
+            for (int64_t i = 0; i < total; ++i) order_removed(h, order[i]);
             h->nlive -= total;
             maybe_compact(h);
         }
