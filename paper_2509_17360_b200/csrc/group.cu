@@ -207,6 +207,7 @@ int sine_group_create(sine_index_t* const* shards, const int* devices, int n, in
 int sine_group_destroy(sine_group_t* g) {
     return group_guarded([&] {
         if (!g) return;
+        std::unique_lock<std::mutex> one(g->mu_query);  // a running query finishes first
         {
             std::lock_guard<std::mutex> lk(g->mu);
             g->quit = true;
@@ -220,6 +221,7 @@ int sine_group_destroy(sine_group_t* g) {
         }
         cudaSetDevice(g->root);
         cudaStreamDestroy(g->root_stream);
+        one.unlock();  // before the mutex goes away with the group
         delete g;
     });
 }
