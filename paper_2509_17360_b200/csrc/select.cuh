@@ -69,7 +69,7 @@ struct SelCtl {
     int32_t nb;        // buckets
     int32_t cutb;      // bucket holding the last victim
     int32_t nbig;      // buckets above the cap
-    int32_t pad;
+    int32_t bnext;     // sort kernel: next bucket to take
     unsigned long long count;  // records
     unsigned long long wtake;  // their size
     unsigned long long rand[3], ror[3];  // AND / OR of the record keys (host presets ~0 / 0)
@@ -151,29 +151,33 @@ __device__ __forceinline__ void block_and_or3(uint64_t a[3], uint64_t o[3], unsi
     for (int w = 0; w < 3; ++w) a[w] = sa[w], o[w] = so[w];
 }
 
+// Word w of a 192-bit key (k0 most significant) without a local array:
+// a runtime index into {k0, k1, k2} would put the key in local memory.
+__device__ __forceinline__ uint64_t key_word(uint64_t k0, uint64_t k1, uint64_t k2, int w) {
+    return w == 0 ? k0 : (w == 1 ? k1 : (w == 2 ? k2 : 0ull));
+}
+
 // 64 bits of the 192-bit key starting at its first bit that varies over a
 // set (given the set's AND / OR): order-preserving up to ties for the set.
 __device__ __forceinline__ uint64_t key_window(uint64_t k0, uint64_t k1, uint64_t k2, const uint64_t a[3],
                                                const uint64_t o[3]) {
-    const uint64_t k[3] = {k0, k1, k2};
     int p = 192;
 #pragma unroll
     for (int w = 2; w >= 0; --w)
         if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
     if (p >= 192) return 0;
     const int w = p >> 6, off = p & 63;
-    uint64_t v = k[w] << off;
-    if (off && w < 2) v |= k[w + 1] >> (64 - off);
+    uint64_t v = key_word(k0, k1, k2, w) << off;
+    if (off) v |= key_word(k0, k1, k2, w + 1) >> (64 - off);
     return v;
 }
 
 // 64 bits of the 192-bit key from big-endian bit p (zero-padded past 192).
 __device__ __forceinline__ uint64_t key_window_at(uint64_t k0, uint64_t k1, uint64_t k2, int p) {
     if (p >= 192) return 0;
-    const uint64_t k[3] = {k0, k1, k2};
     const int w = p >> 6, off = p & 63;
-    uint64_t v = k[w] << off;
-    if (off && w < 2) v |= k[w + 1] >> (64 - off);
+    uint64_t v = key_word(k0, k1, k2, w) << off;
+    if (off) v |= key_word(k0, k1, k2, w + 1) >> (64 - off);
     return v;
 }
 
@@ -196,8 +200,8 @@ __device__ __forceinline__ void slot_keys(const EvictCols& c, int64_t s, int pol
 // 8 bits of a 192-bit key at big-endian bit q (q + 8 <= 192).
 __device__ __forceinline__ uint32_t key_digit8(const uint64_t k[3], int q) {
     const int w = q >> 6, off = q & 63;
-    uint64_t v = k[w] << off;
-    if (off > 56) v |= k[w + 1] >> (64 - off);
+    uint64_t v = key_word(k[0], k[1], k[2], w) << off;
+    if (off > 56) v |= key_word(k[0], k[1], k[2], w + 1) >> (64 - off);
     return static_cast<uint32_t>(v >> 56);
 }
 
@@ -1029,7 +1033,17 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_sort_kernel(SelCtl* ctl, 
     ctl_and_or(ctl, ga, go);
     const int pg = first_varying(ga, go);
     const uint64_t wmin = ctl->wmin, wmax = ctl->wmax;
-    for (int b = blockIdx.x; b <= cutb; b += gridDim.x) {
+    __shared__ int next_b;
+    for (;;) {
+        // buckets from a queue (the cut bucket first: its scan is the longest)
+        if (threadIdx.x == 0) {
+            const int t = atomicAdd(&ctl->bnext, 1);
+            next_b = t == 0 ? cutb : (t <= cutb ? t - 1 : cutb + 1);
+        }
+        __syncthreads();
+        const int b = next_b;
+        __syncthreads();
+        if (b > cutb) break;
         const int64_t n = static_cast<int64_t>(bcnt[b]);
         const int64_t base = boff[b];
         if (n == 0) {
