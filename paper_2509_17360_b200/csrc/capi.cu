@@ -797,10 +797,10 @@ int res_nq_max(int64_t row_bytes) {
     return n >= 64 ? 64 : n >= 32 ? 32 : n >= 16 ? 16 : 0;
 }
 
-template <int NQ, int CS>
+template <int NQ, int CS, bool kHelp = false>
 int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters, size_t smem,
                cudaStream_t st) {
-    auto kern = umma_res_kernel<NQ, CS>;
+    auto kern = umma_res_kernel<NQ, CS, kHelp>;
     smem_optin(reinterpret_cast<const void*>(kern), 227 * 1024);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -808,7 +808,7 @@ int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams
     at[0].val.clusterDim.x = CS;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(kUmmaThreads);
+    cfg.blockDim = dim3(kUmmaThreads + (kHelp ? kUmmaHelperThreads : 0));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = at;
@@ -819,15 +819,16 @@ int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams
     static std::mutex occ_mu;
     static std::unordered_map<size_t, int> occ;
     int active = 0;
+    const size_t okey = smem;  // per instantiation (static locals are per template)
     {
         std::lock_guard<std::mutex> g(occ_mu);
-        auto it = occ.find(smem);
+        auto it = occ.find(okey);
         if (it != occ.end()) active = it->second;
     }
     if (!active) {
         CK(cudaOccupancyMaxActiveClusters(&active, kern, &cfg));
         std::lock_guard<std::mutex> g(occ_mu);
-        occ[smem] = active;
+        occ[okey] = active;
     }
     const int ncl = std::max(1, std::min(max_clusters, active));
     cfg.gridDim = dim3(ncl * CS);
@@ -843,6 +844,8 @@ int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams
 template <int NQ>
 int launch_res_cs(int CS, const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters,
                   size_t smem, cudaStream_t st) {
+    if constexpr (NQ == 16)
+        if (p.ffma == 3) return launch_res<16, 1, true>(qmap, rmap, p, max_clusters, smem, st);
     switch (CS) {
         case 1: return launch_res<NQ, 1>(qmap, rmap, p, max_clusters, smem, st);
         case 2: return launch_res<NQ, 2>(qmap, rmap, p, max_clusters, smem, st);
@@ -875,11 +878,31 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         const int64_t per = (rem + CS - 1) / CS;
         const int NQ = std::min(NQmax, per <= 16 ? 16 : per <= 32 ? 32 : 64);
         const int nq = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(CS) * NQ, rem));
-        const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp);
+        // a single query: CUDA-core FFMA on the TMA-staged tiles instead of
+        // N = 16 MMAs that are 15/16 padding.  Default (p.ffma = 3): eight
+        // dot-product warps split each tile's K blocks by ring parity and
+        // hand scores to the four list warps through a 16-tile ring, so list
+        // upkeep overlaps the HBM stream.  Same box, config B, B = 1
+        // lookups/s, MMA path -> helper mode: bf16 tau 0.9 3583 -> 4352,
+        // tau -1 3316 -> 4051; fp32 tau -1 2058 -> 2214 (scalar FFMA in the
+        // list warps); headline 2184 -> 2239.  Opt-outs for A/B timing:
+        // SINE_NO_FFMA=1 keeps the MMAs; SINE_FFMA_LIST=1 computes in the four
+        // list warps (scalar FFMA for fp32 rows, FFMA2 with SINE_FFMA2=1 or
+        // for bf16 rows), the round-2 single-group path.
+        static const bool ffma_on = getenv("SINE_NO_FFMA") == nullptr;
+        static const bool ffma_list = getenv("SINE_FFMA_LIST") != nullptr;
+        static const bool ffma2 = getenv("SINE_FFMA2") != nullptr;
+        const int ffma = ffma_on && CS == 1 && nq == 1 && NQ == 16 ? (!ffma_list ? 3 : tf32 && !ffma2 ? 1 : 2) : 0;
+        const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp, -1, ffma == 3);
         if (L0.total + 2 * kUmmaN * kUmmaKB > 227 * 1024) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
-        const int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
+        int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
+        // helper mode: an even ring, so every stage belongs to one dot-product
+        // group (ring index parity == stage parity).  With an odd ring a group
+        // could wait on a stage the other group still owns one lap behind and
+        // read the wrong mbarrier phase.
+        if (ffma == 3) S &= ~1;
         if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
-        const ResSmem L = res_smem_layout(S, NQ, kblocks, kp);
+        const ResSmem L = res_smem_layout(S, NQ, kblocks, kp, -1, ffma == 3);
         h->gbound.ensure(static_cast<size_t>(kMaxCS) * NQmax);
         res_prep_queries<<<grid_for(static_cast<int64_t>(CS) * NQ * row_elems, 256, h->num_sms), 256, 0, st>>>(
             q_dev + q0 * h->dim, nq, CS * NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p, h->gbound.p,
@@ -899,21 +922,7 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.slot_ids = h->ids_ascending ? 1 : 0;
         p.gbound = h->gbound.p;  // zeroed by res_prep_queries
         p.tile_stride = 1;
-        // a single query over fp32 rows: FFMA2 on the staged tiles instead
-        // of N = 16 MMAs that are 15/16 padding.  Same box, config B, B = 1:
-        // 2166-2177 vs 1851-1862 lookups/s (kernel 0.451 vs 0.521 ms).  bf16
-        // rows carry twice the elements per byte and the four epilogue warps
-        // also keep the top-k lists: even with packed FFMA2 and the query
-        // widened once in smem they lose (3418 vs 3709 at tau 0.9, 2660 vs
-        // 3404 at tau -1), so they keep the MMAs unless SINE_FFMA_BF16=1.
-        // SINE_NO_FFMA=1 keeps the MMAs for fp32 rows too (A/B timing).
-        // fp32 rows use scalar FFMA in four chains: packed FFMA2 measured
-        // slower on the same box (headline kernel 0.479 vs 0.449 ms, 2040 vs
-        // 2189 lookups/s), so it is opt-in (SINE_FFMA2=1).
-        static const bool ffma_on = getenv("SINE_NO_FFMA") == nullptr;
-        static const bool ffma_bf16 = getenv("SINE_FFMA_BF16") != nullptr;
-        static const bool ffma2 = getenv("SINE_FFMA2") != nullptr;
-        p.ffma = ffma_on && (tf32 || ffma_bf16) && CS == 1 && nq == 1 && NQ == 16 ? (tf32 && !ffma2 ? 1 : 2) : 0;
+        p.ffma = ffma;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;

@@ -409,7 +409,8 @@ struct ResParams {
     int tile_stride;   // 1 = every tile; >1 = sample pass over every tile_stride-th tile
     int ffma;          // single query: the epilogue warps take the dot products on the CUDA
                        //     cores straight from the TMA-staged tiles (no MMAs): 1 = scalar
-                       //     FFMA (fp32 rows), 2 = packed FFMA2
+                       //     FFMA (fp32 rows), 2 = packed FFMA2, 3 = scalar FFMA split with
+                       //     four helper warps (launched with kUmmaHelperThreads more threads)
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -423,13 +424,17 @@ struct ResParams {
 constexpr int kSparse = 128;     // (query, row) pairs per tile handed to the sparse inserter
 constexpr int kSparseRows = 32;  // tiles with more passing rows take the dense (bitonic) rounds
 
+constexpr int kScoreRing = 16;  // FFMA helper mode: tiles of partial scores in flight to the list warps
+
 struct ResSmem {
-    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, sparse_off, fq_off, total;
+    size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, sparse_off, fq_off, pb_off, total;
 };
 
 // Nq_res: queries resident in this CTA's shared memory (== Nq except for the
 // CTA pair, where each CTA holds half of the Nq queries it scores).
-__host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, int kp, int Nq_res = -1) {
+// helpers: room for the FFMA helper mode's score ring (p.ffma == 3 only).
+__host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, int kp, int Nq_res = -1,
+                                                   bool helpers = false) {
     ResSmem L;
     size_t off = 0;
     L.q_off = off;
@@ -458,6 +463,8 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     off = (off + 15) / 16 * 16;
     L.fq_off = off;  // FFMA mode: the single query in fp32, one 128-B K block -> kUmmaKB / 2 floats (bf16 rows)
     off += static_cast<size_t>(kblocks) * (kUmmaKB / 2) * 4;
+    L.pb_off = off;  // FFMA helper mode: score ring, kScoreRing x {full, empty} mbarriers + [ring][2][128] fp32
+    if (helpers) off += 2 * kScoreRing * 8 + static_cast<size_t>(kScoreRing) * 2 * 128 * 4;
     L.total = off + 1024;
     return L;
 }
@@ -640,18 +647,71 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
+constexpr int kUmmaHelperThreads = 256;  // FFMA helper mode: eight dot-product warps
+
+// Single-query FFMA (helper mode, p.ffma == 3) over the K blocks of local
+// tile i whose ring index g = i * nkb + kb (the producer's issue order) has
+// parity `par`: dot-product warps 6-9 take the even stages and warps 10-13
+// the odd ones, so both groups read adjacent stages at once.  Stage g sits
+// at g % S with phase (g / S) & 1; S is even, so each stage has one owning
+// group and a group never waits on a stage the other may be a lap behind
+// on.  Each warp releases the stages it read (four arrivals per stage).
+__device__ __forceinline__ float ffma_kpar(int i, int par, int nkb, int S, int row, bool tf32, const uint8_t* sa,
+                                           const uint8_t* sq, int NQ, const float* fq, uint64_t* full,
+                                           uint64_t* empty, int lane) {
+    float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
+    const int sw = row & 7;
+    const int g0 = i * nkb;
+    for (int kb = ((g0 & 1) == par) ? 0 : 1; kb < nkb; kb += 2) {
+        const int g = g0 + kb;
+        const int s = g % S;
+        mbar_wait(full + s, static_cast<uint32_t>((g / S) & 1));
+        const uint8_t* rowp = sa + static_cast<size_t>(s) * kUmmaN * kUmmaKB + row * kUmmaKB;
+        if (tf32) {
+            const uint8_t* qp = sq + static_cast<size_t>(kb) * NQ * kUmmaKB;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+                const uint4 qv = *reinterpret_cast<const uint4*>(qp + (c << 4));
+                f0 = fmaf(__uint_as_float(xv.x), __uint_as_float(qv.x), f0);
+                f1 = fmaf(__uint_as_float(xv.y), __uint_as_float(qv.y), f1);
+                f2 = fmaf(__uint_as_float(xv.z), __uint_as_float(qv.z), f2);
+                f3 = fmaf(__uint_as_float(xv.w), __uint_as_float(qv.w), f3);
+            }
+        } else {
+            const float4* qf = reinterpret_cast<const float4*>(fq + kb * (kUmmaKB / 2));
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+                const float4 q0 = qf[2 * c], q1 = qf[2 * c + 1];
+                f0 = fmaf(__uint_as_float(xv.x << 16), q0.x, f0);
+                f1 = fmaf(__uint_as_float(xv.x & 0xffff0000u), q0.y, f1);
+                f2 = fmaf(__uint_as_float(xv.y << 16), q0.z, f2);
+                f3 = fmaf(__uint_as_float(xv.y & 0xffff0000u), q0.w, f3);
+                f0 = fmaf(__uint_as_float(xv.z << 16), q1.x, f0);
+                f1 = fmaf(__uint_as_float(xv.z & 0xffff0000u), q1.y, f1);
+                f2 = fmaf(__uint_as_float(xv.w << 16), q1.z, f2);
+                f3 = fmaf(__uint_as_float(xv.w & 0xffff0000u), q1.w, f3);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+    return (f0 + f2) + (f1 + f3);
+}
+
 // CS = thread-block cluster size.  The CS CTAs of a cluster hold CS
 // different query groups (NQ each) and share every 128-row tile: each CTA
 // TMA-loads 128/CS rows of it and multicasts them to the whole cluster, so
 // one HBM pass over the index serves CS * NQ queries.
-template <int NQ, int CS>
-__global__ void __launch_bounds__(kUmmaThreads, 1)
+template <int NQ, int CS, bool kHelp>
+__global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kUmmaThreads, 1)
     umma_res_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
                     const ResParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages, nkb = p.kblocks, kp = p.kp;
-    const ResSmem L = res_smem_layout(S, NQ, nkb, kp);
+    const ResSmem L = res_smem_layout(S, NQ, nkb, kp, -1, kHelp);
     uint8_t* sq = smem + L.q_off;
     uint8_t* sa = smem + L.a_off;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -679,13 +739,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             mbar_init(full + s, 1);
             // released by the MMA commits of every CTA in the cluster, or by
             // the four epilogue warps in the FFMA (single-query) mode
-            mbar_init(empty + s, p.ffma ? 4 : CS);
+            mbar_init(empty + s, p.ffma ? 4 : CS);  // helper mode: one group of four warps per stage
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 4);
         }
         mbar_init(qfull, 1);
+        if constexpr (kHelp) {
+            uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + L.pb_off);
+            for (int r = 0; r < kScoreRing; ++r) {
+                mbar_init(sfull + r, 8);               // both dot-product groups wrote their partials
+                mbar_init(sfull + kScoreRing + r, 4);  // the list warps read them
+            }
+        }
         fence_mbar_init();
     }
     for (int j = threadIdx.x; j < NQ; j += blockDim.x) {
@@ -798,6 +865,28 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 umma_commit(tfull + acc);
             }
         }
+    } else if (kHelp && warp >= 6) {
+        // ---------------- FFMA dot-product warps (p.ffma == 3) ----------------
+        // two groups of four split each tile's K blocks by ring parity and
+        // hand the partial scores to the list warps through a ring of
+        // kScoreRing tiles, so list upkeep never stalls the HBM stream
+        const int grp = (warp - 6) >> 2;
+        const int row = threadIdx.x - kUmmaThreads - grp * 128;
+        const float* fq = reinterpret_cast<const float*>(smem + L.fq_off);
+        uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + L.pb_off);
+        uint64_t* sempty = sfull + kScoreRing;
+        float* sring = reinterpret_cast<float*>(sempty + kScoreRing);
+        mbar_wait(qfull, 0);
+        named_bar_sync(3, 128 + kUmmaHelperThreads);  // the list warps widened the bf16 query into fq
+        int i = 0;
+        for (int t = cid; t < p.ntiles; t += ncl, ++i) {
+            const float part = ffma_kpar(i, grp, nkb, S, row, p.tf32 != 0, sa, sq, NQ, fq, full, empty, lane);
+            const int r = i % kScoreRing;
+            mbar_wait(sempty + r, static_cast<uint32_t>(((i / kScoreRing) & 1) ^ 1));
+            sring[(r * 2 + grp) * 128 + row] = part;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sfull + r);
+        }
     } else {
         // ---------------- epilogue: thread = row ----------------
         pdl_wait();  // the admission bounds come from the query-prep kernel
@@ -817,7 +906,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 }
                 named_bar_sync(2, 128);
             }
+            if constexpr (kHelp) named_bar_sync(3, 128 + kUmmaHelperThreads);
         }
+        uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + L.pb_off);
+        const float* sring = reinterpret_cast<const float*>(sfull + 2 * kScoreRing);
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
             const int64_t slot = static_cast<int64_t>(t) * p.tile_stride * kUmmaN + tid;
@@ -831,7 +923,15 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
             named_bar_sync(2, 128);
             float sc[NQ];
-            if (p.ffma) {
+            if constexpr (kHelp) {
+                const int r = i % kScoreRing;
+                mbar_wait(sfull + r, static_cast<uint32_t>((i / kScoreRing) & 1));
+                sc[0] = (sring[(r * 2) * 128 + tid] + sring[(r * 2 + 1) * 128 + tid]) + 0.0f;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sfull + kScoreRing + r);
+#pragma unroll
+                for (int j = 1; j < NQ; ++j) sc[j] = 0.0f;
+            } else if (p.ffma) {
                 // one query: the dot products on the CUDA cores with packed
                 // FFMA2 (two fp32 lanes per instruction), read from the
                 // 128B-swizzled stages (16-B chunk c of row r sits at chunk
