@@ -221,7 +221,7 @@ struct sine_index {
     // victim selection (select.cuh): records below the sampled bound, the
     // same in bucket order, bucket of each record, splitters, per-bucket
     // count / size, offsets, cursors, oversized buckets, control block
-    DevBuf<SelRec> srec, srec2;
+    DevBuf<SelRec> srec, srec2, ssamp;
     DevBuf<uint16_t> sbid;
     DevBuf<uint32_t> sspl, stab;
     DevBuf<unsigned long long> sbcnt;
@@ -278,6 +278,24 @@ namespace {
 bool pdl_enabled() {
     static const bool on = getenv("SINE_NO_PDL") == nullptr;
     return on;
+}
+
+// Launch with programmatic dependent launch (the kernel calls pdl_wait()
+// before reading its predecessor's output): the launch latency of a chain
+// of short dependent kernels overlaps the predecessor's tail.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -1547,16 +1565,16 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
     const int scap = h->sel_cap;
     // small stores skip the sample: every live slot is a record
     bool all = h->nlive <= scap;
+    h->ssamp.ensure(kSelSample);
     for (int attempt = 0; attempt < 2; ++attempt) {
-        SelCtl c0{};
-        c0.all = all ? 1 : 0;
-        for (int w = 0; w < 3; ++w) c0.rand[w] = ~0ull;
-        c0.wmin = ~0ull;
-        *h->sctl_h.p = c0;
-        CK(cudaMemcpyAsync(h->sctl.p, h->sctl_h.p, sizeof(SelCtl), cudaMemcpyHostToDevice, st));
-        CK(cudaMemsetAsync(bcnt, 0, 2 * kSelMaxBuckets * sizeof(unsigned long long), st));
+        // init (ctl preset, bucket counters, the sample gather), then the
+        // chain below under PDL
+        sel_init_kernel<<<kSelSample / kSelInitThreads, kSelInitThreads, 0, st>>>(
+            cols, policy, now, slot_tie, all ? 1 : 0, h->sctl.p, bcnt, 2 * kSelMaxBuckets, h->ssamp.p);
+        ++h->launches;
         if (!all) {
-            sel_sample_kernel<<<1, 1024, 0, st>>>(cols, policy, now, h->nlive, excess, slot_tie, h->sctl.p);
+            launch_pdl(sel_sample_kernel, 1, 1024, 0, st, static_cast<const SelRec*>(h->ssamp.p), h->nlive, excess,
+                       h->sctl.p);
             ++h->launches;
         }
         SelColumns sc{};
@@ -1572,21 +1590,28 @@ void select_victims_impl(sine_index* h, int policy, double now, int64_t excess, 
         }
         const int64_t tiles = (h->nslots + kSelTile - 1) / kSelTile;
         const int gcol = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, h->num_sms)));
-        sel_collect_kernel<<<gcol, kSelCollectThreads, kSelCollectSmem, st>>>(cols, sc, policy, now, slot_tie,
-                                                                             h->sctl.p, h->srec.p);
-        sel_split_kernel<<<1, 1024, 0, st>>>(excess, h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, scap);
+        launch_pdl(sel_collect_kernel, gcol, kSelCollectThreads, kSelCollectSmem, st, cols, sc, policy, now, slot_tie,
+                   h->sctl.p, h->srec.p);
+        launch_pdl(sel_split_kernel, 1, 1024, 0, st, excess, h->sctl.p, static_cast<const SelRec*>(h->srec.p),
+                   h->sspl.p, h->stab.p, scap);
         // bucket and scatter must split the records the same way (same grid)
         const int grec = h->num_sms;
-        sel_bucket_kernel<<<grec, 1024, kSelBucketSmem, st>>>(h->sctl.p, h->srec.p, h->sspl.p, h->stab.p, h->sbid.p,
-                                                              bcnt, bw);
-        sel_scan_kernel<<<1, 1024, 0, st>>>(h->sctl.p, excess, bcnt, bw, h->sboff.p, h->sbcur.p);
-        sel_scatter_kernel<<<grec, 1024, 0, st>>>(h->sctl.p, h->srec.p, h->sbid.p, h->sboff.p, h->sbcur.p,
-                                                  h->srec2.p);
-        sel_sort_kernel<<<3 * h->num_sms, kSelSortThreads, kSelCountSmem, st>>>(
-            h->sctl.p, excess, slot_tie, h->ids, h->sspl.p, h->srec2.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap, oslot);
-        sel_big_kernel<<<h->num_sms, kSelSortThreads, kSelSortSmem, st>>>(
-            h->sctl.p, excess, slot_tie, h->ids, h->srec2.p, h->srec.p, h->sboff.p, bcnt, h->sbig.p, h->vids.p, scap,
-            oslot);
+        launch_pdl(sel_bucket_kernel, grec, 1024, kSelBucketSmem, st, h->sctl.p, static_cast<const SelRec*>(h->srec.p),
+                   static_cast<const uint32_t*>(h->sspl.p), static_cast<const uint32_t*>(h->stab.p), h->sbid.p, bcnt,
+                   bw);
+        launch_pdl(sel_scan_kernel, 1, 1024, 0, st, h->sctl.p, excess, static_cast<const unsigned long long*>(bcnt),
+                   static_cast<const unsigned long long*>(bw), h->sboff.p, h->sbcur.p);
+        launch_pdl(sel_scatter_kernel, grec, 1024, 0, st, static_cast<const SelCtl*>(h->sctl.p),
+                   static_cast<const SelRec*>(h->srec.p), static_cast<const uint16_t*>(h->sbid.p),
+                   static_cast<const int64_t*>(h->sboff.p), h->sbcur.p, h->srec2.p);
+        launch_pdl(sel_sort_kernel, 3 * h->num_sms, kSelSortThreads, kSelCountSmem, st, h->sctl.p, excess, slot_tie,
+                   static_cast<const int64_t*>(h->ids), static_cast<const uint32_t*>(h->sspl.p),
+                   static_cast<const SelRec*>(h->srec2.p), static_cast<const int64_t*>(h->sboff.p),
+                   static_cast<const unsigned long long*>(bcnt), h->sbig.p, h->vids.p, scap, oslot);
+        launch_pdl(sel_big_kernel, h->num_sms, kSelSortThreads, kSelSortSmem, st, h->sctl.p, excess, slot_tie,
+                   static_cast<const int64_t*>(h->ids), h->srec2.p, h->srec.p, static_cast<const int64_t*>(h->sboff.p),
+                   static_cast<const unsigned long long*>(bcnt), static_cast<const int32_t*>(h->sbig.p), h->vids.p,
+                   scap, oslot);
         h->launches += 7;
         CK(cudaGetLastError());
         record(h, 4, st);

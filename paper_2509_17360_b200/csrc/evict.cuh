@@ -34,7 +34,7 @@ __device__ __forceinline__ double lcfu_score(const EvictCols& c, int64_t s, doub
     double v = __dmul_rn(c.lf[s], c.lc[s]);
     v = __dmul_rn(v, c.ll[s]);
     v = __dmul_rn(v, c.ls[s]);
-    return __ddiv_rn(v, static_cast<double>(size));
+    return v != 0.0 ? __ddiv_rn(v, static_cast<double>(size)) : v;  // +-0 either way (f64_key folds -0)
 }
 
 __device__ __forceinline__ uint64_t primary_key(const EvictCols& c, int64_t s, int policy, double now) {

@@ -12,10 +12,12 @@
 //                                  them when the total does not)
 //
 // Pipeline (one stream, one host sync before the result copy):
-//   1 sel_sample_kernel   one CTA: 4096 strided live slots; a weighted
-//                         radix select over their full keys finds the sample
-//                         at the size quantile of the excess plus a 6-sigma
-//                         margin; its key `hi` bounds the victim prefix with
+//   0 sel_init_kernel     SelCtl preset, bucket counters zeroed, 4096
+//                         strided slots' keys and sizes gathered (16 CTAs)
+//   1 sel_sample_kernel   one CTA: a weighted radix select over the samples'
+//                         full keys narrows to the <= 16 samples around the
+//                         size quantile of the excess plus a 6-sigma margin;
+//                         the largest, `hi`, bounds the victim prefix with
 //                         overwhelming probability
 //   2 sel_collect_kernel  THE pass over the store (HBM-bound): each live
 //                         slot's primary key from its columns; slots with
@@ -79,6 +81,7 @@ struct SelCtl {
 };
 
 constexpr int kSelSample = 4096;       // sel_sample_kernel: 1024 threads x 4
+constexpr int kSelSampleKeep = 16;     // sel_sample_kernel: stop narrowing at this many samples
 constexpr int kSelSplitSample = 4096;  // sel_split_kernel: 1024 threads x 4
 constexpr int kSelMaxBuckets = 1024;
 constexpr int kSelSortThreads = 512;
@@ -196,6 +199,37 @@ __device__ __forceinline__ void slot_keys(const EvictCols& c, int64_t s, int pol
     k2 = slot_tie ? static_cast<uint64_t>(s) : i64_key(c.ids[s]);
 }
 
+// ------------------------------------------------------------ 0 init/gather
+// SelCtl preset (ANDs ~0, ORs 0, wmin ~0), bucket counters zeroed, and --
+// unless every live slot becomes a record -- the 4096 strided samples'
+// keys and sizes (size -1: dead slot) gathered by 16 CTAs.  One CTA pulling
+// these scattered columns is bound by a single SM's memory pipe (the
+// one-CTA sample kernel spent 49 us on it); spread out it is one latency.
+constexpr int kSelInitThreads = 256;
+__global__ void __launch_bounds__(kSelInitThreads) sel_init_kernel(const EvictCols c, int policy, double now,
+                                                                   int slot_tie, int all, SelCtl* ctl,
+                                                                   unsigned long long* bcnt, int nbcnt,
+                                                                   SelRec* samp) {
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        SelCtl c0{};
+        c0.all = all;
+        for (int w = 0; w < 3; ++w) c0.rand[w] = ~0ull;
+        c0.wmin = ~0ull;
+        *ctl = c0;
+    }
+    for (int j = i; j < nbcnt; j += gridDim.x * blockDim.x) bcnt[j] = 0;
+    if (!all && i < kSelSample) {
+        const int64_t s = ((2 * static_cast<int64_t>(i) + 1) * c.nslots) / (2 * kSelSample);
+        SelRec r;
+        slot_keys(c, s, policy, now, slot_tie, r.k0, r.k1, r.k2);
+        const int64_t w = c.size[s];
+        r.size = valid_bit(c.valid, s) ? w : -1;
+        samp[i] = r;
+    }
+}
+
 // ---------------------------------------------------------------- 1 sample
 // 8 bits of a 192-bit key at big-endian bit q (q + 8 <= 192).
 __device__ __forceinline__ uint32_t key_digit8(const uint64_t k[3], int q) {
@@ -209,8 +243,8 @@ __device__ __forceinline__ uint32_t key_digit8(const uint64_t k[3], int q) {
 // digits from the first varying bit; a sample stays alive while it matches
 // every chosen digit) until one sample is left: the one where the
 // cumulative size reaches the target.  hi = its full key.
-__global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int policy, double now, int64_t nlive,
-                                                         int64_t excess, int slot_tie, SelCtl* ctl) {
+__global__ void __launch_bounds__(1024) sel_sample_kernel(const SelRec* samp, int64_t nlive, int64_t excess,
+                                                         SelCtl* ctl) {
     __shared__ uint32_t hl[256], hh[256], hc[256];
     __shared__ int64_t wtot[32];
     __shared__ int64_t wsum;
@@ -218,10 +252,11 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
     __shared__ int nvalid, digit, left;
     __shared__ int64_t below;
     constexpr int per = kSelSample / 1024;
+    pdl_wait();  // the samples come from sel_init_kernel
+    pdl_trigger();
     if (threadIdx.x < 3) sa[threadIdx.x] = ~0ull, so[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) nvalid = 0;
     __syncthreads();
-    const int64_t ns = c.nslots;
     uint64_t k[per][3];
     int64_t W[per];
     bool alive[per];
@@ -230,12 +265,10 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
     int64_t wloc = 0;
 #pragma unroll
     for (int j = 0; j < per; ++j) {
-        const int i = per * threadIdx.x + j;
-        const int64_t s = ((2 * static_cast<int64_t>(i) + 1) * ns) / (2 * kSelSample);
-        // loads issued regardless of validity (one latency, not two)
-        alive[j] = valid_bit(c.valid, s);
-        slot_keys(c, s, policy, now, slot_tie, k[j][0], k[j][1], k[j][2]);
-        W[j] = c.size[s];
+        const SelRec r = samp[per * threadIdx.x + j];
+        alive[j] = r.size >= 0;
+        k[j][0] = r.k0, k[j][1] = r.k1, k[j][2] = r.k2;
+        W[j] = r.size;
     }
 #pragma unroll
     for (int j = 0; j < per; ++j) {
@@ -270,7 +303,10 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
         if (a[w] ^ o[w]) p = 64 * w + __clzll(a[w] ^ o[w]);
     int64_t rem = static_cast<int64_t>(ceil(g * static_cast<double>(ws)));
     int nleft = nv;
-    for (int q0 = p; q0 < 192 && nleft > 1;) {
+    // narrow until at most kSelSampleKeep samples share the chosen digits,
+    // then take the largest of them: a bound at or above the quantile sample
+    // (a few more records for collect to keep; each 8-bit pass costs ~3 us)
+    for (int q0 = p; q0 < 192 && nleft > kSelSampleKeep;) {
         const int q = q0 < 184 ? q0 : 184;  // the last digit may overlap fixed bits
         if (threadIdx.x < 256) hl[threadIdx.x] = hh[threadIdx.x] = hc[threadIdx.x] = 0;
         __syncthreads();
@@ -366,20 +402,38 @@ __global__ void __launch_bounds__(1024) sel_sample_kernel(const EvictCols c, int
         q0 = pn > q + 8 ? pn : q + 8;
         __syncthreads();
     }
-    // the surviving sample (keys are unique); `all` when none survived
-    __shared__ int winner;
-    if (threadIdx.x == 0) winner = -1;
-    __syncthreads();
+    // the largest surviving sample (keys are unique); `all` when none survived
+    __shared__ unsigned long long wk[32][3];
+    __shared__ int wany[32];
+    bool any = false;
+    uint64_t m0 = 0, m1 = 0, m2 = 0;
 #pragma unroll
     for (int j = 0; j < per; ++j)
-        if (alive[j]) winner = per * threadIdx.x + j;
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < per; ++j)
-        if (per * static_cast<int>(threadIdx.x) + j == winner) {
-            ctl->hi[0] = k[j][0], ctl->hi[1] = k[j][1], ctl->hi[2] = k[j][2];
+        if (alive[j] && (!any || key_less(m0, m1, m2, k[j][0], k[j][1], k[j][2]))) {
+            m0 = k[j][0], m1 = k[j][1], m2 = k[j][2];
+            any = true;
         }
-    if (threadIdx.x == 0 && winner < 0) ctl->all = 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t o0 = __shfl_xor_sync(0xffffffffu, m0, off), o1 = __shfl_xor_sync(0xffffffffu, m1, off),
+                       o2 = __shfl_xor_sync(0xffffffffu, m2, off);
+        const bool oany = __shfl_xor_sync(0xffffffffu, any, off);
+        if (oany && (!any || key_less(m0, m1, m2, o0, o1, o2))) m0 = o0, m1 = o1, m2 = o2, any = true;
+    }
+    if (lane == 0) wk[warp][0] = m0, wk[warp][1] = m1, wk[warp][2] = m2, wany[warp] = any;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bool f = false;
+        uint64_t b0 = 0, b1 = 0, b2 = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+            if (wany[w] && (!f || key_less(b0, b1, b2, wk[w][0], wk[w][1], wk[w][2])))
+                b0 = wk[w][0], b1 = wk[w][1], b2 = wk[w][2], f = true;
+        if (f)
+            ctl->hi[0] = b0, ctl->hi[1] = b1, ctl->hi[2] = b2;
+        else
+            ctl->all = 1;
+    }
 }
 
 // --------------------------------------------------------------- 2 collect
@@ -431,6 +485,9 @@ __global__ void __launch_bounds__(kSelCollectThreads, 1) sel_collect_kernel(cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nc = cols.ncol;
     const int64_t ntiles = (c.nslots + kSelTile - 1) / kSelTile;
+    // PDL: the producer streams the columns at once (nothing in this launch
+    // chain writes them); the consumers wait for ctl below
+    pdl_trigger();
     if (threadIdx.x == 0) {
         for (int i = 0; i < kSelStages; ++i) {
             mbar_init(full + i, 1);
@@ -460,6 +517,7 @@ __global__ void __launch_bounds__(kSelCollectThreads, 1) sel_collect_kernel(cons
         }
         return;
     }
+    pdl_wait();  // ctl (hi, all, counters) comes from the init / sample kernels
     SelRec* st = wst + warp * kSelWarpStage;
     int nst = 0;
     const int all = ctl->all;
@@ -485,10 +543,14 @@ __global__ void __launch_bounds__(kSelCollectThreads, 1) sel_collect_kernel(cons
                 size = __double_as_longlong(S[5 * kSelTile + j]);
                 created = S[6 * kSelTile + j];
                 double v = 0.0;  // cal_score (engine.py:33-48): exact order, no FMA contraction
-                if (size != 0 && !(__dsub_rn(S[4 * kSelTile + j], now) <= 0.0))
-                    v = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(S[j], S[kSelTile + j]), S[2 * kSelTile + j]),
-                                            S[3 * kSelTile + j]),
-                                  static_cast<double>(size));
+                if (size != 0 && !(__dsub_rn(S[4 * kSelTile + j], now) <= 0.0)) {
+                    v = __dmul_rn(__dmul_rn(__dmul_rn(S[j], S[kSelTile + j]), S[2 * kSelTile + j]),
+                                  S[3 * kSelTile + j]);
+                    // a zero product (log(1) factors are common) divides to
+                    // +-0 (one key); skipping it keeps the IEEE division off
+                    // its slow path, which a zero dividend takes
+                    if (v != 0.0) v = __ddiv_rn(v, static_cast<double>(size));
+                }
                 k0 = f64_key(v);
             } else {
                 size = __double_as_longlong(S[kSelTile + j]);
@@ -559,6 +621,8 @@ using SplitSort = cub::BlockRadixSort<uint32_t, 1024, kSelSplitSample / 1024, cu
 
 __global__ void __launch_bounds__(1024) sel_split_kernel(int64_t excess, SelCtl* ctl, const SelRec* rec,
                                                         uint32_t* spl, uint32_t* tab, int cap) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ typename SplitSort::TempStorage ts;
     __shared__ uint32_t S[kSelMaxBuckets];
     if (!ctl->all && static_cast<int64_t>(ctl->wtake) < excess) {
@@ -633,6 +697,8 @@ __device__ __forceinline__ void cta_range(int64_t M, int64_t& b, int64_t& e) {
 __global__ void __launch_bounds__(1024) sel_bucket_kernel(SelCtl* ctl, const SelRec* rec, const uint32_t* spl,
                                                          const uint32_t* tab, uint16_t* bid,
                                                          unsigned long long* bcnt, unsigned long long* bw) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint64_t sel_smem[];
     if (ctl->retry) return;
     const int nb = ctl->nb, ns = nb - 1;
@@ -652,15 +718,26 @@ __global__ void __launch_bounds__(1024) sel_bucket_kernel(SelCtl* ctl, const Sel
     int64_t b, e;
     cta_range(static_cast<int64_t>(ctl->count), b, e);
     uint64_t wmn = ~0ull, wmx = 0ull;
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-        const SelRec r = rec[i];
-        const uint64_t w64 = key_window_at(r.k0, r.k1, r.k2, pg);
-        wmn = w64 < wmn ? w64 : wmn;
-        wmx = w64 > wmx ? w64 : wmx;
-        const int k = ns ? find_bucket(static_cast<uint32_t>(w64 >> 32), S, T) : 0;
-        bid[i] = static_cast<uint16_t>(k);
-        atomicAdd(&sc[k], 1u);
-        smem_add64(&swl[k], &swh[k], static_cast<uint64_t>(r.size));
+    constexpr int U = 4;  // records per thread per round, loads first (latency-bound rounds)
+    for (int64_t i0 = b + threadIdx.x; i0 < e; i0 += U * blockDim.x) {
+        SelRec r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+            if (i < e) r[u] = rec[i];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+            if (i >= e) continue;
+            const uint64_t w64 = key_window_at(r[u].k0, r[u].k1, r[u].k2, pg);
+            wmn = w64 < wmn ? w64 : wmn;
+            wmx = w64 > wmx ? w64 : wmx;
+            const int k = ns ? find_bucket(static_cast<uint32_t>(w64 >> 32), S, T) : 0;
+            bid[i] = static_cast<uint16_t>(k);
+            atomicAdd(&sc[k], 1u);
+            smem_add64(&swl[k], &swh[k], static_cast<uint64_t>(r[u].size));
+        }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -683,33 +760,62 @@ __global__ void __launch_bounds__(1024) sel_bucket_kernel(SelCtl* ctl, const Sel
 
 __global__ void __launch_bounds__(1024) sel_scatter_kernel(const SelCtl* ctl, const SelRec* rec, const uint16_t* bid,
                                                           const int64_t* boff, uint32_t* bcur, SelRec* rec2) {
-    __shared__ uint32_t lc[kSelMaxBuckets], lb[kSelMaxBuckets];
+    pdl_wait();
+    pdl_trigger();
+    __shared__ uint32_t lc[kSelMaxBuckets];
+    __shared__ int64_t lb[kSelMaxBuckets];  // this CTA's first position in bucket k (boff folded in)
     if (ctl->retry) return;
     const int nb = ctl->nb, cutb = ctl->cutb;
     for (int j = threadIdx.x; j < nb; j += blockDim.x) lc[j] = 0;
     __syncthreads();
     int64_t b, e;
     cta_range(static_cast<int64_t>(ctl->count), b, e);
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-        const int k = bid[i];
-        if (k <= cutb) atomicAdd(&lc[k], 1u);
+    // four records per thread per round, loads first: the rounds are
+    // latency-bound, not bandwidth-bound
+    constexpr int U = 4;
+    for (int64_t i0 = b + threadIdx.x; i0 < e; i0 += U * blockDim.x) {
+        int k[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+            k[u] = i < e ? bid[i] : kSelMaxBuckets;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k[u] <= cutb) atomicAdd(&lc[k[u]], 1u);
     }
     __syncthreads();
     for (int j = threadIdx.x; j <= cutb; j += blockDim.x) {
-        lb[j] = lc[j] ? atomicAdd(bcur + j, lc[j]) : 0u;
+        lb[j] = boff[j] + (lc[j] ? atomicAdd(bcur + j, lc[j]) : 0u);
         lc[j] = 0;
     }
     __syncthreads();
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-        const int k = bid[i];
-        if (k > cutb) continue;
-        rec2[boff[k] + lb[k] + atomicAdd(&lc[k], 1u)] = rec[i];
+    const uint4* src = reinterpret_cast<const uint4*>(rec);
+    uint4* dst = reinterpret_cast<uint4*>(rec2);
+    for (int64_t i0 = b + threadIdx.x; i0 < e; i0 += U * blockDim.x) {
+        int k[U];
+        uint4 r0[U], r1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+            k[u] = i < e ? bid[i] : kSelMaxBuckets;
+            if (k[u] <= cutb) r0[u] = src[2 * i], r1[u] = src[2 * i + 1];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k[u] <= cutb) {
+                const int64_t at = lb[k[u]] + atomicAdd(&lc[k[u]], 1u);
+                dst[2 * at] = r0[u];
+                dst[2 * at + 1] = r1[u];
+            }
     }
 }
 
 // ------------------------------------------------------------------ 5 scan
 __global__ void __launch_bounds__(1024) sel_scan_kernel(SelCtl* ctl, int64_t excess, const unsigned long long* bcnt,
                                                        const unsigned long long* bw, int64_t* boff, uint32_t* bcur) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int64_t wtot[32];
     __shared__ int64_t total;
     __shared__ int cut;
@@ -889,15 +995,44 @@ __device__ __forceinline__ bool bucket_emit(GetRec get, const uint16_t (&idx)[IP
                                             int64_t* out, SelCtl* ctl, Sh& sh, int64_t* oslot = nullptr) {
     int64_t sz[IPT];
     int64_t loc = 0;
+    // groups of four: record loads, then the id loads, then the stores (the
+    // stores may alias the loads as far as the compiler knows, so without
+    // the grouping every record is a serial load -> load -> store chain)
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const int rk = threadIdx.x * IPT + j;
-        sz[j] = 0;
-        if (rk < n) {
-            const SelRec r = get(idx[j]);
-            out[base + rk] = rec_id(r, slot_tie, ids);
-            if (oslot) oslot[base + rk] = static_cast<int64_t>(r.k2);  // slot-ordered stores only
-            loc += (sz[j] = r.size);
+    for (int j0 = 0; j0 < IPT; j0 += 4) {
+        constexpr int G = 4;
+        uint64_t k2[G];
+        int64_t idv[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int j = j0 + g;
+            if (j >= IPT) break;
+            const int rk = threadIdx.x * IPT + j;
+            sz[j] = 0;
+            k2[g] = 0;
+            if (rk < n) {
+                const SelRec r = get(idx[j]);
+                k2[g] = r.k2;
+                sz[j] = r.size;
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int j = j0 + g;
+            if (j >= IPT) break;
+            const int rk = threadIdx.x * IPT + j;
+            if (rk < n) idv[g] = slot_tie ? ids[k2[g]] : static_cast<int64_t>(k2[g] ^ 0x8000000000000000ull);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int j = j0 + g;
+            if (j >= IPT) break;
+            const int rk = threadIdx.x * IPT + j;
+            if (rk < n) {
+                out[base + rk] = idv[g];
+                if (oslot) oslot[base + rk] = static_cast<int64_t>(k2[g]);  // slot-ordered stores only
+                loc += sz[j];
+            }
         }
     }
     if (!cut) return false;
@@ -959,8 +1094,18 @@ __device__ __forceinline__ bool count_sort_emit(const SelRec* src, int n, int pg
     for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) sh.hist[i] = 0;
     if (threadIdx.x == 0) sh.tie = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-        atomicAdd(&sh.hist[bucket_offset(src[i], pg, lo64, shift) >> 32], 1u);
+    constexpr int U = 4;  // records per thread per round, loads first
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
+        uint32_t bin[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x;
+            bin[u] = i < n ? static_cast<uint32_t>(bucket_offset(src[i], pg, lo64, shift) >> 32) : kSelBins;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (bin[u] < kSelBins) atomicAdd(&sh.hist[bin[u]], 1u);
+    }
     __syncthreads();
     {  // exclusive scan of the bins
         constexpr int per = kSelBins / kSelSortThreads;
@@ -975,13 +1120,23 @@ __device__ __forceinline__ bool count_sort_emit(const SelRec* src, int n, int pg
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint64_t o = bucket_offset(src[i], pg, lo64, shift);  // second read: L1
-        const uint32_t k = static_cast<uint32_t>(o >> 32);
-        const uint32_t at = atomicAdd(&sh.hist[k], 1u);
-        sh.sidx[at] = static_cast<uint16_t>(i);
-        sh.sbin[at] = static_cast<uint16_t>(k);
-        sh.ssub[at] = static_cast<uint32_t>(o);
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
+        uint64_t o[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x;
+            o[u] = i < n ? bucket_offset(src[i], pg, lo64, shift) : 0ull;  // second read: L1 / L2
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i >= n) continue;
+            const uint32_t k = static_cast<uint32_t>(o[u] >> 32);
+            const uint32_t at = atomicAdd(&sh.hist[k], 1u);
+            sh.sidx[at] = static_cast<uint16_t>(i);
+            sh.sbin[at] = static_cast<uint16_t>(k);
+            sh.ssub[at] = static_cast<uint32_t>(o[u]);
+        }
     }
     __syncthreads();
     for (int r = threadIdx.x; r + 1 < n; r += blockDim.x) {
@@ -1024,6 +1179,8 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_sort_kernel(SelCtl* ctl, 
                                                                   const SelRec* rec2, const int64_t* boff,
                                                                   const unsigned long long* bcnt, int32_t* big,
                                                                   int64_t* out, int cap, int64_t* oslot) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint64_t sel_smem[];
     CountShared& sh = *reinterpret_cast<CountShared*>(sel_smem);
     if (ctl->retry) return;
@@ -1085,6 +1242,8 @@ __global__ void __launch_bounds__(kSelSortThreads) sel_big_kernel(SelCtl* ctl, i
                                                                  const unsigned long long* bcnt,
                                                                  const int32_t* big, int64_t* out, int cap,
                                                                  int64_t* oslot) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint64_t sel_smem[];
     BucketShared& sh = *reinterpret_cast<BucketShared*>(sel_smem);
     if (ctl->retry) return;
