@@ -809,16 +809,24 @@ bool umma_eligible(const sine_index* h, int64_t B, bool bf16, uint32_t mode, int
 void merge_launch(sine_index* h, int ncta, int nq, int kp, const double* q64, int k, double min_sim, bool rerank,
                   int64_t* ids_dev, double* sims_dev, int32_t* counts_dev, cudaStream_t st, int64_t cert_off);
 
+// widest query group of the FFMA helper mode (queries <= this take the CUDA
+// cores instead of N = 16 MMAs).  Same box, config B, tau 0.9, ms per batch
+// helper mode vs MMAs: fp32 B = 2 0.446 vs 0.514, B = 4 0.524 vs 0.514,
+// B = 8 0.806 vs 0.515; bf16 B = 2 0.302 vs 0.267, B = 4 0.438 vs 0.268
+// (the widened-query smem reads and FMAs outgrow the halved bf16 tile time).
+constexpr int kFfmaMaxQF32 = 2;
+constexpr int kFfmaMaxQBF16 = 1;
+
 // widest resident query group (Q <= 96 KB of shared memory), 0 if < 16
 int res_nq_max(int64_t row_bytes) {
     const int64_t n = (96 * 1024) / row_bytes;
     return n >= 64 ? 64 : n >= 32 ? 32 : n >= 16 ? 16 : 0;
 }
 
-template <int NQ, int CS, bool kHelp = false>
+template <int NQ, int CS, int HQ = 0>
 int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters, size_t smem,
                cudaStream_t st) {
-    auto kern = umma_res_kernel<NQ, CS, kHelp>;
+    auto kern = umma_res_kernel<NQ, CS, HQ>;
     smem_optin(reinterpret_cast<const void*>(kern), 227 * 1024);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -826,7 +834,7 @@ int launch_res(const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams
     at[0].val.clusterDim.x = CS;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(kUmmaThreads + (kHelp ? kUmmaHelperThreads : 0));
+    cfg.blockDim = dim3(kUmmaThreads + (HQ > 0 ? kUmmaHelperThreads : 0));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = at;
@@ -863,7 +871,11 @@ template <int NQ>
 int launch_res_cs(int CS, const CUtensorMap& qmap, const CUtensorMap& rmap, const ResParams& p, int max_clusters,
                   size_t smem, cudaStream_t st) {
     if constexpr (NQ == 16)
-        if (p.ffma == 3) return launch_res<16, 1, true>(qmap, rmap, p, max_clusters, smem, st);
+        if (p.ffma == 3) switch (p.hq) {
+                case 1: return launch_res<16, 1, 1>(qmap, rmap, p, max_clusters, smem, st);
+                case 2: return launch_res<16, 1, 2>(qmap, rmap, p, max_clusters, smem, st);
+                default: return launch_res<16, 1, 4>(qmap, rmap, p, max_clusters, smem, st);
+            }
     switch (CS) {
         case 1: return launch_res<NQ, 1>(qmap, rmap, p, max_clusters, smem, st);
         case 2: return launch_res<NQ, 2>(qmap, rmap, p, max_clusters, smem, st);
@@ -907,20 +919,31 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         // SINE_NO_FFMA=1 keeps the MMAs; SINE_FFMA_LIST=1 computes in the four
         // list warps (scalar FFMA for fp32 rows, FFMA2 with SINE_FFMA2=1 or
         // for bf16 rows), the round-2 single-group path.
+        // Small groups (up to ffma_maxq queries) take the helper mode too: each
+        // staged row chunk is loaded once and serves every query of the group.
         static const bool ffma_on = getenv("SINE_NO_FFMA") == nullptr;
         static const bool ffma_list = getenv("SINE_FFMA_LIST") != nullptr;
         static const bool ffma2 = getenv("SINE_FFMA2") != nullptr;
-        const int ffma = ffma_on && CS == 1 && nq == 1 && NQ == 16 ? (!ffma_list ? 3 : tf32 && !ffma2 ? 1 : 2) : 0;
-        const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp, -1, ffma == 3);
+        static const int maxq_env = getenv("SINE_FFMA_MAXQ") ? atoi(getenv("SINE_FFMA_MAXQ")) : -1;
+        const int ffma_maxq = maxq_env >= 0 ? std::min(maxq_env, 4) : (tf32 ? kFfmaMaxQF32 : kFfmaMaxQBF16);
+        int ffma = 0, hq = 0;
+        if (ffma_on && CS == 1 && NQ == 16) {
+            if (nq == 1) ffma = !ffma_list ? 3 : tf32 && !ffma2 ? 1 : 2;
+            else if (nq <= ffma_maxq) ffma = 3;
+            if (ffma == 3) hq = nq <= 1 ? 1 : nq <= 2 ? 2 : 4;
+        }
+        const int fqn = hq > 1 && !tf32 ? hq : 1;
+        const ResSmem L0 = res_smem_layout(0, NQ, kblocks, kp, -1, hq, fqn);
         if (L0.total + 2 * kUmmaN * kUmmaKB > 227 * 1024) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
-        int S = static_cast<int>(std::min<size_t>(8, (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
+        static const int s_cap = getenv("SINE_RES_STAGES") ? atoi(getenv("SINE_RES_STAGES")) : 8;
+        int S = static_cast<int>(std::min<size_t>(std::max(2, s_cap), (227 * 1024 - L0.total) / (kUmmaN * kUmmaKB)));
         // helper mode: an even ring, so every stage belongs to one dot-product
         // group (ring index parity == stage parity).  With an odd ring a group
         // could wait on a stage the other group still owns one lap behind and
         // read the wrong mbarrier phase.
         if (ffma == 3) S &= ~1;
         if (S < 2) fail(SINE_EINVAL, "tensor-core plan does not fit shared memory");
-        const ResSmem L = res_smem_layout(S, NQ, kblocks, kp, -1, ffma == 3);
+        const ResSmem L = res_smem_layout(S, NQ, kblocks, kp, -1, hq, fqn);
         h->gbound.ensure(static_cast<size_t>(kMaxCS) * NQmax);
         res_prep_queries<<<grid_for(static_cast<int64_t>(CS) * NQ * row_elems, 256, h->num_sms), 256, 0, st>>>(
             q_dev + q0 * h->dim, nq, CS * NQ, h->dim, row_elems, tf32 ? 1 : 0, h->qbf.p, h->gbound.p,
@@ -941,6 +964,7 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         p.gbound = h->gbound.p;  // zeroed by res_prep_queries
         p.tile_stride = 1;
         p.ffma = ffma;
+        p.hq = hq;
         p.valid = h->valid;
         p.ids = h->ids;
         p.out_key = h->lkey.p;

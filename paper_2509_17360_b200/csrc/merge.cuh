@@ -38,6 +38,7 @@ struct MergeParams {
 };
 
 constexpr int kMergeThreads = 256;
+constexpr int kMergeCompact = 2048;  // live candidates kept in the compact list
 
 // Block-wide exclusive scan of one value per thread (256 threads).
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot) {
@@ -105,55 +106,69 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     __shared__ uint32_t nsel;
 
     extern __shared__ uint32_t pool[];  // [ncta * kp] candidate keys, 0 = empty
+    // live entries (key >= the admission bound), compacted: the selection
+    // below touches only these when they fit (the common case: a few hundred)
+    __shared__ uint32_t ckey[kMergeCompact];
+    __shared__ int32_t cslot[kMergeCompact];
+    __shared__ uint32_t ctot;
     pdl_wait();  // launched early (PDL): the scan's lists are complete past this point
     const int qi = blockIdx.x;
     const int kp = p.kp, nq = p.nq;
     const int nflat = p.ncta * kp;
     for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) ns[c] = p.in_n[c * nq + qi];
-    if (threadIdx.x == 0) nsel = 0;
+    if (threadIdx.x == 0) {
+        nsel = 0;
+        ctot = 0;
+    }
     __syncthreads();
     // stage the pooled keys once: every radix pass below reads shared memory.
-    // Loads go out 16 per thread before any store (the staging is latency
-    // bound), and keys below the chip-wide admission bound are dropped: that
-    // bound is <= the true k'-th best key (every CTA's k'-th best is), so
-    // they cannot make the top k' -- the selection then touches only the
-    // few hundred live keys instead of every list entry.
+    // Keys and slots go out 16 per thread before any store (the staging is
+    // latency bound), and keys below the chip-wide admission bound are
+    // dropped: that bound is <= the true k'-th best key (every CTA's k'-th
+    // best is), so they cannot make the top k'.
     const uint32_t gb = p.gbound ? p.gbound[qi] : 0u;
+    const int lane = threadIdx.x & 31;
     for (int f0 = 0; f0 < nflat; f0 += 16 * kMergeThreads) {
         uint32_t v[16];
+        int32_t sl[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int f = f0 + j * kMergeThreads + threadIdx.x;
             v[j] = 0u;
+            sl[j] = 0;
             if (f < nflat) {
                 const int c = f / kp, e = f - c * kp;
-                if (e < ns[c]) v[j] = __ldg(p.in_key + (static_cast<size_t>(c) * nq + qi) * kp + e);
+                if (e < ns[c]) {
+                    const size_t o = (static_cast<size_t>(c) * nq + qi) * kp + e;
+                    v[j] = __ldg(p.in_key + o);
+                    sl[j] = __ldg(p.in_slot + o);
+                }
             }
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int f = f0 + j * kMergeThreads + threadIdx.x;
-            if (f < nflat) pool[f] = v[j] >= gb ? v[j] : 0u;
+            const bool live = f < nflat && v[j] != 0u && v[j] >= gb;
+            if (f < nflat) pool[f] = live ? v[j] : 0u;
+            // warp-aggregated append to the compact list
+            const uint32_t b = __ballot_sync(0xffffffffu, live);
+            if (b) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&ctot, static_cast<uint32_t>(__popc(b)));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const uint32_t at = base + __popc(b & ((1u << lane) - 1u));
+                if (live && at < kMergeCompact) {
+                    ckey[at] = v[j];
+                    cslot[at] = sl[j];
+                }
+            }
         }
     }
     __syncthreads();
+    const uint32_t total = ctot;  // live candidates (after the admission-bound prefilter)
+    const bool compact = total <= static_cast<uint32_t>(kMergeCompact);
 
-    auto flat_ok = [&](int f, int& c, int& e) {
-        c = f / kp;
-        e = f - c * kp;
-        return pool[f] != 0u;
-    };
-    auto key_at = [&](int c, int e) { return pool[c * kp + e]; };
     auto slot_at = [&](int c, int e) { return p.in_slot[(static_cast<size_t>(c) * nq + qi) * kp + e]; };
-
-    // total live candidates (after the admission-bound prefilter)
-    uint32_t local = 0;
-    for (int f = threadIdx.x; f < nflat; f += kMergeThreads) local += pool[f] != 0u ? 1u : 0u;
-    const uint32_t before_me = block_excl_scan(local, scratch);
-    if (threadIdx.x == kMergeThreads - 1) scratch[12] = before_me + local;
-    __syncthreads();
-    const uint32_t total = scratch[12];
-    __syncthreads();
 
     // every row that is not a candidate has a filter score <= bound_key
     // (the selection cut, or the worst entry of a CTA's full list), or was
@@ -165,24 +180,31 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
         for (int c = threadIdx.x; c < p.ncta; c += kMergeThreads) {
             if (ns[c] != kp) continue;
             uint32_t mk = 0xffffffffu;
-            for (int e = 0; e < kp; ++e) mk = min(mk, key_at(c, e));
+            for (int e = 0; e < kp; ++e) mk = min(mk, pool[c * kp + e]);
             atomicMax(&bound_key, mk);
         }
-        for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
-            int c, e;
-            if (!flat_ok(f, c, e)) continue;
-            const uint32_t at = atomicAdd(&nsel, 1u);
-            sel_key[at] = key_at(c, e);
-            sel_slot[at] = slot_at(c, e);
+        for (int i = threadIdx.x; i < static_cast<int>(total); i += kMergeThreads) {
+            sel_key[i] = ckey[i];
+            sel_slot[i] = cslot[i];
         }
+        if (threadIdx.x == 0) nsel = total;
     } else {
+        // the selection runs over the compact list (n = total) when it fits,
+        // else over the whole pool (n = nflat, empty entries skipped)
+        const int n = compact ? static_cast<int>(total) : nflat;
+        auto key_of = [&](int f) { return compact ? ckey[f] : pool[f]; };
+        auto slot_of = [&](int f) {
+            if (compact) return cslot[f];
+            const int c = f / kp;
+            return slot_at(c, f - c * kp);
+        };
         uint32_t nbefore, nequal;
         const uint32_t kstar = block_select<uint32_t>(
-            [&](int f, uint32_t& key) {  // pool[f] == key_at(f / kp, f % kp), no division
-                key = pool[f];
+            [&](int f, uint32_t& key) {
+                key = key_of(f);
                 return key != 0u;
             },
-            nflat, static_cast<uint32_t>(kp), true, 32, hist, scratch, &nbefore, &nequal);
+            n, static_cast<uint32_t>(kp), true, 32, hist, scratch, &nbefore, &nequal);
         if (threadIdx.x == 0) bound_key = kstar;
         const uint32_t need_eq = kp - nbefore;
         // ties at the cut: keep the need_eq smallest ids
@@ -191,23 +213,21 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             uint32_t b2, e2;
             idcut = block_select<uint64_t>(
                 [&](int f, uint64_t& key) {
-                    if (pool[f] != kstar) return false;
-                    const int c = f / kp, e = f - c * kp;
-                    key = i64_key(__ldg(p.ids + slot_at(c, e)));
+                    if (key_of(f) != kstar) return false;
+                    key = i64_key(__ldg(p.ids + slot_of(f)));
                     return true;
                 },
-                nflat, need_eq, false, 64, hist, scratch, &b2, &e2);
+                n, need_eq, false, 64, hist, scratch, &b2, &e2);
         }
-        for (int f = threadIdx.x; f < nflat; f += kMergeThreads) {
-            int c, e;
-            if (!flat_ok(f, c, e)) continue;
-            const uint32_t key = key_at(c, e);
+        for (int f = threadIdx.x; f < n; f += kMergeThreads) {
+            const uint32_t key = key_of(f);
+            if (key == 0u) continue;
             bool take = key > kstar;
-            if (key == kstar) take = (idcut == ~0ull) || i64_key(__ldg(p.ids + slot_at(c, e))) <= idcut;
+            if (key == kstar) take = (idcut == ~0ull) || i64_key(__ldg(p.ids + slot_of(f))) <= idcut;
             if (take) {
                 const uint32_t at = atomicAdd(&nsel, 1u);
                 sel_key[at] = key;
-                sel_slot[at] = slot_at(c, e);
+                sel_slot[at] = slot_of(f);
             }
         }
     }
@@ -221,39 +241,49 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     __syncthreads();
 
     if (p.rerank) {
-        // fp64 re-score: one warp per candidate, lane-strided fma chain then
-        // a fixed butterfly -> identical rows give identical similarities.
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        // fp64 re-score: lane l of a warp sums x[t] * q[t] for t = l, l + 32,
+        // ... in ascending order (one fma chain), then a fixed butterfly ->
+        // identical rows give identical similarities.  A warp scores up to
+        // four candidates at once so their row loads overlap (the chains and
+        // their order are unchanged by the interleaving).
+        const int warp = threadIdx.x >> 5;
         const double* q = p.q64 + static_cast<size_t>(qi) * p.dim;
-        for (int i = warp; i < m; i += kMergeThreads / 32) {
-            const double* x = p.rows64 + static_cast<size_t>(sel_slot[i]) * p.dim;
-            double a = 0.0;
+        constexpr int kW = kMergeThreads / 32;
+        for (int i0 = warp; i0 < m; i0 += 4 * kW) {
+            const double* x[4];
+            bool on[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int i = i0 + c * kW;
+                on[c] = i < m;
+                x[c] = p.rows64 + static_cast<size_t>(on[c] ? sel_slot[i] : sel_slot[i0]) * p.dim;
+            }
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
             int64_t t = lane;
-            // same per-lane order as a plain strided loop (bit-identical
-            // sums), with 16 independent row loads in flight per lane
-            for (; t + 32 * 15 < p.dim; t += 32 * 16) {
-                double xv[16], qv[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    xv[u] = __ldg(x + t + 32 * u);
-                    qv[u] = __ldg(q + t + 32 * u);
-                }
-#pragma unroll
-                for (int u = 0; u < 16; ++u) a = fma(xv[u], qv[u], a);
-            }
             for (; t + 32 * 7 < p.dim; t += 32 * 8) {
-                double xv[8], qv[8];
+                double qv[8], xv[4][8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    xv[u] = __ldg(x + t + 32 * u);
-                    qv[u] = __ldg(q + t + 32 * u);
-                }
+                for (int u = 0; u < 8; ++u) qv[u] = __ldg(q + t + 32 * u);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) a = fma(xv[u], qv[u], a);
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) xv[c][u] = on[c] ? __ldg(x[c] + t + 32 * u) : 0.0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[c] = fma(xv[c][u], qv[u], a[c]);
             }
-            for (; t < p.dim; t += 32) a = fma(__ldg(x + t), __ldg(q + t), a);
-            a = warp_sum64(a);
-            if (lane == 0) sel_sim[i] = a + 0.0;
+            for (; t < p.dim; t += 32) {
+                const double qv = __ldg(q + t);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (on[c]) a[c] = fma(__ldg(x[c] + t), qv, a[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double s = warp_sum64(a[c]);
+                if (lane == 0 && on[c]) sel_sim[i0 + c * kW] = s + 0.0;
+            }
         }
         __syncthreads();
     }
@@ -288,7 +318,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
             double bound = static_cast<double>(p.thr0);
             if (bound_key) bound = fmax(bound, static_cast<double>(key_f32(bound_key)));
             if (p.gbound && p.gbound[qi]) bound = fmax(bound, static_cast<double>(key_f32(p.gbound[qi])));
-            const double need = outn == p.k ? p.out_sims[static_cast<size_t>(qi) * p.k + p.k - 1] : p.min_sim;
+            const double need = outn == p.k ? sel_sim[order[p.k - 1]] : p.min_sim;
             p.cert[qi] = (!p.rerank || bound + p.err < need) ? 1 : 0;
             if (p.debug)
                 printf("cert q%d total=%u kp=%d bound_key=%08x bound=%.6f err=%g need=%.6f thr0=%f -> %d\n", qi,

@@ -411,6 +411,7 @@ struct ResParams {
                        //     cores straight from the TMA-staged tiles (no MMAs): 1 = scalar
                        //     FFMA (fp32 rows), 2 = packed FFMA2, 3 = scalar FFMA split with
                        //     four helper warps (launched with kUmmaHelperThreads more threads)
+    int hq;            // p.ffma == 3: queries of the helper mode (1, 2 or 4; >= nq)
     const uint32_t* valid;
     const int64_t* ids;
     uint32_t* out_key;
@@ -425,6 +426,8 @@ constexpr int kSparse = 128;     // (query, row) pairs per tile handed to the sp
 constexpr int kSparseRows = 32;  // tiles with more passing rows take the dense (bitonic) rounds
 
 constexpr int kScoreRing = 16;  // FFMA helper mode: tiles of partial scores in flight to the list warps
+// ring depth for HQ helper queries (the ring holds [depth][2][HQ][128] fp32)
+__host__ __device__ constexpr int score_ring_depth(int hq) { return hq <= 1 ? kScoreRing : hq == 2 ? 8 : 4; }
 
 struct ResSmem {
     size_t q_off, a_off, bar_off, list_key_off, list_slot_off, qstate_off, pend_off, sparse_off, fq_off, pb_off, total;
@@ -432,9 +435,10 @@ struct ResSmem {
 
 // Nq_res: queries resident in this CTA's shared memory (== Nq except for the
 // CTA pair, where each CTA holds half of the Nq queries it scores).
-// helpers: room for the FFMA helper mode's score ring (p.ffma == 3 only).
+// hq: queries of the FFMA helper mode (p.ffma == 3; 0 = no helpers) -- room
+// for its score ring; fqn: queries widened to fp32 in smem (bf16 rows).
 __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, int kp, int Nq_res = -1,
-                                                   bool helpers = false) {
+                                                   int hq = 0, int fqn = 1) {
     ResSmem L;
     size_t off = 0;
     L.q_off = off;
@@ -462,9 +466,12 @@ __host__ __device__ inline ResSmem res_smem_layout(int S, int Nq, int kblocks, i
     off += 16 + static_cast<size_t>(kSparse) * 16;
     off = (off + 15) / 16 * 16;
     L.fq_off = off;  // FFMA mode: the single query in fp32, one 128-B K block -> kUmmaKB / 2 floats (bf16 rows)
-    off += static_cast<size_t>(kblocks) * (kUmmaKB / 2) * 4;
-    L.pb_off = off;  // FFMA helper mode: score ring, kScoreRing x {full, empty} mbarriers + [ring][2][128] fp32
-    if (helpers) off += 2 * kScoreRing * 8 + static_cast<size_t>(kScoreRing) * 2 * 128 * 4;
+    off += static_cast<size_t>(fqn) * kblocks * (kUmmaKB / 2) * 4;
+    L.pb_off = off;  // FFMA helper mode: score ring, depth x {full, empty} mbarriers + [depth][2][hq][128] fp32
+    if (hq > 0) {
+        const int rd = score_ring_depth(hq);
+        off += 2 * rd * 8 + static_cast<size_t>(rd) * 2 * hq * 128 * 4;
+    }
     L.total = off + 1024;
     return L;
 }
@@ -649,17 +656,24 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
 
 constexpr int kUmmaHelperThreads = 256;  // FFMA helper mode: eight dot-product warps
 
-// Single-query FFMA (helper mode, p.ffma == 3) over the K blocks of local
+// FFMA (helper mode, p.ffma == 3) of HQ queries over the K blocks of local
 // tile i whose ring index g = i * nkb + kb (the producer's issue order) has
 // parity `par`: dot-product warps 6-9 take the even stages and warps 10-13
 // the odd ones, so both groups read adjacent stages at once.  Stage g sits
 // at g % S with phase (g / S) & 1; S is even, so each stage has one owning
 // group and a group never waits on a stage the other may be a lap behind
 // on.  Each warp releases the stages it read (four arrivals per stage).
-__device__ __forceinline__ float ffma_kpar(int i, int par, int nkb, int S, int row, bool tf32, const uint8_t* sa,
-                                           const uint8_t* sq, int NQ, const float* fq, uint64_t* full,
-                                           uint64_t* empty, int lane) {
-    float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
+// Each row chunk is loaded once and serves all HQ queries: fp32 queries are
+// read from the 128B-swizzled query tile (query j, 16-B chunk c at
+// c ^ (j & 7) -- compile-time offsets), bf16 rows against the queries
+// widened to fp32 in `fq` ([HQ][nkb][64]).  Four fma chains per query.
+template <int HQ>
+__device__ __forceinline__ void ffma_kpar(float (&out)[HQ], int i, int par, int nkb, int S, int row, bool tf32,
+                                          const uint8_t* sa, const uint8_t* sq, int NQ, const float* fq,
+                                          uint64_t* full, uint64_t* empty, int lane) {
+    float f[HQ][4];
+#pragma unroll
+    for (int j = 0; j < HQ; ++j) f[j][0] = f[j][1] = f[j][2] = f[j][3] = 0.0f;
     const int sw = row & 7;
     const int g0 = i * nkb;
     for (int kb = ((g0 & 1) == par) ? 0 : 1; kb < nkb; kb += 2) {
@@ -672,46 +686,60 @@ __device__ __forceinline__ float ffma_kpar(int i, int par, int nkb, int S, int r
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
-                const uint4 qv = *reinterpret_cast<const uint4*>(qp + (c << 4));
-                f0 = fmaf(__uint_as_float(xv.x), __uint_as_float(qv.x), f0);
-                f1 = fmaf(__uint_as_float(xv.y), __uint_as_float(qv.y), f1);
-                f2 = fmaf(__uint_as_float(xv.z), __uint_as_float(qv.z), f2);
-                f3 = fmaf(__uint_as_float(xv.w), __uint_as_float(qv.w), f3);
+#pragma unroll
+                for (int j = 0; j < HQ; ++j) {
+                    const uint4 qv = *reinterpret_cast<const uint4*>(qp + j * kUmmaKB + ((c ^ (j & 7)) << 4));
+                    f[j][0] = fmaf(__uint_as_float(xv.x), __uint_as_float(qv.x), f[j][0]);
+                    f[j][1] = fmaf(__uint_as_float(xv.y), __uint_as_float(qv.y), f[j][1]);
+                    f[j][2] = fmaf(__uint_as_float(xv.z), __uint_as_float(qv.z), f[j][2]);
+                    f[j][3] = fmaf(__uint_as_float(xv.w), __uint_as_float(qv.w), f[j][3]);
+                }
             }
         } else {
-            const float4* qf = reinterpret_cast<const float4*>(fq + kb * (kUmmaKB / 2));
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const uint4 xv = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
-                const float4 q0 = qf[2 * c], q1 = qf[2 * c + 1];
-                f0 = fmaf(__uint_as_float(xv.x << 16), q0.x, f0);
-                f1 = fmaf(__uint_as_float(xv.x & 0xffff0000u), q0.y, f1);
-                f2 = fmaf(__uint_as_float(xv.y << 16), q0.z, f2);
-                f3 = fmaf(__uint_as_float(xv.y & 0xffff0000u), q0.w, f3);
-                f0 = fmaf(__uint_as_float(xv.z << 16), q1.x, f0);
-                f1 = fmaf(__uint_as_float(xv.z & 0xffff0000u), q1.y, f1);
-                f2 = fmaf(__uint_as_float(xv.w << 16), q1.z, f2);
-                f3 = fmaf(__uint_as_float(xv.w & 0xffff0000u), q1.w, f3);
+                const float x0 = __uint_as_float(xv.x << 16), x1 = __uint_as_float(xv.x & 0xffff0000u);
+                const float x2 = __uint_as_float(xv.y << 16), x3 = __uint_as_float(xv.y & 0xffff0000u);
+                const float x4 = __uint_as_float(xv.z << 16), x5 = __uint_as_float(xv.z & 0xffff0000u);
+                const float x6 = __uint_as_float(xv.w << 16), x7 = __uint_as_float(xv.w & 0xffff0000u);
+#pragma unroll
+                for (int j = 0; j < HQ; ++j) {
+                    const float4* qf = reinterpret_cast<const float4*>(fq + (static_cast<size_t>(j) * nkb + kb) * (kUmmaKB / 2));
+                    const float4 q0 = qf[2 * c], q1 = qf[2 * c + 1];
+                    f[j][0] = fmaf(x0, q0.x, f[j][0]);
+                    f[j][1] = fmaf(x1, q0.y, f[j][1]);
+                    f[j][2] = fmaf(x2, q0.z, f[j][2]);
+                    f[j][3] = fmaf(x3, q0.w, f[j][3]);
+                    f[j][0] = fmaf(x4, q1.x, f[j][0]);
+                    f[j][1] = fmaf(x5, q1.y, f[j][1]);
+                    f[j][2] = fmaf(x6, q1.z, f[j][2]);
+                    f[j][3] = fmaf(x7, q1.w, f[j][3]);
+                }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);
     }
-    return (f0 + f2) + (f1 + f3);
+#pragma unroll
+    for (int j = 0; j < HQ; ++j) out[j] = (f[j][0] + f[j][2]) + (f[j][1] + f[j][3]);
 }
 
 // CS = thread-block cluster size.  The CS CTAs of a cluster hold CS
 // different query groups (NQ each) and share every 128-row tile: each CTA
 // TMA-loads 128/CS rows of it and multicasts them to the whole cluster, so
 // one HBM pass over the index serves CS * NQ queries.
-template <int NQ, int CS, bool kHelp>
-__global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kUmmaThreads, 1)
+// HQ > 0: the FFMA helper mode over HQ queries (p.ffma == 3, NQ == 16, CS == 1).
+template <int NQ, int CS, int HQ>
+__global__ void __launch_bounds__(HQ > 0 ? kUmmaThreads + kUmmaHelperThreads : kUmmaThreads, 1)
     umma_res_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap rmap,
                     const ResParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages, nkb = p.kblocks, kp = p.kp;
-    const ResSmem L = res_smem_layout(S, NQ, nkb, kp, -1, kHelp);
+    constexpr bool kHelp = HQ > 0;
+    constexpr int kRing = score_ring_depth(HQ);
+    const ResSmem L = res_smem_layout(S, NQ, nkb, kp, -1, HQ, HQ > 1 && !p.tf32 ? HQ : 1);
     uint8_t* sq = smem + L.q_off;
     uint8_t* sa = smem + L.a_off;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -748,9 +776,9 @@ __global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kU
         mbar_init(qfull, 1);
         if constexpr (kHelp) {
             uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + L.pb_off);
-            for (int r = 0; r < kScoreRing; ++r) {
-                mbar_init(sfull + r, 8);               // both dot-product groups wrote their partials
-                mbar_init(sfull + kScoreRing + r, 4);  // the list warps read them
+            for (int r = 0; r < kRing; ++r) {
+                mbar_init(sfull + r, 8);          // both dot-product groups wrote their partials
+                mbar_init(sfull + kRing + r, 4);  // the list warps read them
             }
         }
         fence_mbar_init();
@@ -869,21 +897,24 @@ __global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kU
         // ---------------- FFMA dot-product warps (p.ffma == 3) ----------------
         // two groups of four split each tile's K blocks by ring parity and
         // hand the partial scores to the list warps through a ring of
-        // kScoreRing tiles, so list upkeep never stalls the HBM stream
+        // kRing tiles, so list upkeep never stalls the HBM stream
         const int grp = (warp - 6) >> 2;
         const int row = threadIdx.x - kUmmaThreads - grp * 128;
         const float* fq = reinterpret_cast<const float*>(smem + L.fq_off);
         uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + L.pb_off);
-        uint64_t* sempty = sfull + kScoreRing;
-        float* sring = reinterpret_cast<float*>(sempty + kScoreRing);
+        uint64_t* sempty = sfull + kRing;
+        float* sring = reinterpret_cast<float*>(sempty + kRing);
         mbar_wait(qfull, 0);
         named_bar_sync(3, 128 + kUmmaHelperThreads);  // the list warps widened the bf16 query into fq
         int i = 0;
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
-            const float part = ffma_kpar(i, grp, nkb, S, row, p.tf32 != 0, sa, sq, NQ, fq, full, empty, lane);
-            const int r = i % kScoreRing;
-            mbar_wait(sempty + r, static_cast<uint32_t>(((i / kScoreRing) & 1) ^ 1));
-            sring[(r * 2 + grp) * 128 + row] = part;
+            constexpr int kQ = HQ > 0 ? HQ : 1;
+            float part[kQ];
+            ffma_kpar<kQ>(part, i, grp, nkb, S, row, p.tf32 != 0, sa, sq, NQ, fq, full, empty, lane);
+            const int r = i % kRing;
+            mbar_wait(sempty + r, static_cast<uint32_t>(((i / kRing) & 1) ^ 1));
+#pragma unroll
+            for (int j = 0; j < kQ; ++j) sring[((r * 2 + grp) * HQ + j) * 128 + row] = part[j];
             __syncwarp();
             if (lane == 0) mbar_arrive(sfull + r);
         }
@@ -898,10 +929,14 @@ __global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kU
         float* fq = reinterpret_cast<float*>(smem + L.fq_off);
         if (p.ffma) {
             mbar_wait(qfull, 0);
-            if (!p.tf32) {  // query row 0 of each bf16 K block is unswizzled: widen it once
-                for (int e = tid; e < nkb * (kUmmaKB / 2); e += 128) {
-                    const int kb = e / (kUmmaKB / 2), c = e % (kUmmaKB / 2);
-                    const uint16_t v = reinterpret_cast<const uint16_t*>(sq + static_cast<size_t>(kb) * NQ * kUmmaKB)[c];
+            if (!p.tf32) {  // widen the bf16 queries once (query j's 16-B chunk c sits at c ^ (j & 7))
+                constexpr int kWide = HQ > 1 ? HQ : 1;
+                for (int e = tid; e < kWide * nkb * (kUmmaKB / 2); e += 128) {
+                    const int j = e / (nkb * (kUmmaKB / 2));
+                    const int r = e - j * nkb * (kUmmaKB / 2);
+                    const int kb = r / (kUmmaKB / 2), c = r % (kUmmaKB / 2);
+                    const uint16_t v = *reinterpret_cast<const uint16_t*>(
+                        sq + static_cast<size_t>(kb) * NQ * kUmmaKB + j * kUmmaKB + ((((c >> 3) ^ (j & 7)) << 4) | ((c & 7) << 1)));
                     fq[e] = __uint_as_float(static_cast<uint32_t>(v) << 16);
                 }
                 named_bar_sync(2, 128);
@@ -909,7 +944,7 @@ __global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kU
             if constexpr (kHelp) named_bar_sync(3, 128 + kUmmaHelperThreads);
         }
         uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + L.pb_off);
-        const float* sring = reinterpret_cast<const float*>(sfull + 2 * kScoreRing);
+        const float* sring = reinterpret_cast<const float*>(sfull + 2 * kRing);
         for (int t = cid; t < p.ntiles; t += ncl, ++i) {
             const int acc = i & 1;
             const int64_t slot = static_cast<int64_t>(t) * p.tile_stride * kUmmaN + tid;
@@ -924,13 +959,14 @@ __global__ void __launch_bounds__(kHelp ? kUmmaThreads + kUmmaHelperThreads : kU
             named_bar_sync(2, 128);
             float sc[NQ];
             if constexpr (kHelp) {
-                const int r = i % kScoreRing;
-                mbar_wait(sfull + r, static_cast<uint32_t>((i / kScoreRing) & 1));
-                sc[0] = (sring[(r * 2) * 128 + tid] + sring[(r * 2 + 1) * 128 + tid]) + 0.0f;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(sfull + kScoreRing + r);
+                const int r = i % kRing;
+                mbar_wait(sfull + r, static_cast<uint32_t>((i / kRing) & 1));
 #pragma unroll
-                for (int j = 1; j < NQ; ++j) sc[j] = 0.0f;
+                for (int j = 0; j < NQ; ++j)
+                    sc[j] = j < HQ ? (sring[((r * 2) * HQ + j) * 128 + tid] + sring[((r * 2 + 1) * HQ + j) * 128 + tid]) + 0.0f
+                                   : 0.0f;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sfull + kRing + r);
             } else if (p.ffma) {
                 // one query: the dot products on the CUDA cores with packed
                 // FFMA2 (two fp32 lanes per instruction), read from the

@@ -95,6 +95,41 @@ def test_config_b_batch_4096(config_b, scan, tau):
 
 
 @pytest.mark.parametrize("scan", ["fp32", "bf16"])
+@pytest.mark.parametrize("tau", TAUS)
+@pytest.mark.parametrize("b", [2, 3, 4, 5, 8, 16])
+def test_config_b_small_batches(config_b, torch, scan, tau, b):
+    """Small groups: fp32 B = 2 runs the multi-query FFMA helper mode (each
+    staged row chunk serves both queries), the rest the N = 16 MMAs.
+    Answers exact against the float64 truth; the filter alone certifies
+    most queries (so a wrong filter cannot hide behind the re-runs)."""
+    idx, q, truth, _, _ = config_b
+    certs = []
+    for start in (0, 23, q.shape[0] - b):
+        rows = range(start, start + b)
+        ids, sims, counts = idx.query_batch(q[start:start + b], K_B, tau, scan=scan)
+        for r, j in enumerate(rows):
+            tid, tsim = truth.answer(j, tau)
+            check_query(ids[r], sims[r], counts[r], tid, tsim, K_B, tau, f"B={b} {scan} tau={tau} q{j}")
+        qd = torch.from_numpy(np.ascontiguousarray(q[start:start + b])).cuda()
+        di = torch.empty((b, K_B), dtype=torch.int64, device="cuda")
+        ds = torch.empty((b, K_B), dtype=torch.float64, device="cuda")
+        dc = torch.empty((b,), dtype=torch.int32, device="cuda")
+        ce = torch.zeros((b,), dtype=torch.uint8, device="cuda")
+        st = torch.cuda.current_stream()
+        idx.query_device_cert(b, qd.data_ptr(), K_B, tau, di.data_ptr(), ds.data_ptr(), dc.data_ptr(), ce.data_ptr(),
+                              st.cuda_stream, scan=scan)
+        st.synchronize()
+        ce = ce.cpu().numpy()
+        certs.extend(ce.tolist())
+        for r, j in enumerate(rows):
+            if ce[r]:  # a certified filter answer is the exact answer as is
+                tid, tsim = truth.answer(j, tau)
+                check_query(di[r].cpu().numpy(), ds[r].cpu().numpy(), int(dc[r]), tid, tsim, K_B, tau,
+                            f"B={b} {scan} tau={tau} certified q{j}")
+    assert np.mean(certs) >= 0.8, certs
+
+
+@pytest.mark.parametrize("scan", ["fp32", "bf16"])
 def test_config_b_async_submit_wait(config_b, scan):
     """The e2e API the bench times: sine_query_submit / sine_query_wait,
     4 batches in flight, B=1 each."""
