@@ -12,6 +12,10 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_17360_b200 import GpuCosineIndex  # noqa: E402
+from paper_2509_17360_b200 import _native  # noqa: E402
+
+if os.environ.get("PROBE_LIB"):  # A/B against another build of the library (same process layout)
+    _native.load_library(os.environ["PROBE_LIB"])
 
 N, D, K = 1_000_000, 768, 10
 PEAK = 6550.0e9
@@ -55,4 +59,4 @@ for B in bs:
             same = bool(np.array_equal(ids.cpu().numpy(), ref))
             out.append({"B": B, "scan": scan, "tau": tau, "ms": round(ms, 4), "hbm_frac": round(byts / (ms * 1e-3) / PEAK, 3),
                         "ids_equal_certified_path": same})
-            print(json.dumps(out[-1]), flush=True)
+            print(json.dumps(out[-1]), os.environ.get("PROBE_LIB", "head"), flush=True)
