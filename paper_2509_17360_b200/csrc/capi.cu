@@ -984,7 +984,8 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         // writes the max score; the kp-th largest tile maximum is a valid
         // lower bound on the kp-th best score (kp distinct rows reach it).
         const int sample_tiles = std::min(2 * max_clusters, ntiles / 8);
-        if (thr0 < 0.5f && sample_tiles >= 2 * kp && nq >= 8) {
+        static const int sample_minq = getenv("SINE_SAMPLE_MINQ") ? atoi(getenv("SINE_SAMPLE_MINQ")) : 8;
+        if (thr0 < 0.5f && sample_tiles >= 2 * kp && nq >= sample_minq) {
             h->tmax.ensure(static_cast<size_t>(sample_tiles) * CS * NQ);
             ResParams sp = p;
             sp.ntiles = sample_tiles;
