@@ -984,7 +984,12 @@ void umma_res_query(sine_index* h, int64_t B, const double* q_dev, int k, int kp
         // writes the max score; the kp-th largest tile maximum is a valid
         // lower bound on the kp-th best score (kp distinct rows reach it).
         const int sample_tiles = std::min(2 * max_clusters, ntiles / 8);
-        static const int sample_minq = getenv("SINE_SAMPLE_MINQ") ? atoi(getenv("SINE_SAMPLE_MINQ")) : 8;
+        // Below sample_minq queries the pass costs more than the warm-up it
+        // saves.  Same box, config B, tau -1, ms with / without the sample
+        // pass: fp32 B = 8 0.564 / 0.543, B = 16 0.565 / 0.564; bf16 B = 8
+        // 0.306 / 0.320, B = 16 0.308 / 0.375, B = 64 0.359 / 1.00.
+        static const int sample_minq_env = getenv("SINE_SAMPLE_MINQ") ? atoi(getenv("SINE_SAMPLE_MINQ")) : -1;
+        const int sample_minq = sample_minq_env >= 0 ? sample_minq_env : (tf32 ? 16 : 8);
         if (thr0 < 0.5f && sample_tiles >= 2 * kp && nq >= sample_minq) {
             h->tmax.ensure(static_cast<size_t>(sample_tiles) * CS * NQ);
             ResParams sp = p;
