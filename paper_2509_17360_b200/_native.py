@@ -15,7 +15,9 @@ import numpy as np
 
 from .errors import ValidationError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsine_b200.so")
+# SINE_LIB_PATH: another build of the library (same-box A/B timing runs)
+LIB_PATH = os.environ.get("SINE_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                           "libsine_b200.so")
 
 SINE_OK, SINE_EINVAL, SINE_ECUDA, SINE_ENCCL, SINE_ENOMEM, SINE_ENOTFOUND, SINE_EDUP, SINE_ENORM = range(8)
 
