@@ -250,6 +250,35 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
         const double* q = p.q64 + static_cast<size_t>(qi) * p.dim;
         constexpr int kW = kMergeThreads / 32;
         for (int i0 = warp; i0 < m; i0 += 4 * kW) {
+            if (i0 + kW >= m) {  // this warp's last candidate alone: 16 row loads in flight per lane
+                const double* xr = p.rows64 + static_cast<size_t>(sel_slot[i0]) * p.dim;
+                double a = 0.0;
+                int64_t t = lane;
+                for (; t + 32 * 15 < p.dim; t += 32 * 16) {
+                    double xv[16], qv[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        xv[u] = __ldg(xr + t + 32 * u);
+                        qv[u] = __ldg(q + t + 32 * u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) a = fma(xv[u], qv[u], a);
+                }
+                for (; t + 32 * 7 < p.dim; t += 32 * 8) {
+                    double xv[8], qv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        xv[u] = __ldg(xr + t + 32 * u);
+                        qv[u] = __ldg(q + t + 32 * u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a = fma(xv[u], qv[u], a);
+                }
+                for (; t < p.dim; t += 32) a = fma(__ldg(xr + t), __ldg(q + t), a);
+                a = warp_sum64(a);
+                if (lane == 0) sel_sim[i0] = a + 0.0;
+                continue;
+            }
             const double* x[4];
             bool on[4];
 #pragma unroll
